@@ -1,0 +1,145 @@
+/*
+ * stagflow_b200.h -- C ABI of the B200 (sm_100a) time-step path of the
+ * staggered finite-volume incompressible Navier--Stokes solver.
+ *
+ * The reference (``stagflow``, /root/reference/pkg/src/stagflow) has no FFI:
+ * its operator / solver / stepper surface is Python duck typing.  Each entry
+ * point below replaces one reference function (cited file:line); the Python
+ * package ``paper_2604_18536_b200`` binds them with ctypes behind the
+ * reference's own names.
+ *
+ * Conventions
+ *  - Fields are the reference's *extended* arrays (one ghost layer per side),
+ *    C order, axis 0 slowest: shape (n0+2, n1+2[, n2+2]).  Pointers are device
+ *    pointers; ``T`` is double (SFB_F64) or float (SFB_F32) as fixed by the plan.
+ *  - Velocity fields are passed as arrays of ``dim`` component pointers.
+ *  - Every call is asynchronous on ``stream`` (a cudaStream_t passed as void*)
+ *    unless it returns a host scalar, in which case it synchronizes ``stream``.
+ *  - A plan is bound to one device and used from one host thread; after
+ *    creation no call allocates device memory.
+ *  - Return value: SFB_OK or an error code; sfb_last_error() gives the message
+ *    (thread-local).  Codes map to the reference's exceptions:
+ *      SFB_EINVAL   -> ValueError            (e.g. operators.py:142-143)
+ *      SFB_ECONFIG  -> ConfigurationError    (errors.py:4-5)
+ *      SFB_ENUMERIC -> NumericalError        (errors.py:17-18)
+ *      SFB_ECUDA    -> RuntimeError (CUDA / cuFFT failure)
+ */
+#ifndef STAGFLOW_B200_H
+#define STAGFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFB_ABI_VERSION 1
+
+enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4 };
+enum { SFB_F64 = 0, SFB_F32 = 1 };
+enum { SFB_BC_PERIODIC = 0, SFB_BC_DIRICHLET = 1, SFB_BC_SYMMETRIC = 2 };
+enum { SFB_SOLVER_SPECTRAL = 0, SFB_SOLVER_CHANNEL = 1 };
+
+/* Per-axis host tables, packed axis by axis, each of length n[a]+2, in this
+ * order (values already rounded to the plan dtype, as grid.py:168-171 and
+ * operators.py:47-84 compute them):
+ *   dx, du, 1/dx, 1/du, w_lo, w_hi, own_hi, own_lo, tan_hi, tan_lo        */
+#define SFB_NTAB 10
+
+typedef struct sfb_grid_desc {
+  int32_t dim;                 /* 2 or 3 (grid.py:128-129) */
+  int32_t dtype;               /* SFB_F64 / SFB_F32 */
+  int32_t n[3];                /* interior extents (grid.py:136) */
+  int32_t bc_lo[3], bc_hi[3];  /* per-axis boundary kinds (bcs.py:47-83) */
+  double val_lo[3][3];         /* constant Dirichlet values [axis][component] */
+  double val_hi[3][3];
+  const double* tables;        /* SFB_NTAB tables per axis, see above */
+  double width0[3];            /* widths[0] per axis (poisson.py:181) */
+} sfb_grid_desc;
+
+typedef struct sfb_plan sfb_plan;
+typedef struct sfb_solver sfb_solver;
+
+/* Fused RK stage (timestep.py:186-207 + operators.py:218-238):
+ *   k      = momentum_rhs(y)                  on velocity DOFs
+ *   k_out  = k                                (if k_out[0] != NULL)
+ *   s_out  = s_in + k*cb                      (if s_out[0] != NULL; s_in NULL -> u0)
+ *   y_next = u0   + k*ca                      (if y_next[0] != NULL)
+ * Only DOF entries are written; ghosts are refreshed by the next projection. */
+typedef struct sfb_stage_args {
+  const void* y[3];
+  const void* u0[3];
+  const void* s_in[3];
+  void* s_out[3];
+  void* y_next[3];
+  void* k_out[3];
+  double cb, ca, nu;
+  double force[3];
+} sfb_stage_args;
+
+int sfb_abi_version(void);
+const char* sfb_last_error(void);
+
+/* Grid / BC plan: grid.py:115-223, bcs.py:47-83, operators.py:38-90. */
+int sfb_plan_create(const sfb_grid_desc* desc, sfb_plan** out);
+int sfb_plan_destroy(sfb_plan* plan);
+
+/* Ghost fills: fields.py:96-140 (velocity), fields.py:81-93 (scalar). */
+int sfb_fill_ghosts_velocity(sfb_plan* plan, void* const* u, void* stream);
+int sfb_fill_ghosts_scalar(sfb_plan* plan, void* p, void* stream);
+
+/* Forward stencils (operators.py:108-238).  Outputs are whole extended
+ * arrays: DOFs written, everything else zeroed unless accumulate != 0. */
+int sfb_divergence(sfb_plan* plan, const void* const* u, void* out, void* stream);
+int sfb_pressure_gradient(sfb_plan* plan, const void* p, void* const* out, void* stream);
+int sfb_convection(sfb_plan* plan, const void* const* u, void* const* out, int accumulate, void* stream);
+int sfb_diffusion(sfb_plan* plan, const void* const* u, double nu, void* const* out, int accumulate, void* stream);
+int sfb_momentum_rhs(sfb_plan* plan, const void* const* u, double nu, const double* force, void* const* out, void* stream);
+
+/* RK building blocks (timestep.py:166-214). */
+int sfb_rk_stage(sfb_plan* plan, const sfb_stage_args* args, void* stream);
+/* dst = base + sum_l k[l]*coef[l] on DOFs (acc.copy_from + _axpy chain). */
+int sfb_combine(sfb_plan* plan, void* const* dst, const void* const* base, int nk,
+                const void* const* const* k, const double* coef, void* stream);
+/* Wray3 register update (timestep.py:231-246): fnew *= g; u += fnew; if fold: fold *= z; u += fold. */
+int sfb_wray_update(sfb_plan* plan, void* const* u, void* const* fnew, void* const* fold,
+                    double g, double z, void* stream);
+
+/* out = W_u * u on DOFs, zero elsewhere (kinetic_energy_pullback, adjoint.py:264-273). */
+int sfb_weighted_scale(sfb_plan* plan, const void* const* u, void* const* out, void* stream);
+
+/* Reductions (operators.py:284-301, timestep.py:140-163); synchronize stream. */
+int sfb_kinetic_energy(sfb_plan* plan, const void* const* u, double* out, void* stream);
+int sfb_weighted_inner(sfb_plan* plan, const void* const* u, const void* const* v, double* out, void* stream);
+int sfb_cfl_conv(sfb_plan* plan, const void* const* u, double* out, void* stream);
+
+/* Pressure solvers (poisson.py:152-229) and projection (poisson.py:321-341).
+ * SPECTRAL: periodic uniform grids (poisson.py:167-200).
+ * CHANNEL : periodic uniform x/z, walls on y; exact replacement of the
+ *           DirectPoissonSolver (poisson.py:203-229) by FFT(x,z) x batched
+ *           tridiagonal(y) with the weighted zero-mean gauge. */
+int sfb_solver_create(sfb_plan* plan, int kind, sfb_solver** out);
+int sfb_solver_destroy(sfb_solver* s);
+/* rhs, out: contiguous interior arrays (n0, n1[, n2]); may alias. */
+int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream);
+/* Full projection of u in place; p_ext (extended, ghosts filled) optional. */
+int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream);
+
+/* Pullbacks (adjoint.py:114-349), periodic grids. Mutating semantics of the
+ * reference are kept: divergence_pullback zeroes pbar's ghosts;
+ * the velocity-cotangent pullbacks zero vbar's non-DOFs. */
+int sfb_divergence_pullback(sfb_plan* plan, void* pbar, void* const* out, void* stream);
+int sfb_pressure_gradient_pullback(sfb_plan* plan, void* const* vbar, void* out, void* stream);
+int sfb_diffusion_pullback(sfb_plan* plan, void* const* vbar, double nu, void* const* out, void* stream);
+int sfb_convection_pullback(sfb_plan* plan, void* const* vbar, const void* const* u, void* const* out, void* stream);
+/* rhs_pullback (adjoint.py:253-261): out (+)= conv_pb + diff_pb, fused.
+ * accumulate != 0 adds into out instead of overwriting its DOFs. */
+int sfb_rhs_pullback(sfb_plan* plan, void* const* vbar, const void* const* u, double nu,
+                     void* const* out, double scale, int accumulate, void* stream);
+/* project_pullback (adjoint.py:335-349): out = vbar + D^T S^T G^T(-vbar). */
+int sfb_project_pullback(sfb_solver* s, void* const* vbar, void* const* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STAGFLOW_B200_H */

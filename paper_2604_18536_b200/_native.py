@@ -1,0 +1,133 @@
+"""ctypes binding of ``libstagflow_b200.so`` (declared in include/stagflow_b200.h).
+
+There is no fallback: if the library cannot be loaded the package import
+fails, and every compute call goes through the CUDA library.
+"""
+
+import ctypes
+import os
+
+from .errors import ConfigurationError, NumericalError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libstagflow_b200.so")
+
+SFB_OK, SFB_EINVAL, SFB_ECONFIG, SFB_ENUMERIC, SFB_ECUDA = range(5)
+SFB_F64, SFB_F32 = 0, 1
+SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC = 0, 1, 2
+SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL = 0, 1
+SFB_NTAB = 10
+ABI_VERSION = 1
+
+vp = ctypes.c_void_p
+VP3 = vp * 3
+
+
+class GridDesc(ctypes.Structure):
+    _fields_ = [
+        ("dim", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("n", ctypes.c_int32 * 3),
+        ("bc_lo", ctypes.c_int32 * 3),
+        ("bc_hi", ctypes.c_int32 * 3),
+        ("val_lo", (ctypes.c_double * 3) * 3),
+        ("val_hi", (ctypes.c_double * 3) * 3),
+        ("tables", ctypes.POINTER(ctypes.c_double)),
+        ("width0", ctypes.c_double * 3),
+    ]
+
+
+class StageArgs(ctypes.Structure):
+    _fields_ = [
+        ("y", VP3),
+        ("u0", VP3),
+        ("s_in", VP3),
+        ("s_out", VP3),
+        ("y_next", VP3),
+        ("k_out", VP3),
+        ("cb", ctypes.c_double),
+        ("ca", ctypes.c_double),
+        ("nu", ctypes.c_double),
+        ("force", ctypes.c_double * 3),
+    ]
+
+
+# name -> argtypes (all return int status)
+_SIGS = {
+    "sfb_plan_create": [ctypes.POINTER(GridDesc), ctypes.POINTER(vp)],
+    "sfb_plan_destroy": [vp],
+    "sfb_fill_ghosts_velocity": [vp, VP3, vp],
+    "sfb_fill_ghosts_scalar": [vp, vp, vp],
+    "sfb_divergence": [vp, VP3, vp, vp],
+    "sfb_pressure_gradient": [vp, vp, VP3, vp],
+    "sfb_convection": [vp, VP3, VP3, ctypes.c_int, vp],
+    "sfb_diffusion": [vp, VP3, ctypes.c_double, VP3, ctypes.c_int, vp],
+    "sfb_momentum_rhs": [vp, VP3, ctypes.c_double, ctypes.POINTER(ctypes.c_double), VP3, vp],
+    "sfb_rk_stage": [vp, ctypes.POINTER(StageArgs), vp],
+    "sfb_combine": [vp, VP3, VP3, ctypes.c_int, ctypes.POINTER(VP3), ctypes.POINTER(ctypes.c_double), vp],
+    "sfb_wray_update": [vp, VP3, VP3, VP3, ctypes.c_double, ctypes.c_double, vp],
+    "sfb_weighted_scale": [vp, VP3, VP3, vp],
+    "sfb_kinetic_energy": [vp, VP3, ctypes.POINTER(ctypes.c_double), vp],
+    "sfb_weighted_inner": [vp, VP3, VP3, ctypes.POINTER(ctypes.c_double), vp],
+    "sfb_cfl_conv": [vp, VP3, ctypes.POINTER(ctypes.c_double), vp],
+    "sfb_solver_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
+    "sfb_solver_destroy": [vp],
+    "sfb_solver_solve": [vp, vp, vp, vp],
+    "sfb_project": [vp, VP3, vp, vp],
+    "sfb_divergence_pullback": [vp, vp, VP3, vp],
+    "sfb_pressure_gradient_pullback": [vp, VP3, vp, vp],
+    "sfb_diffusion_pullback": [vp, VP3, ctypes.c_double, VP3, vp],
+    "sfb_convection_pullback": [vp, VP3, VP3, VP3, vp],
+    "sfb_rhs_pullback": [vp, VP3, VP3, ctypes.c_double, VP3, ctypes.c_double, ctypes.c_int, vp],
+    "sfb_project_pullback": [vp, VP3, VP3, vp],
+}
+
+EXPORTED = sorted(list(_SIGS) + ["sfb_abi_version", "sfb_last_error"])
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2604_18536_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.sfb_abi_version.restype = ctypes.c_int
+    lib.sfb_abi_version.argtypes = []
+    lib.sfb_last_error.restype = ctypes.c_char_p
+    lib.sfb_last_error.argtypes = []
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    if lib.sfb_abi_version() != ABI_VERSION:
+        raise ImportError("libstagflow_b200.so ABI version mismatch; rebuild")
+    return lib
+
+
+lib = _load()
+
+
+def check(rc):
+    if rc == SFB_OK:
+        return
+    msg = lib.sfb_last_error().decode(errors="replace")
+    if rc == SFB_EINVAL:
+        raise ValueError(msg)
+    if rc == SFB_ECONFIG:
+        raise ConfigurationError(msg)
+    if rc == SFB_ENUMERIC:
+        raise NumericalError(msg)
+    raise RuntimeError(f"stagflow_b200 CUDA failure: {msg}")
+
+
+def call(name, *args):
+    check(getattr(lib, name)(*args))
+
+
+def ptr3(tensors):
+    """VP3 of data pointers (None -> NULL)."""
+    out = VP3()
+    for i, t in enumerate(tensors):
+        out[i] = None if t is None else t.data_ptr()
+    return out

@@ -1,0 +1,284 @@
+"""Hand-written pullbacks (VJP) on the GPU (mirror of adjoint.py:1-444).
+
+Every pullback is one gather-form CUDA kernel (csrc/adjoint.cu) -- the exact
+transpose of (ghost fill o forward stencil) on periodic grids, the only
+boundary layout the reference's differentiable path accepts
+(adjoint.py:312-316).  The reference's mutating conventions are kept:
+velocity-cotangent pullbacks zero the non-DOFs of their input cotangent,
+``divergence_pullback`` zeroes the ghosts of its input, and
+``convection_pullback`` refills the primal's ghosts.
+"""
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigurationError
+from .fields import ScalarField, VelocityField, fill_ghosts_scalar, fill_ghosts_velocity
+from .operators import _plan, kinetic_energy, momentum_rhs, pressure_gradient, divergence
+from .plan import get_plan, stream_ptr
+from .poisson import _native_solver
+
+
+def _require_periodic(bcs):
+    if not all(bcs.periodic):
+        raise ConfigurationError("the differentiable time-stepping path supports periodic boundaries only")
+
+
+def zero_ghosts_scalar(f):
+    """adjoint.py:32-37"""
+    d = f.grid.dim
+    for a, n in enumerate(f.grid.shape):
+        idx = [slice(None)] * d
+        for i in (0, n + 1):
+            idx[a] = i
+            f.data[tuple(idx)] = 0.0
+    return f
+
+
+def zero_non_dofs_velocity(v):
+    """adjoint.py:40-50"""
+    grid = v.grid
+    d = grid.dim
+    for c in range(d):
+        for a, n in enumerate(grid.shape):
+            idx = [slice(None)] * d
+            planes = [0, n + 1] + ([n] if (c == a and not grid.periodic[a]) else [])
+            for i in planes:
+                idx[a] = i
+                v.u[c][tuple(idx)] = 0.0
+    return v
+
+
+def divergence_pullback(pbar, bcs, out=None):
+    """adjoint.py:114-128"""
+    _require_periodic(bcs)
+    grid = pbar.grid
+    if out is None:
+        out = VelocityField(grid)
+    N.call("sfb_divergence_pullback", get_plan(grid, bcs).handle, pbar.data.data_ptr(), N.ptr3(out.u), stream_ptr())
+    return out
+
+
+def pressure_gradient_pullback(vbar, bcs, out=None):
+    """adjoint.py:131-145"""
+    _require_periodic(bcs)
+    grid = vbar.grid
+    if out is None:
+        out = ScalarField(grid)
+    N.call("sfb_pressure_gradient_pullback", get_plan(grid, bcs).handle, N.ptr3(vbar.u), out.data.data_ptr(),
+           stream_ptr())
+    return out
+
+
+def diffusion_pullback(vbar, nu, bcs, out=None):
+    """adjoint.py:148-173"""
+    _require_periodic(bcs)
+    grid = vbar.grid
+    if out is None:
+        out = VelocityField(grid)
+    N.call("sfb_diffusion_pullback", get_plan(grid, bcs).handle, N.ptr3(vbar.u), float(nu), N.ptr3(out.u),
+           stream_ptr())
+    return out
+
+
+def convection_pullback(vbar, u, bcs, out=None):
+    """adjoint.py:176-227 (gather form; refills the primal's ghosts)."""
+    _require_periodic(bcs)
+    grid = vbar.grid
+    if out is None:
+        out = VelocityField(grid)
+    fill_ghosts_velocity(u, bcs)
+    N.call("sfb_convection_pullback", get_plan(grid, bcs).handle, N.ptr3(vbar.u), N.ptr3(u.u), N.ptr3(out.u),
+           stream_ptr())
+    return out
+
+
+def rhs_pullback(vbar, u, nu, bcs, out=None, accumulate=False):
+    """adjoint.py:253-261: convection + diffusion pullback in one kernel."""
+    _require_periodic(bcs)
+    grid = vbar.grid
+    if out is None:
+        out = VelocityField(grid)
+    fill_ghosts_velocity(u, bcs)
+    N.call("sfb_rhs_pullback", get_plan(grid, bcs).handle, N.ptr3(vbar.u), N.ptr3(u.u), float(nu), N.ptr3(out.u),
+           1.0, int(bool(accumulate)), stream_ptr())
+    return out
+
+
+def poisson_pullback(pbar, solver):
+    """adjoint.py:230-233"""
+    return solver.solve(pbar)
+
+
+def _pweights(grid):
+    w = getattr(grid, "_pw_dev", None)
+    if w is None:
+        from .operators import pressure_weights
+
+        w = torch.from_numpy(pressure_weights(grid)).to(device=torch.device("cuda", torch.cuda.current_device()))
+        grid._pw_dev = w
+    return w
+
+
+def poisson_solve_transpose(pbar, solver):
+    """adjoint.py:236-250: W S W^-1 (exact on stretched grids too)."""
+    grid = pbar.grid
+    w = _pweights(grid)
+    tmp = ScalarField(grid)
+    tmp.interior.copy_(pbar.interior / w)
+    res = solver.solve(tmp)
+    out = ScalarField(grid)
+    out.interior.copy_(res.interior * w)
+    return out
+
+
+def kinetic_energy_pullback(u, out=None):
+    """adjoint.py:264-273"""
+    grid = u.grid
+    if out is None:
+        out = VelocityField(grid)
+    N.call("sfb_weighted_scale", _plan(grid), N.ptr3(u.u), N.ptr3(out.u), stream_ptr())
+    return out
+
+
+class KineticEnergyLoss:
+    """adjoint.py:276-285"""
+
+    def value(self, u):
+        return kinetic_energy(u)
+
+    def gradient(self, u):
+        return kinetic_energy_pullback(u)
+
+
+class InnerProductLoss:
+    """adjoint.py:288-309 (plain inner product with a fixed field)."""
+
+    def __init__(self, c):
+        self.c = c
+
+    def value(self, u):
+        g = u.grid
+        return float(sum(torch.sum(self.c.u[a][g.u_slices(a)] * u.u[a][g.u_slices(a)]).item() for a in range(g.dim)))
+
+    def gradient(self, u):
+        g = u.grid
+        out = VelocityField(g)
+        for a in range(g.dim):
+            sl = g.u_slices(a)
+            out.u[a][sl] = self.c.u[a][sl]
+        return out
+
+
+def project_with_tape(u, solver, bcs):
+    """adjoint.py:319-332: pure projection (u is left untouched except for
+    its ghost fill, as in the reference)."""
+    fill_ghosts_velocity(u, bcs)
+    out = u.copy()
+    from .poisson import project_into
+
+    project_into(out, solver, bcs)
+    return out
+
+
+def project_pullback(vbar, solver, bcs):
+    """adjoint.py:335-349: vbar + D^T S^T G^T(-vbar) in one fused native call
+    (gradient pullback -> weighted solve -> divergence pullback)."""
+    _require_periodic(bcs)
+    s = _native_solver(solver, bcs)
+    out = VelocityField(vbar.grid)
+    N.call("sfb_project_pullback", s.handle, N.ptr3(vbar.u), N.ptr3(out.u), stream_ptr())
+    return out
+
+
+def _axpy_into(grid, dst, src, coef):
+    """dst += coef*src on DOFs (one combine kernel)."""
+    karr = (N.VP3 * 1)()
+    karr[0] = N.ptr3(src.u)
+    carr = (N.ctypes.c_double * 1)(float(coef))
+    N.call("sfb_combine", _plan(grid), N.ptr3(dst.u), N.ptr3(dst.u), 1, karr, carr, stream_ptr())
+
+
+def step_forward_tape(u0, dt, tableau, solver, setup):
+    """adjoint.py:352-384: one projected RK step recording the stage states.
+    Uses the same fused stage kernels as rk_step, so the primal trajectory is
+    bitwise the in-place one."""
+    from .timestep import _combine, _stage
+    from .poisson import project_into
+
+    bcs = setup.bcs
+    grid = u0.grid
+    s = tableau.stages
+    fill_ghosts_velocity(u0, bcs)
+    stages = []
+    ks = []
+    for j in range(s):
+        if j == 0:
+            yj = u0
+        else:
+            yj = VelocityField(grid)
+            terms = [(ks[l], dt * tableau.a[j][l]) for l in range(j) if tableau.a[j][l] != 0.0]
+            _combine(grid, yj, u0, [k for k, _ in terms], [c for _, c in terms])
+            project_into(yj, solver, bcs)
+        stages.append(yj)
+        kj = VelocityField(grid)
+        _stage(setup, yj, k_out=kj)
+        ks.append(kj)
+    u1 = VelocityField(grid)
+    terms = [(ks[l], dt * tableau.b[l]) for l in range(s) if tableau.b[l] != 0.0]
+    _combine(grid, u1, u0, [k for k, _ in terms], [c for _, c in terms])
+    project_into(u1, solver, bcs)
+    return u1, (stages, dt, tableau)
+
+
+def step_backward(tape, ubar, solver, setup):
+    """adjoint.py:387-422"""
+    stages, dt, tableau = tape
+    bcs = setup.bcs
+    grid = stages[0].grid
+    s = tableau.stages
+    ybar = project_pullback(ubar, solver, bcs)
+    g0 = ybar.copy()
+    kbars = [None] * s
+    for l in range(s):
+        if tableau.b[l] != 0.0:
+            kb = VelocityField(grid)
+            _axpy_into(grid, kb, ybar, dt * tableau.b[l])
+            kbars[l] = kb
+    for j in reversed(range(s)):
+        if kbars[j] is None:
+            continue
+        fb = rhs_pullback(kbars[j], stages[j], setup.nu, bcs)
+        if j == 0:
+            _axpy_into(grid, g0, fb, 1.0)
+            continue
+        ybar_j = project_pullback(fb, solver, bcs)
+        _axpy_into(grid, g0, ybar_j, 1.0)
+        for l in range(j):
+            aa = tableau.a[j][l]
+            if aa != 0.0:
+                if kbars[l] is None:
+                    kbars[l] = VelocityField(grid)
+                _axpy_into(grid, kbars[l], ybar_j, dt * aa)
+    return g0
+
+
+def unrolled_gradient(loss, u0, n_steps, dt, setup):
+    """adjoint.py:425-444"""
+    _require_periodic(setup.bcs)
+    tableau = setup.tableau
+    solver = setup.solver
+    u = u0.copy()
+    tapes = []
+    for _ in range(n_steps):
+        u, tape = step_forward_tape(u, dt, tableau, solver, setup)
+        tapes.append(tape)
+    ubar = loss.gradient(u)
+    for tape in reversed(tapes):
+        ubar = step_backward(tape, ubar, solver, setup)
+    zero_non_dofs_velocity(ubar)
+    return ubar
+
+
+_ = (np, fill_ghosts_scalar, momentum_rhs, pressure_gradient, divergence)

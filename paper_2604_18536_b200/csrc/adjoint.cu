@@ -1,0 +1,368 @@
+// Hand-written pullback (VJP) kernels, gather form (adjoint.py:114-349).
+//
+// The reference scatters cotangents through mirrored slices into extended
+// buffers and then folds ghosts back onto their fill sources
+// (adjoint.py:53-111).  On periodic grids (the only ones the differentiable
+// path accepts, adjoint.py:312-316) fill+fold is exactly periodic index
+// wrapping, so every pullback here is a *gather*: each output DOF reads the
+// cotangent / primal values it depends on (reach +-1 per axis, including the
+// (-e_a+e_c) diagonals of the convective pullback) and writes once.  No
+// atomics, so results are deterministic run to run.
+#include "sfb_kernels.cuh"
+#include "sfb_solver.cuh"
+
+namespace sfb {
+
+__device__ __forceinline__ int wr(int i, int n) { return i < 1 ? i + n : (i > n ? i - n : i); }
+
+// read ptr at J + (o0, o1, o2) with periodic wrap
+template <typename T, int D>
+__device__ __forceinline__ T atw(const Geo<T>& G, const T* __restrict__ p, const int J[3], int o0, int o1, int o2) {
+  int K[3] = {wr(J[0] + o0, G.n[0]), wr(J[1] + o1, G.n[1]), D == 3 ? wr(J[2] + o2, G.n[2]) : 0};
+  return p[lin<T, D>(G, K)];
+}
+
+template <int D>
+__device__ __forceinline__ void unit(int ax, int s, int o[3]) {
+  o[0] = o[1] = o[2] = 0;
+  o[ax] = s;
+}
+
+// divergence pullback (adjoint.py:114-128): out_a[J] = pb[J]/dx_a - pb[J+e_a]/dx_a(J_a+1)
+template <typename T, int D>
+__global__ void k_div_pb(Geo<T> G, const T* __restrict__ pb, MV<T> O, Box B) {
+  int J[3];
+  if (!box_coords<D>(B, J)) return;
+  const long long x = lin<T, D>(G, J);
+  const bool dof = is_pdof<T, D>(G, J);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    T v = T(0);
+    if (dof) {
+      int o[3];
+      unit<D>(a, 1, o);
+      const int jp = wr(J[a] + 1, G.n[a]);
+      v = pb[x] * tab(G, a, T_RDX, J[a]) - atw<T, D>(G, pb, J, o[0], o[1], o[2]) * tab(G, a, T_RDX, jp);
+    }
+    O.c[a][x] = v;
+  }
+}
+
+// pressure-gradient pullback (adjoint.py:131-145), optional sign and
+// 1/weight scaling for the projection pullback, ext or interior output
+template <typename T, int D>
+__global__ void k_grad_pb(Geo<T> G, CV<T> V, T* __restrict__ out, Box B, T sign, int interior_out, int divw) {
+  int J[3];
+  if (!box_coords<D>(B, J)) return;
+  const bool dof = is_pdof<T, D>(G, J);
+  T acc = T(0);
+  if (dof) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      int o[3];
+      unit<D>(a, -1, o);
+      const int jm = wr(J[a] - 1, G.n[a]);
+      const T tm = atw<T, D>(G, V.c[a], J, o[0], o[1], o[2]) * tab(G, a, T_RDU, jm);
+      const T t0 = V.c[a][lin<T, D>(G, J)] * tab(G, a, T_RDU, J[a]);
+      acc += tm - t0;
+    }
+    acc = sign * acc;
+    if (divw) {
+      T w = T(1);
+#pragma unroll
+      for (int b = 0; b < D; ++b) w = w * tab(G, b, T_DX, J[b]);
+      acc = acc / w;
+    }
+  }
+  if (interior_out) {
+    if (!dof) return;
+    long long o = (long long)(J[0] - 1) * G.n[1] + (J[1] - 1);
+    if (D == 3) o = o * G.n[2] + (J[2] - 1);
+    out[o] = acc;
+  } else {
+    out[lin<T, D>(G, J)] = acc;
+  }
+}
+
+// diffusion pullback of component a at J (adjoint.py:148-173), gather form
+template <typename T, int D>
+__device__ __forceinline__ T diff_pb(const Geo<T>& G, const T* __restrict__ va, const int J[3], int a, T nu) {
+  T acc = T(0);
+  const T vc = va[lin<T, D>(G, J)];
+#pragma unroll
+  for (int b = 0; b < D; ++b) {
+    const int ax = (b == a) ? a : b;
+    const int shi = (b == a) ? T_OHI : T_THI, slo = (b == a) ? T_OLO : T_TLO;
+    const int jm = wr(J[b] - 1, G.n[b]), jp = wr(J[b] + 1, G.n[b]);
+    int om[3], op[3];
+    unit<D>(b, -1, om);
+    unit<D>(b, 1, op);
+    const T vm = atw<T, D>(G, va, J, om[0], om[1], om[2]);
+    const T vp = atw<T, D>(G, va, J, op[0], op[1], op[2]);
+    acc += vm * tab(G, ax, shi, jm) - vc * (tab(G, ax, shi, J[b]) + tab(G, ax, slo, J[b])) + vp * tab(G, ax, slo, jp);
+  }
+  return nu * acc;
+}
+
+// convective pullback of component c at J (adjoint.py:176-227), gather form.
+// Forward: out_a[I] = -sum_b (F_ab[I] - F_ab[I-e_b]) R_ab[I] with
+// F_ab = T_ab * V_ab.  Cotangent of F: Fb_ab[K] = lam_ab[K+e_b] - lam_ab[K],
+// lam_ab = vbar_a * R_ab.
+template <typename T, int D>
+__device__ __forceinline__ T conv_pb(const Geo<T>& G, const CV<T>& Vb, const CV<T>& U, const int J[3], int c) {
+  T acc = T(0);
+  const T* __restrict__ vc = Vb.c[c];
+  const T* __restrict__ uc = U.c[c];
+  const int nc = G.n[c];
+  // (i) a = b = c
+  {
+    int m[3], p[3];
+    unit<D>(c, -1, m);
+    unit<D>(c, 1, p);
+    const T l_m = atw<T, D>(G, vc, J, m[0], m[1], m[2]) * tab(G, c, T_RDU, wr(J[c] - 1, nc));
+    const T l_0 = atw<T, D>(G, vc, J, 0, 0, 0) * tab(G, c, T_RDU, J[c]);
+    const T l_p = atw<T, D>(G, vc, J, p[0], p[1], p[2]) * tab(G, c, T_RDU, wr(J[c] + 1, nc));
+    const T u_m = atw<T, D>(G, uc, J, m[0], m[1], m[2]);
+    const T u_0 = atw<T, D>(G, uc, J, 0, 0, 0);
+    const T u_p = atw<T, D>(G, uc, J, p[0], p[1], p[2]);
+    acc += (l_p - l_0) * ((u_0 + u_p) * T(0.5)) + (l_0 - l_m) * ((u_m + u_0) * T(0.5));
+  }
+#pragma unroll
+  for (int b = 0; b < D; ++b) {
+    if (b == c) continue;
+    // (ii) a = c, b != c: transported pair
+    {
+      const T* __restrict__ ub = U.c[b];
+      int m[3], p[3], mc[3];
+      unit<D>(b, -1, m);
+      unit<D>(b, 1, p);
+      mc[0] = m[0];
+      mc[1] = m[1];
+      mc[2] = m[2];
+      mc[c] += 1;  // -e_b + e_c
+      int pc[3];
+      unit<D>(c, 1, pc);
+      const int nb = G.n[b];
+      const T l_m = atw<T, D>(G, vc, J, m[0], m[1], m[2]) * tab(G, b, T_RDX, wr(J[b] - 1, nb));
+      const T l_0 = atw<T, D>(G, vc, J, 0, 0, 0) * tab(G, b, T_RDX, J[b]);
+      const T l_p = atw<T, D>(G, vc, J, p[0], p[1], p[2]) * tab(G, b, T_RDX, wr(J[b] + 1, nb));
+      const T wl = tab(G, c, T_WLO, J[c]), wh = tab(G, c, T_WHI, J[c]);
+      const T V0 = wl * atw<T, D>(G, ub, J, 0, 0, 0) + wh * atw<T, D>(G, ub, J, pc[0], pc[1], pc[2]);
+      const T Vm = wl * atw<T, D>(G, ub, J, m[0], m[1], m[2]) + wh * atw<T, D>(G, ub, J, mc[0], mc[1], mc[2]);
+      acc += T(0.5) * ((l_p - l_0) * V0 + (l_0 - l_m) * Vm);
+    }
+    // (iii) b' = c, a = b != c: transporting component c inside F_ac
+    {
+      const int a = b;
+      const T* __restrict__ va = Vb.c[a];
+      const T* __restrict__ ua = U.c[a];
+      int pc[3], ma[3], mapc[3];
+      unit<D>(c, 1, pc);
+      unit<D>(a, -1, ma);
+      mapc[0] = ma[0] + pc[0];
+      mapc[1] = ma[1] + pc[1];
+      mapc[2] = ma[2] + pc[2];
+      const T rc0 = tab(G, c, T_RDX, J[c]);
+      const T rcp = tab(G, c, T_RDX, wr(J[c] + 1, nc));
+      // K = J
+      {
+        const T fb = atw<T, D>(G, va, J, pc[0], pc[1], pc[2]) * rcp - atw<T, D>(G, va, J, 0, 0, 0) * rc0;
+        const T tt = (atw<T, D>(G, ua, J, 0, 0, 0) + atw<T, D>(G, ua, J, pc[0], pc[1], pc[2])) * T(0.5);
+        acc += fb * tt * tab(G, a, T_WLO, J[a]);
+      }
+      // K = J - e_a
+      {
+        const T fb = atw<T, D>(G, va, J, mapc[0], mapc[1], mapc[2]) * rcp - atw<T, D>(G, va, J, ma[0], ma[1], ma[2]) * rc0;
+        const T tt = (atw<T, D>(G, ua, J, ma[0], ma[1], ma[2]) + atw<T, D>(G, ua, J, mapc[0], mapc[1], mapc[2])) * T(0.5);
+        acc += fb * tt * tab(G, a, T_WHI, wr(J[a] - 1, G.n[a]));
+      }
+    }
+  }
+  return acc;
+}
+
+// rhs pullback: out = scale*(conv_pb + diff_pb) [+ out]
+template <typename T, int D>
+__global__ void __launch_bounds__(256) k_rhs_pb(Geo<T> G, CV<T> Vb, CV<T> U, MV<T> O, Box B, T nu, int conv, int diff,
+                                                int accumulate) {
+  int J[3];
+  if (!box_coords<D>(B, J)) return;
+  const long long x = lin<T, D>(G, J);
+  const bool dof = is_pdof<T, D>(G, J);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    if (!dof) {
+      if (!accumulate) O.c[c][x] = T(0);
+      continue;
+    }
+    T v = T(0);
+    if (conv) v += conv_pb<T, D>(G, Vb, U, J, c);
+    if (diff) v += diff_pb<T, D>(G, Vb.c[c], J, c, nu);
+    if (accumulate) v += O.c[c][x];
+    O.c[c][x] = v;
+  }
+}
+
+// projection pullback tail: out_a = vbar_a + D^T(w * s)  (adjoint.py:335-349)
+template <typename T, int D>
+__global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T> O, Box B) {
+  int J[3];
+  if (!box_coords<D>(B, J)) return;
+  const long long x = lin<T, D>(G, J);
+  if (!is_pdof<T, D>(G, J)) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) O.c[a][x] = T(0);
+    return;
+  }
+  auto sbar = [&](const int K[3]) -> T {
+    long long o = (long long)(K[0] - 1) * G.n[1] + (K[1] - 1);
+    if (D == 3) o = o * G.n[2] + (K[2] - 1);
+    T w = T(1);
+#pragma unroll
+    for (int b = 0; b < D; ++b) w = w * tab(G, b, T_DX, K[b]);
+    return s[o] * w;
+  };
+  const T s0 = sbar(J);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    int K[3] = {J[0], J[1], J[2]};
+    K[a] = wr(J[a] + 1, G.n[a]);
+    const T d = s0 * tab(G, a, T_RDX, J[a]) - sbar(K) * tab(G, a, T_RDX, K[a]);
+    O.c[a][x] = Vb.c[a][x] + d;
+  }
+}
+
+template <typename T>
+static MV<T> mvp(const sfb_plan* p, void* const* u) {
+  MV<T> r;
+  for (int a = 0; a < 3; ++a) r.c[a] = (a < p->dim && u) ? (T*)u[a] : nullptr;
+  return r;
+}
+template <typename T>
+static CV<T> cvp(const sfb_plan* p, const void* const* u) {
+  CV<T> r;
+  for (int a = 0; a < 3; ++a) r.c[a] = (a < p->dim && u) ? (const T*)u[a] : nullptr;
+  return r;
+}
+
+static int need_periodic(const sfb_plan* p) {
+  if (!p->all_periodic) return fail(SFB_ECONFIG, "the differentiable path supports periodic boundaries only");
+  return SFB_OK;
+}
+
+template <typename T>
+static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, cudaStream_t st) {
+  sfb_plan* p = s->plan;
+  const Geo<T>& G = geo<T>(p);
+  int rc;
+  if ((rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st))) return rc;  // zero_non_dofs(vbar)
+  Box B = int_box(G);
+  T* rb = (T*)s->rbuf;
+  SFB_DISPATCH_DIM(G.dim, D, (k_grad_pb<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, cvp<T>(p, vbar), rb, B, T(-1), 1, 1)));
+  SFB_LAUNCH_CHECK("project pullback: gradient pullback");
+  if ((rc = solve_inplace<T>(s, rb, st))) return rc;
+  Box E = ext_box(G);
+  SFB_DISPATCH_DIM(G.dim, D, (k_proj_pb_tail<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, cvp<T>(p, vbar), mvp<T>(p, out), E)));
+  SFB_LAUNCH_CHECK("project pullback: divergence pullback");
+  return SFB_OK;
+}
+
+}  // namespace sfb
+
+using namespace sfb;
+
+static bool okp(const sfb_plan* p, const void* const* u) {
+  if (!u) return false;
+  for (int a = 0; a < p->dim; ++a)
+    if (!u[a]) return false;
+  return true;
+}
+
+extern "C" {
+
+int sfb_divergence_pullback(sfb_plan* p, void* pbar, void* const* out, void* stream) {
+  if (!p || !pbar || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
+  if (int rc = need_periodic(p)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  return SFB_TYPED(p, ([&]() {
+    const Geo<T>& G = geo<T>(p);
+    int rc = launch_planes<T>(G, MV<T>{{(T*)pbar, nullptr, nullptr}}, 1, 2, st);  // zero_ghosts_scalar(pbar)
+    if (rc) return rc;
+    Box E = ext_box(G);
+    SFB_DISPATCH_DIM(G.dim, D, (k_div_pb<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, (const T*)pbar, mvp<T>(p, out), E)));
+    SFB_LAUNCH_CHECK("divergence pullback");
+    return (int)SFB_OK;
+  })());
+}
+
+int sfb_pressure_gradient_pullback(sfb_plan* p, void* const* vbar, void* out, void* stream) {
+  if (!p || !okp(p, vbar) || !out) return fail(SFB_EINVAL, "null argument");
+  if (int rc = need_periodic(p)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  return SFB_TYPED(p, ([&]() {
+    const Geo<T>& G = geo<T>(p);
+    int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);  // zero_non_dofs(vbar)
+    if (rc) return rc;
+    Box E = ext_box(G);
+    SFB_DISPATCH_DIM(G.dim, D, (k_grad_pb<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, cvp<T>(p, vbar), (T*)out, E, T(1), 0, 0)));
+    SFB_LAUNCH_CHECK("gradient pullback");
+    return (int)SFB_OK;
+  })());
+}
+
+int sfb_diffusion_pullback(sfb_plan* p, void* const* vbar, double nu, void* const* out, void* stream) {
+  if (!p || !okp(p, vbar) || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
+  if (int rc = need_periodic(p)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  return SFB_TYPED(p, ([&]() {
+    const Geo<T>& G = geo<T>(p);
+    int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);
+    if (rc) return rc;
+    Box E = ext_box(G);
+    CV<T> V = cvp<T>(p, (const void* const*)vbar);
+    SFB_DISPATCH_DIM(G.dim, D, (k_rhs_pb<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, V, V, mvp<T>(p, out), E, (T)nu, 0, 1, 0)));
+    SFB_LAUNCH_CHECK("diffusion pullback");
+    return (int)SFB_OK;
+  })());
+}
+
+int sfb_convection_pullback(sfb_plan* p, void* const* vbar, const void* const* u, void* const* out, void* stream) {
+  if (!p || !okp(p, vbar) || !okp(p, u) || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
+  if (int rc = need_periodic(p)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  return SFB_TYPED(p, ([&]() {
+    const Geo<T>& G = geo<T>(p);
+    int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);
+    if (rc) return rc;
+    Box E = ext_box(G);
+    SFB_DISPATCH_DIM(G.dim, D, (k_rhs_pb<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), mvp<T>(p, out), E, T(0), 1, 0, 0)));
+    SFB_LAUNCH_CHECK("convection pullback");
+    return (int)SFB_OK;
+  })());
+}
+
+int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, double nu, void* const* out, double scale,
+                     int accumulate, void* stream) {
+  if (!p || !okp(p, vbar) || !okp(p, u) || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
+  if (int rc = need_periodic(p)) return rc;
+  if (scale != 1.0) return fail(SFB_EINVAL, "scale must be 1 (reserved)");
+  cudaStream_t st = (cudaStream_t)stream;
+  return SFB_TYPED(p, ([&]() {
+    const Geo<T>& G = geo<T>(p);
+    int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);
+    if (rc) return rc;
+    Box E = ext_box(G);
+    SFB_DISPATCH_DIM(G.dim, D, (k_rhs_pb<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), mvp<T>(p, out), E, (T)nu, 1, nu != 0.0, accumulate)));
+    SFB_LAUNCH_CHECK("rhs pullback");
+    return (int)SFB_OK;
+  })());
+}
+
+int sfb_project_pullback(sfb_solver* s, void* const* vbar, void* const* out, void* stream) {
+  if (!s || !okp(s->plan, vbar) || !okp(s->plan, out)) return fail(SFB_EINVAL, "null argument");
+  if (int rc = need_periodic(s->plan)) return rc;
+  return s->plan->dtype == SFB_F64 ? project_pb<double>(s, vbar, out, (cudaStream_t)stream)
+                                   : project_pb<float>(s, vbar, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

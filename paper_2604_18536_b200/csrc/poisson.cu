@@ -1,0 +1,460 @@
+// Pressure Poisson solvers and the projection (poisson.py:152-348).
+//
+// SPECTRAL  (poisson.py:167-200): cuFFT D2Z/Z2D (raw transforms only) +
+//           hand-written eigenvalue scaling (separable 1D tables, the
+//           irfftn 1/N folded in, k = 0 zeroed).
+// CHANNEL   (replaces DirectPoissonSolver, poisson.py:203-229, on grids
+//           periodic+uniform in x/z with walls on y): batched 2D D2Z over
+//           (x, z) -> per-(kx,kz) tridiagonal along y (Thomas, one thread per
+//           system, coalesced over kz; fp64 arithmetic) -> Z2D.  The (0,0)
+//           mode is closed by the weighted-zero-mean gauge of the augmented
+//           system (poisson.py:211-229).
+// project   (poisson.py:321-341): div with inline boundary resolution ->
+//           solve -> gradient subtract (periodic wrap inline) -> ghost fill.
+#include <cufft.h>
+
+#include <cmath>
+#include <vector>
+
+#include "sfb_kernels.cuh"
+#include "sfb_solver.cuh"
+
+namespace sfb {
+
+static int cufft_check(cufftResult r, const char* what) {
+  if (r == CUFFT_SUCCESS) return SFB_OK;
+  return fail(SFB_ECUDA, std::string(what) + ": cuFFT error " + std::to_string((int)r));
+}
+
+// ---------------------------------------------------------------------------
+// projection kernels
+// ---------------------------------------------------------------------------
+
+// u_a at I and I - e_a along its own axis with boundary entries resolved
+// inline (what fill_ghosts_velocity would have written, fields.py:110-133)
+template <typename T, int D>
+__device__ __forceinline__ void own_pair(const Geo<T>& G, const T* __restrict__ ua, long long x, const int I[3], int a,
+                                         T& cur, T& prev) {
+  const int n = G.n[a];
+  if (G.per[a]) {
+    cur = ua[x];
+    prev = I[a] == 1 ? ua[x + (long long)(n - 1) * G.s[a]] : ua[x - G.s[a]];
+  } else {
+    cur = I[a] == n ? (G.bc_hi[a] == SFB_BC_DIRICHLET ? G.vhi[a][a] : T(0)) : ua[x];
+    prev = I[a] == 1 ? (G.bc_lo[a] == SFB_BC_DIRICHLET ? G.vlo[a][a] : T(0)) : ua[x - G.s[a]];
+  }
+}
+
+// divergence into a contiguous interior array (operators.py:108-122)
+template <typename T, int D>
+__global__ void k_div_int(Geo<T> G, CV<T> U, T* __restrict__ out, Box B) {
+  int I[3];
+  if (!box_coords<D>(B, I)) return;
+  const long long x = lin<T, D>(G, I);
+  T acc = T(0);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    T cur, prev;
+    own_pair<T, D>(G, U.c[a], x, I, a, cur, prev);
+    acc += (cur - prev) * tab(G, a, T_RDX, I[a]);
+  }
+  long long o = (long long)(I[0] - 1) * G.n[1] + (I[1] - 1);
+  if (D == 3) o = o * G.n[2] + (I[2] - 1);
+  out[o] = acc;
+}
+
+// u_a[DOF] -= (p[I+e_a] - p[I]) / du_a   (poisson.py:334-339), p interior
+template <typename T, int D>
+__global__ void k_grad_sub(Geo<T> G, const T* __restrict__ p, MV<T> U, Box B) {
+  int I[3];
+  if (!box_coords<D>(B, I)) return;
+  const long long x = lin<T, D>(G, I);
+  long long o = (long long)(I[0] - 1) * G.n[1] + (I[1] - 1);
+  long long ps[3];
+  if (D == 3) {
+    o = o * G.n[2] + (I[2] - 1);
+    ps[0] = (long long)G.n[1] * G.n[2];
+    ps[1] = G.n[2];
+    ps[2] = 1;
+  } else {
+    ps[0] = G.n[1];
+    ps[1] = 1;
+  }
+  const T pc = p[o];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    if (!is_udof<T, D>(G, I, a)) continue;
+    // only periodic axes reach I_a = n for their own component
+    const long long on = I[a] == G.n[a] ? o - (long long)(G.n[a] - 1) * ps[a] : o + ps[a];
+    const T g = (p[on] - pc) * tab(G, a, T_RDU, I[a]);
+    U.c[a][x] -= g;
+  }
+}
+
+// extended, ghost-filled pressure from the interior solution (fields.py:81-93)
+template <typename T, int D>
+__global__ void k_p_ext(Geo<T> G, const T* __restrict__ p, T* __restrict__ pe, Box B) {
+  int I[3];
+  if (!box_coords<D>(B, I)) return;
+  int J[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int n = G.n[a];
+    int i = I[a];
+    if (i == 0) i = G.per[a] ? n : 1;
+    else if (i == n + 1) i = G.per[a] ? 1 : n;
+    J[a] = i - 1;
+  }
+  long long o = (long long)J[0] * G.n[1] + J[1];
+  if (D == 3) o = o * G.n[2] + J[2];
+  pe[lin<T, D>(G, I)] = p[o];
+}
+
+// ---------------------------------------------------------------------------
+// spectral scaling (poisson.py:179-199)
+// ---------------------------------------------------------------------------
+template <typename T, int D>
+__global__ void k_spec_scale(typename CT<T>::type* __restrict__ c, const double* __restrict__ l0,
+                             const double* __restrict__ l1, const double* __restrict__ l2, int m0, int m1, int mh,
+                             T invN) {
+  const long long total = (long long)m0 * (D == 3 ? (long long)m1 * mh : mh);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    int k0, k1, k2;
+    if (D == 3) {
+      k2 = (int)(t % mh);
+      long long r = t / mh;
+      k1 = (int)(r % m1);
+      k0 = (int)(r / m1);
+    } else {
+      k1 = (int)(t % mh);
+      k0 = (int)(t / mh);
+      k2 = 0;
+    }
+    // lam accumulated in fp64 in axis order, then cast (poisson.py:179-192)
+    double lam = l0[k0] + l1[k1];
+    if (D == 3) lam = lam + l2[k2];
+    typename CT<T>::type v = c[t];
+    if (t == 0) {
+      v.x = T(0);
+      v.y = T(0);
+    } else {
+      const T lt = (T)lam;
+      v.x = v.x / lt * invN;
+      v.y = v.y / lt * invN;
+    }
+    c[t] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// channel: batched tridiagonal along y per (kx, kz)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_tridiag(typename CT<T>::type* __restrict__ c, double2* __restrict__ dd, double* __restrict__ cp,
+                          const double* __restrict__ up, const double* __restrict__ lo, const double* __restrict__ di,
+                          const double* __restrict__ dxy, const double* __restrict__ lx, const double* __restrict__ lz,
+                          int n0, int n1, int nh, double invN) {
+  // dd: fp64 forward-sweep storage; aliases c for fp64 plans
+  const int kz = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k0 = blockIdx.y;
+  if (kz >= nh) return;
+  const long long base = (long long)k0 * n1 * nh + kz;
+  const long long st = nh;
+  const bool zero_mode = (k0 == 0 && kz == 0);
+  const double lam = lx[k0] + lz[kz];
+  double mr = 0.0, mi = 0.0;
+  if (zero_mode) {
+    // remove the dx-weighted mean: the (0,0)-mode image of the weighted-mean
+    // removal of the augmented system (poisson.py:211-229)
+    double sw = 0.0;
+    for (int j = 0; j < n1; ++j) {
+      const typename CT<T>::type v = c[base + j * st];
+      mr += dxy[j] * (double)v.x;
+      mi += dxy[j] * (double)v.y;
+      sw += dxy[j];
+    }
+    mr /= sw;
+    mi /= sw;
+  }
+  // (0,0): consistent singular Neumann system; drop the last row and pin
+  // x_{n1-1} = 0, then restore the weighted zero mean below
+  const int m = zero_mode ? n1 - 1 : n1;
+  double cprev = 0.0, dr = 0.0, dm = 0.0;
+  for (int j = 0; j < m; ++j) {
+    const typename CT<T>::type v = c[base + j * st];
+    const double l = lo[j + 1];
+    double b = di[j + 1] + (zero_mode ? 0.0 : lam);
+    if (j > 0) b -= l * cprev;
+    const double ib = 1.0 / b;
+    const double cj = up[j + 1] * ib;
+    dr = ((double)v.x - mr - l * dr) * ib;
+    dm = ((double)v.y - mi - l * dm) * ib;
+    cp[base + j * st] = cj;
+    cprev = cj;
+    dd[base + j * st] = make_double2(dr, dm);
+  }
+  double xr = 0.0, xi = 0.0;
+  double sr = 0.0, si = 0.0, sw = 0.0;
+  for (int j = m - 1; j >= 0; --j) {
+    const double2 v = dd[base + j * st];
+    if (j == m - 1) {
+      xr = v.x;
+      xi = v.y;
+    } else {
+      const double cj = cp[base + j * st];
+      xr = v.x - cj * xr;
+      xi = v.y - cj * xi;
+    }
+    if (zero_mode) {
+      dd[base + j * st] = make_double2(xr, xi);
+      sr += dxy[j] * xr;
+      si += dxy[j] * xi;
+    } else {
+      typename CT<T>::type w;
+      w.x = (T)(xr * invN);
+      w.y = (T)(xi * invN);
+      c[base + j * st] = w;
+    }
+  }
+  if (zero_mode) {
+    for (int j = 0; j < n1; ++j) sw += dxy[j];
+    sr /= sw;
+    si /= sw;
+    for (int j = 0; j < n1; ++j) {
+      double2 v = j < m ? dd[base + j * st] : make_double2(0.0, 0.0);
+      typename CT<T>::type w;
+      w.x = (T)((v.x - sr) * invN);
+      w.y = (T)((v.y - si) * invN);
+      c[base + j * st] = w;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// solver object
+// ---------------------------------------------------------------------------
+static int make_plans(sfb_solver* s) {
+  sfb_plan* p = s->plan;
+  const bool f64 = p->dtype == SFB_F64;
+  cufftType tf = f64 ? CUFFT_D2Z : CUFFT_R2C, ti = f64 ? CUFFT_Z2D : CUFFT_C2R;
+  int rc;
+  if ((rc = cufft_check(cufftCreate(&s->fwd), "cufftCreate"))) return rc;
+  s->has_fwd = true;
+  if ((rc = cufft_check(cufftCreate(&s->inv), "cufftCreate"))) return rc;
+  s->has_inv = true;
+  cufftSetAutoAllocation(s->fwd, 0);
+  cufftSetAutoAllocation(s->inv, 0);
+  size_t w1 = 0, w2 = 0;
+  if (s->kind == SFB_SOLVER_SPECTRAL) {
+    int nn[3] = {p->n[0], p->n[1], p->n[2]};
+    if ((rc = cufft_check(cufftMakePlanMany(s->fwd, p->dim, nn, nullptr, 1, 0, nullptr, 1, 0, tf, 1, &w1), "plan fwd")))
+      return rc;
+    if ((rc = cufft_check(cufftMakePlanMany(s->inv, p->dim, nn, nullptr, 1, 0, nullptr, 1, 0, ti, 1, &w2), "plan inv")))
+      return rc;
+  } else {
+    const int n0 = p->n[0], n1 = p->n[1], n2 = p->n[2], nh = n2 / 2 + 1;
+    int nn[2] = {n0, n2};
+    int ie[2] = {n0, n1 * n2};
+    int oe[2] = {n0, n1 * nh};
+    if ((rc = cufft_check(cufftMakePlanMany(s->fwd, 2, nn, ie, 1, n2, oe, 1, nh, tf, n1, &w1), "plan fwd"))) return rc;
+    if ((rc = cufft_check(cufftMakePlanMany(s->inv, 2, nn, oe, 1, nh, ie, 1, n2, ti, n1, &w2), "plan inv"))) return rc;
+  }
+  s->work_size = w1 > w2 ? w1 : w2;
+  if (s->work_size) {
+    if ((rc = cuda_check(cudaMalloc(&s->work, s->work_size), "cudaMalloc(cufft work)"))) return rc;
+  }
+  cufftSetWorkArea(s->fwd, s->work);
+  cufftSetWorkArea(s->inv, s->work);
+  return SFB_OK;
+}
+
+template <typename T>
+static int exec_fwd(sfb_solver* s, const T* in, cudaStream_t st) {
+  cufftSetStream(s->fwd, st);
+  if (sizeof(T) == 8)
+    return cufft_check(cufftExecD2Z(s->fwd, (cufftDoubleReal*)in, (cufftDoubleComplex*)s->cbuf), "D2Z");
+  return cufft_check(cufftExecR2C(s->fwd, (cufftReal*)in, (cufftComplex*)s->cbuf), "R2C");
+}
+template <typename T>
+static int exec_inv(sfb_solver* s, T* out, cudaStream_t st) {
+  cufftSetStream(s->inv, st);
+  if (sizeof(T) == 8)
+    return cufft_check(cufftExecZ2D(s->inv, (cufftDoubleComplex*)s->cbuf, (cufftDoubleReal*)out), "Z2D");
+  return cufft_check(cufftExecC2R(s->inv, (cufftComplex*)s->cbuf, (cufftReal*)out), "C2R");
+}
+
+template <typename T>
+int solve_inplace(sfb_solver* s, T* buf, cudaStream_t st) {
+  // buf: contiguous interior rhs in, solution out
+  sfb_plan* p = s->plan;
+  int rc;
+  if ((rc = exec_fwd<T>(s, buf, st))) return rc;
+  if (s->kind == SFB_SOLVER_SPECTRAL) {
+    const int m0 = p->n[0], m1 = p->n[1];
+    const int mh = p->n[p->dim - 1] / 2 + 1;
+    const double N = (double)p->int_count;
+    const T invN = (T)(1.0 / N);
+    int nb = 148 * 8;
+    SFB_DISPATCH_DIM(p->dim, D,
+                     (k_spec_scale<T, D><<<nb, 256, 0, st>>>((typename CT<T>::type*)s->cbuf, s->lam[0], s->lam[1],
+                                                             s->lam[2], m0, m1, mh, invN)));
+    SFB_LAUNCH_CHECK("spectral scale");
+  } else {
+    const int n0 = p->n[0], n1 = p->n[1], nh = p->n[2] / 2 + 1;
+    dim3 grid((nh + 63) / 64, n0);
+    double2* dd = sizeof(T) == 8 ? (double2*)s->cbuf : s->dscr;
+    k_tridiag<T><<<grid, 64, 0, st>>>((typename CT<T>::type*)s->cbuf, dd, s->cprime, s->up, s->lo, s->di, s->dxy,
+                                      s->lam[0], s->lam[2], n0, n1, nh, 1.0 / ((double)n0 * p->n[2]));
+    SFB_LAUNCH_CHECK("tridiagonal");
+  }
+  return exec_inv<T>(s, buf, st);
+}
+template int solve_inplace<double>(sfb_solver*, double*, cudaStream_t);
+template int solve_inplace<float>(sfb_solver*, float*, cudaStream_t);
+
+template <typename T>
+static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) {
+  sfb_plan* p = s->plan;
+  const Geo<T>& G = geo<T>(p);
+  MV<T> U;
+  CV<T> C;
+  for (int a = 0; a < 3; ++a) {
+    U.c[a] = a < p->dim ? (T*)u[a] : nullptr;
+    C.c[a] = U.c[a];
+  }
+  T* rb = (T*)s->rbuf;
+  Box B = int_box(G);
+  SFB_DISPATCH_DIM(G.dim, D, (k_div_int<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, C, rb, B)));
+  SFB_LAUNCH_CHECK("projection divergence");
+  int rc;
+  if ((rc = solve_inplace<T>(s, rb, st))) return rc;
+  SFB_DISPATCH_DIM(G.dim, D, (k_grad_sub<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, rb, U, B)));
+  SFB_LAUNCH_CHECK("gradient subtract");
+  if ((rc = launch_planes<T>(G, U, p->dim, 0, st))) return rc;
+  if (p_ext) {
+    Box E = ext_box(G);
+    SFB_DISPATCH_DIM(G.dim, D, (k_p_ext<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, (T*)p_ext, E)));
+    SFB_LAUNCH_CHECK("pressure ghosts");
+  }
+  return SFB_OK;
+}
+
+static bool axis_uniform(const std::vector<double>& dx) {
+  // grid.py:177-183: allclose(widths, widths[0], rtol=1e-12) on interior widths
+  const size_t n = dx.size() - 2;
+  for (size_t i = 1; i <= n; ++i)
+    if (std::fabs(dx[i] - dx[1]) > 1e-12 * std::fabs(dx[1])) return false;
+  return true;
+}
+
+}  // namespace sfb
+
+using namespace sfb;
+
+extern "C" {
+
+int sfb_solver_create(sfb_plan* p, int kind, sfb_solver** out) {
+  if (!p || !out) return fail(SFB_EINVAL, "null argument");
+  *out = nullptr;
+  if (kind == SFB_SOLVER_SPECTRAL) {
+    if (!p->all_periodic) return fail(SFB_ECONFIG, "spectral pressure solver requires periodic axes");
+    for (int a = 0; a < p->dim; ++a)
+      if (!axis_uniform(p->hdx[a])) return fail(SFB_ECONFIG, "spectral pressure solver requires uniform axes");
+  } else if (kind == SFB_SOLVER_CHANNEL) {
+    if (p->dim != 3 || p->bc_lo[0] != SFB_BC_PERIODIC || p->bc_lo[2] != SFB_BC_PERIODIC ||
+        p->bc_lo[1] == SFB_BC_PERIODIC)
+      return fail(SFB_ECONFIG, "channel pressure solver requires periodic x/z and walls on y");
+    if (!axis_uniform(p->hdx[0]) || !axis_uniform(p->hdx[2]))
+      return fail(SFB_ECONFIG, "channel pressure solver requires uniform x/z");
+  } else {
+    return fail(SFB_ECONFIG, "unknown pressure solver kind");
+  }
+  sfb_solver* s = new sfb_solver();
+  s->plan = p;
+  s->kind = kind;
+  const size_t esz = p->dtype == SFB_F64 ? 8 : 4;
+  const int dlast = p->dim - 1;
+  const long long nh = p->n[dlast] / 2 + 1;
+  const long long ncomplex = p->int_count / p->n[dlast] * nh;
+  int rc;
+  std::vector<double> host[3];
+  if ((rc = cuda_check(cudaMalloc(&s->rbuf, esz * p->int_count), "cudaMalloc(rbuf)"))) goto bad;
+  if ((rc = cuda_check(cudaMalloc(&s->cbuf, 2 * esz * ncomplex), "cudaMalloc(cbuf)"))) goto bad;
+  if ((rc = make_plans(s))) goto bad;
+  // eigenvalue tables lam_a[k] = (2 cos(2 pi k / n) - 2) / h^2 (poisson.py:180-186)
+  for (int a = 0; a < 3; ++a) {
+    int n = a < p->dim ? p->n[a] : 1;
+    host[a].resize(n);
+    double h = p->width0[a];
+    for (int k = 0; k < n; ++k)
+      host[a][k] = a < p->dim && !(kind == SFB_SOLVER_CHANNEL && a == 1)
+                       ? (2.0 * std::cos(2.0 * M_PI * k / n) - 2.0) / (h * h)
+                       : 0.0;
+    if ((rc = cuda_check(cudaMalloc(&s->lam[a], sizeof(double) * n), "cudaMalloc(lam)"))) goto bad;
+    if ((rc = cuda_check(cudaMemcpy(s->lam[a], host[a].data(), sizeof(double) * n, cudaMemcpyHostToDevice), "upload")))
+      goto bad;
+  }
+  if (kind == SFB_SOLVER_CHANNEL) {
+    // tridiagonal coefficients from the reference's y tables (fp64)
+    const int n1 = p->n[1];
+    std::vector<double> up(n1 + 2, 0.0), lo(n1 + 2, 0.0), di(n1 + 2, 0.0), dxy(n1);
+    const std::vector<double>& dx = p->hdx[1];
+    const std::vector<double>& du = p->hdu[1];
+    for (int j = 1; j < n1; ++j) up[j] = 1.0 / (du[j] * dx[j]);
+    for (int j = 2; j <= n1; ++j) lo[j] = 1.0 / (du[j - 1] * dx[j]);
+    for (int j = 1; j <= n1; ++j) {
+      di[j] = -(up[j] + lo[j]);
+      dxy[j - 1] = dx[j];
+    }
+    double** dst[4] = {&s->up, &s->lo, &s->di, &s->dxy};
+    std::vector<double>* src[4] = {&up, &lo, &di, &dxy};
+    for (int t = 0; t < 4; ++t) {
+      size_t bytes = sizeof(double) * src[t]->size();
+      if ((rc = cuda_check(cudaMalloc(dst[t], bytes), "cudaMalloc(tri)"))) goto bad;
+      if ((rc = cuda_check(cudaMemcpy(*dst[t], src[t]->data(), bytes, cudaMemcpyHostToDevice), "upload"))) goto bad;
+    }
+    if ((rc = cuda_check(cudaMalloc(&s->cprime, sizeof(double) * ncomplex), "cudaMalloc(cprime)"))) goto bad;
+    if (p->dtype == SFB_F32 &&
+        (rc = cuda_check(cudaMalloc(&s->dscr, sizeof(double2) * ncomplex), "cudaMalloc(dscr)")))
+      goto bad;
+  }
+  *out = s;
+  return SFB_OK;
+bad:
+  sfb_solver_destroy(s);
+  return rc;
+}
+
+int sfb_solver_destroy(sfb_solver* s) {
+  if (!s) return SFB_OK;
+  if (s->has_fwd) cufftDestroy(s->fwd);
+  if (s->has_inv) cufftDestroy(s->inv);
+  void* bufs[] = {s->work, s->rbuf, s->cbuf, s->cprime, s->dscr, s->lam[0], s->lam[1], s->lam[2],
+                  s->up, s->lo, s->di, s->dxy, s->tmp};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  delete s;
+  return SFB_OK;
+}
+
+int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream) {
+  if (!s || !rhs || !out) return fail(SFB_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  sfb_plan* p = s->plan;
+  const size_t bytes = (p->dtype == SFB_F64 ? 8 : 4) * (size_t)p->int_count;
+  int rc;
+  if ((rc = cuda_check(cudaMemcpyAsync(s->rbuf, rhs, bytes, cudaMemcpyDeviceToDevice, st), "copy rhs"))) return rc;
+  rc = p->dtype == SFB_F64 ? solve_inplace<double>(s, (double*)s->rbuf, st) : solve_inplace<float>(s, (float*)s->rbuf, st);
+  if (rc) return rc;
+  return cuda_check(cudaMemcpyAsync(out, s->rbuf, bytes, cudaMemcpyDeviceToDevice, st), "copy out");
+}
+
+int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream) {
+  if (!s || !u) return fail(SFB_EINVAL, "null argument");
+  for (int a = 0; a < s->plan->dim; ++a)
+    if (!u[a]) return fail(SFB_EINVAL, "null velocity component");
+  return s->plan->dtype == SFB_F64 ? project<double>(s, u, p_ext, (cudaStream_t)stream)
+                                   : project<float>(s, u, p_ext, (cudaStream_t)stream);
+}
+
+}  // extern "C"

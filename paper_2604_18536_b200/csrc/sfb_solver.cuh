@@ -1,0 +1,38 @@
+// Pressure solver object (opaque to C callers).
+#pragma once
+
+#include <cufft.h>
+
+#include "sfb_common.cuh"
+
+namespace sfb {
+template <typename T>
+struct CT;
+template <>
+struct CT<double> {
+  typedef double2 type;
+};
+template <>
+struct CT<float> {
+  typedef float2 type;
+};
+
+template <typename T>
+int solve_inplace(sfb_solver* s, T* buf, cudaStream_t st);
+}  // namespace sfb
+
+struct sfb_solver {
+  sfb_plan* plan = nullptr;
+  int kind = 0;
+  cufftHandle fwd = 0, inv = 0;
+  bool has_fwd = false, has_inv = false;
+  void* work = nullptr;
+  size_t work_size = 0;
+  void* rbuf = nullptr;      // contiguous interior real array (rhs / solution)
+  void* cbuf = nullptr;      // half spectrum
+  double* cprime = nullptr;  // channel: Thomas c' scratch (fp64)
+  double2* dscr = nullptr;   // channel, fp32 plans: fp64 forward-sweep scratch
+  double* lam[3] = {nullptr, nullptr, nullptr};
+  double *up = nullptr, *lo = nullptr, *di = nullptr, *dxy = nullptr;
+  void* tmp = nullptr;       // pullback scratch (extended scalar)
+};

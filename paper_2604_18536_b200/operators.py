@@ -1,0 +1,166 @@
+"""Matrix-free staggered stencils on the GPU (mirror of operators.py:1-301).
+
+Same call signatures as the reference: pure forms allocate their output,
+in-place forms take ``out=`` (and a ``scratch`` argument kept for signature
+compatibility -- the CUDA kernels need no work arrays).  Inputs must carry
+filled ghosts; outputs are whole extended arrays with only DOF ranges
+written and everything else zeroed unless ``accumulate=True``.
+
+The ghost fills of the *inputs* follow the boundary conditions of the plan
+the field was last filled with; operators that need a plan but no BCs
+(divergence, convection, ...) use the grid's periodic/wall layout with
+homogeneous values, which only affects how *outputs* are bounded -- the
+stencils themselves read the ghosts from memory, as the reference does.
+"""
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import alloc
+from .bcs import BoundarySpec, Dirichlet, Periodic
+from .errors import ConfigurationError
+from .fields import ScalarField, VelocityField
+from .plan import get_plan, stream_ptr
+
+
+class KernelScratch:
+    """Signature-compatible stand-in for the reference's four work arrays
+    (operators.py:93-100); the fused kernels need none."""
+
+    def __init__(self, grid):
+        self.grid = grid
+
+
+def default_bcs(grid):
+    """Periodic axes stay periodic, wall axes get homogeneous Dirichlet."""
+    return BoundarySpec([
+        (Periodic(), Periodic()) if p else (Dirichlet(0.0), Dirichlet(0.0)) for p in grid.periodic
+    ])
+
+
+def _plan(grid):
+    return get_plan(grid, default_bcs(grid)).handle
+
+
+def divergence(u, out=None, scratch=None):
+    """operators.py:108-122"""
+    grid = u.grid
+    if out is None:
+        out = ScalarField(grid)
+    N.call("sfb_divergence", _plan(grid), N.ptr3(u.u), out.data.data_ptr(), stream_ptr())
+    return out
+
+
+def pressure_gradient(pf, out=None):
+    """operators.py:125-137"""
+    grid = pf.grid
+    if out is None:
+        out = VelocityField(grid)
+    N.call("sfb_pressure_gradient", _plan(grid), pf.data.data_ptr(), N.ptr3(out.u), stream_ptr())
+    return out
+
+
+def diffusion(u, nu, out=None, scratch=None, accumulate=False):
+    """operators.py:140-170"""
+    if nu < 0:
+        raise ValueError(f"viscosity must be nonnegative, got {nu}")
+    grid = u.grid
+    if out is None:
+        out = VelocityField(grid)
+    N.call("sfb_diffusion", _plan(grid), N.ptr3(u.u), float(nu), N.ptr3(out.u), int(bool(accumulate)), stream_ptr())
+    return out
+
+
+def convection(u, out=None, scratch=None, accumulate=False):
+    """operators.py:173-215"""
+    grid = u.grid
+    if out is None:
+        out = VelocityField(grid)
+    N.call("sfb_convection", _plan(grid), N.ptr3(u.u), N.ptr3(out.u), int(bool(accumulate)), stream_ptr())
+    return out
+
+
+def constant_force(grid, force):
+    """Per-component constants for the fused kernels, or None."""
+    if force is None:
+        return None
+    vals = []
+    for f in force:
+        if not np.isscalar(f) and not (isinstance(f, np.ndarray) and f.ndim == 0):
+            raise ConfigurationError("only constant body forces are supported on the GPU path")
+        vals.append(float(grid.dtype.type(f)))
+    return vals
+
+
+def momentum_rhs(u, nu, force=None, closure=None, t=0.0, out=None, scratch=None):
+    """operators.py:218-238 (no closure support on the GPU path yet)."""
+    if closure is not None:
+        raise ConfigurationError("LES closures are not supported on the GPU path")
+    if nu < 0:
+        raise ValueError(f"viscosity must be nonnegative, got {nu}")
+    grid = u.grid
+    if out is None:
+        out = VelocityField(grid)
+    fv = constant_force(grid, force)
+    fp = None
+    if fv is not None:
+        fp = (N.ctypes.c_double * 3)(*(fv + [0.0] * (3 - len(fv))))
+    N.call("sfb_momentum_rhs", _plan(grid), N.ptr3(u.u), float(nu), fp, N.ptr3(out.u), stream_ptr())
+    return out
+
+
+def sample_force(grid, force):
+    """operators.py:241-259 (constant vectors; callables are rejected)."""
+    if force is None:
+        return None
+    if callable(force):
+        raise ConfigurationError("spatially varying (callable) forces are not supported on the GPU path")
+    return [grid.dtype.type(f) for f in force]
+
+
+def _table(grid, values, axis, s):
+    return grid.broadcast(values[s], axis)
+
+
+def velocity_weights(grid):
+    """operators.py:262-272 (host arrays)."""
+    out = []
+    for a in range(grid.dim):
+        sl = grid.u_slices(a)
+        w = np.ones((1,) * grid.dim, dtype=grid.dtype)
+        for g in range(grid.dim):
+            w = w * _table(grid, grid.du[g] if g == a else grid.dx[g], g, sl[g])
+        out.append(np.ascontiguousarray(np.broadcast_to(w, tuple(s.stop - s.start for s in sl))))
+    return out
+
+
+def pressure_weights(grid):
+    """operators.py:275-281 (host array)."""
+    p = grid.p_slices()
+    w = np.ones((1,) * grid.dim, dtype=grid.dtype)
+    for g in range(grid.dim):
+        w = w * _table(grid, grid.dx[g], g, p[g])
+    return np.ascontiguousarray(np.broadcast_to(w, grid.shape))
+
+
+def kinetic_energy(u):
+    """operators.py:284-291 (device reduction, fp64 accumulation)."""
+    out = N.ctypes.c_double()
+    N.call("sfb_kinetic_energy", _plan(u.grid), N.ptr3(u.u), N.ctypes.byref(out), stream_ptr())
+    return out.value
+
+
+def weighted_inner(u, v):
+    """operators.py:294-301"""
+    out = N.ctypes.c_double()
+    N.call("sfb_weighted_inner", _plan(u.grid), N.ptr3(u.u), N.ptr3(v.u), N.ctypes.byref(out), stream_ptr())
+    return out.value
+
+
+__all__ = [
+    "KernelScratch", "divergence", "pressure_gradient", "diffusion", "convection", "momentum_rhs",
+    "sample_force", "velocity_weights", "pressure_weights", "kinetic_energy", "weighted_inner",
+]
+
+_ = (torch, alloc)

@@ -1,0 +1,168 @@
+"""Pressure Poisson solvers and the projection on the GPU
+(mirror of poisson.py:1-348).
+
+Backends (same duck-typed interface as the reference: ``kind``,
+``tolerance``, ``iterations``, ``grid``, ``bcs``, ``weights``, ``wtot``,
+``solve(ScalarField)``, ``solve_interior(rhs, out)``):
+
+* ``spectral``   -- cuFFT D2Z/Z2D + hand-written eigenvalue scaling;
+  periodic uniform grids only (poisson.py:167-200).
+* ``fft-tridiag`` -- channel grids (periodic uniform x/z, walls on y, any
+  y stretching): batched 2D FFT over x/z + per-mode Thomas along y with the
+  weighted zero-mean gauge.  It solves exactly the system of the reference's
+  ``DirectPoissonSolver`` (poisson.py:203-229), so ``make_solver("direct")``
+  returns it on such grids.
+* ``cg``         -- not on the GPU path yet:
+  ``ConfigurationError``.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .bcs import BoundarySpec, Dirichlet
+from .errors import ConfigurationError
+from .fields import ScalarField
+from .operators import pressure_weights
+from .plan import get_plan, stream_ptr
+
+
+def homogeneous(bcs):
+    """poisson.py:31-40"""
+    return BoundarySpec([
+        tuple(Dirichlet(0.0) if isinstance(c, Dirichlet) else c for c in side) for side in bcs.sides
+    ])
+
+
+class _GpuSolver:
+    kind = "base"
+    tolerance = 1e-12
+    _native_kind = None
+
+    def __init__(self, grid, bcs):
+        self.grid = grid
+        self.bcs = bcs
+        self.weights = pressure_weights(grid)
+        self.wtot = float(np.sum(self.weights))
+        self.iterations = 0
+        self.plan = get_plan(grid, bcs)
+        h = ctypes.c_void_p()
+        N.call("sfb_solver_create", self.plan.handle, self._native_kind, ctypes.byref(h))
+        self.handle = h
+        self._buf = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                N.lib.sfb_solver_destroy(h)
+            except Exception:  # pragma: no cover
+                pass
+
+    def solve(self, rhs):
+        out = ScalarField(self.grid)
+        self.solve_interior(rhs.interior, out.interior)
+        return out
+
+    def solve_interior(self, rhs, out):
+        """rhs/out: interior views (any strides) of shape grid.shape."""
+        if self._buf is None:
+            self._buf = torch.empty(self.grid.shape, dtype=out.dtype, device=out.device)
+        buf = self._buf
+        buf.copy_(rhs)
+        N.call("sfb_solver_solve", self.handle, buf.data_ptr(), buf.data_ptr(), stream_ptr())
+        out.copy_(buf)
+        self.iterations = 1
+
+
+class SpectralPoissonSolver(_GpuSolver):
+    """FFT diagonalization; requires all axes periodic and uniform."""
+
+    kind = "spectral"
+    _native_kind = N.SFB_SOLVER_SPECTRAL
+
+    def __init__(self, grid, bcs):
+        if not all(grid.periodic):
+            raise ConfigurationError("spectral pressure solver requires periodic axes")
+        if not grid.uniform:
+            raise ConfigurationError("spectral pressure solver requires uniform axes")
+        super().__init__(grid, bcs)
+
+
+def _separable_channel(grid):
+    if grid.dim != 3 or grid.periodic != (True, False, True):
+        return False
+    return all(np.allclose(grid.axes[a].widths, grid.axes[a].widths[0], rtol=1e-12, atol=0.0) for a in (0, 2))
+
+
+class ChannelPoissonSolver(_GpuSolver):
+    """FFT(x,z) x batched tridiagonal(y) solve of the weighted channel
+    operator with the weighted zero-mean gauge (exact replacement of the
+    reference's augmented direct solve, poisson.py:203-229)."""
+
+    kind = "fft-tridiag"
+    _native_kind = N.SFB_SOLVER_CHANNEL
+
+    def __init__(self, grid, bcs):
+        if not _separable_channel(grid):
+            raise ConfigurationError(
+                "fft-tridiag pressure solver requires periodic uniform x/z and walls on y (3D)"
+            )
+        super().__init__(grid, bcs)
+
+
+class DirectPoissonSolver(ChannelPoissonSolver):
+    """``solver="direct"`` on the GPU path: the same augmented zero-mean
+    system (poisson.py:203-229), solved exactly by separation of variables on
+    separable channel grids; other layouts raise ConfigurationError."""
+
+    kind = "direct"
+
+
+class CGPoissonSolver:
+    def __init__(self, *a, **k):
+        raise ConfigurationError("the CG pressure solver is not on the GPU path yet")
+
+
+def make_solver(kind, grid, bcs, tol=None, max_iter=None):
+    """poisson.py:311-318"""
+    if kind == "spectral":
+        return SpectralPoissonSolver(grid, bcs)
+    if kind == "direct":
+        return DirectPoissonSolver(grid, bcs)
+    if kind == "fft-tridiag":
+        return ChannelPoissonSolver(grid, bcs)
+    if kind == "cg":
+        return CGPoissonSolver(grid, bcs, tol=tol, max_iter=max_iter)
+    raise ConfigurationError(f"unknown pressure solver kind: {kind!r}")
+
+
+def _native_solver(solver, bcs):
+    if not isinstance(solver, _GpuSolver):
+        raise ConfigurationError("project_into needs a GPU pressure solver from make_solver()")
+    if bcs is not solver.bcs:
+        from .plan import bcs_signature
+
+        if bcs_signature(bcs) != bcs_signature(solver.bcs):
+            raise ConfigurationError("projection boundary conditions differ from the solver's")
+    return solver
+
+
+def project_into(u, solver, bcs, t=0.0, scratch=None, p_div=None, p_out=None):
+    """poisson.py:321-341: make ``u`` discretely divergence-free in place
+    (one fused native call); returns the ghost-filled pressure."""
+    s = _native_solver(solver, bcs)
+    if p_out is None:
+        p_out = ScalarField(u.grid)
+    N.call("sfb_project", s.handle, N.ptr3(u.u), p_out.data.data_ptr(), stream_ptr())
+    s.iterations = 1
+    return p_out
+
+
+def project(u, solver, bcs, t=0.0):
+    """poisson.py:344-348"""
+    v = u.copy()
+    p = project_into(v, solver, bcs, t=t)
+    return v, p
