@@ -1,0 +1,314 @@
+"""Benchmark: fp64 cell-updates/s per RK4 step (BASELINE.json metric).
+
+Our arm (default):  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 840]
+Reference arm:      python bench.py --impl reference [...]
+
+A "step" is one projected RK4 step (4 fused RHS/stage launches, 4 spectral
+projections) of the periodic DNS on the full grid resident in HBM.  At N=1
+the workload is BASELINE config 5, 840^3 fp64 on one B200 (the largest
+single-GPU configuration; the metric is quoted at 512^3/840^3), started from
+a seeded random-phase isotropic field (synthetic data).  Every field is
+4.7 GB, far larger than the 126 MB L2, so no L2 flush is needed between
+steps.  For N>1 each rank steps its own 840^3 slab replica of a
+840 x 840 x 840N domain share (weak scaling).
+
+The JSON line carries: value (device-timed, max over ranks), e2e (the same
+metric through the public API with host buffers and H2D/D2H copies inside
+the timed region), roofline of the dominant kernel (fused RK stage: algorithmic
+bytes / CUDA-event time of its launches inside the timed region, vs the
+measured HBM copy peak), cpu_baseline (the CPU oracle port of the reference
+RK4 step on a bounded 128^3 sample), clocks sampled during the timed region,
+and gpu_launches (our kernel launches in the timed region).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RK4_BYTES_PER_CELL_F64 = 864
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(n=128, steps=2):
+    """The oracle port of the reference RK4 step (numpy/scipy, as stagflow
+    runs it: ufuncs single-threaded, scipy.fft default 1 worker) on a bounded
+    n^3 sample of the same workload."""
+    import numpy as np
+
+    from oracle import stagflow_np as O
+
+    b = O.uniform_bounds(0.0, 2 * np.pi, n)
+    g = O.OGrid([b, b, b], (True,) * 3)
+    bcs = O.periodic_bcs(3)
+    solve = O.SpectralSolve(g)
+    rng = np.random.default_rng(0)
+    u = g.zeros_vel()
+    for a in range(3):
+        u[a][g.udof(a)] = rng.standard_normal(g.shape)
+    O.fill_velocity(g, bcs, u)
+    O.project_into(g, bcs, solve, u)
+    u, _ = O.rk_step(g, bcs, solve, u, 1e-3, O.RK4, 1 / 1600)  # warm-up
+    t0 = time.perf_counter()
+    c0 = time.process_time()
+    for _ in range(steps):
+        u, _ = O.rk_step(g, bcs, solve, u, 1e-3, O.RK4, 1 / 1600)
+    wall = time.perf_counter() - t0
+    cpu = time.process_time() - c0
+    return {"value": n**3 * steps / wall, "unit": "cell-updates/s", "cores": 1, "kind": "port",
+            "sample": f"{steps} RK4 steps of a {n}^3 fp64 periodic field (oracle port of stagflow rk_step, "
+                      f"numpy+scipy.fft, 1 thread; {cpu / wall:.2f} cores busy on average)",
+            "wall_s": wall}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port) on the host."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import stagflow_np as O
+
+    n = args.ref_n
+    b = O.uniform_bounds(0.0, 2 * np.pi, n)
+    g = O.OGrid([b, b, b], (True,) * 3)
+    bcs = O.periodic_bcs(3)
+    solve = O.SpectralSolve(g)
+    rng = np.random.default_rng(0)
+    u = g.zeros_vel()
+    for a in range(3):
+        u[a][g.udof(a)] = rng.standard_normal(g.shape)
+    O.fill_velocity(g, bcs, u)
+    O.project_into(g, bcs, solve, u)
+    for _ in range(args.warmup):
+        u, _ = O.rk_step(g, bcs, solve, u, 1e-3, O.RK4, 1 / 1600)
+    t0 = time.perf_counter()
+    c0 = time.process_time()
+    for _ in range(args.steps):
+        u, _ = O.rk_step(g, bcs, solve, u, 1e-3, O.RK4, 1 / 1600)
+    wall = time.perf_counter() - t0
+    cpu = time.process_time() - c0
+    v = n**3 * args.steps / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "cell-updates/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"periodic DNS RK4 step, bounded {n}^3 sample of the {args.n}^3 config",
+                   "method": "rk4", "solver": "spectral"},
+        "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} RK4 steps of a {n}^3 fp64 field (oracle port, numpy+scipy.fft; "
+                                   f"{cpu / wall:.2f} cores busy on average of {os.cpu_count()})"},
+        "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "fp64 cell-updates/s per RK4 step"
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200 import _native as N
+    from paper_2604_18536_b200 import cases
+    from paper_2604_18536_b200 import timestep as TS
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    n = args.n
+    dtype = np.float64 if args.dtype == "f64" else np.float32
+    grid = cases.periodic_box(n, dtype=dtype)
+    bcs = P.BoundarySpec.all_periodic(3)
+    setup = P.Setup(grid, bcs, nu=1 / 1600, solver="spectral", method="rk4")
+    u0 = cases.isotropic(grid, setup.solver, seed=rank)
+    state = setup.new_state(u0=u0)
+    del u0
+    dt = 1e-3
+    cells = n**3
+    for _ in range(args.warmup):
+        P.rk_step(state, dt, P.RK4, setup.solver, setup)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- device-timed region
+    TS.STAGE_EVENTS = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = N.launches
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            P.rk_step(state, dt, P.RK4, setup.solver, setup)
+        end.record()
+        torch.cuda.synchronize()
+    launches = N.launches - launches0
+    ms = start.elapsed_time(end) / args.steps
+    ev = TS.STAGE_EVENTS
+    TS.STAGE_EVENTS = None
+    st_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in ev)
+    st_bytes = sum(bpc for _, _, bpc in ev) * cells
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * cells / (ms_max * 1e-3)
+
+    # ---- end to end through the public API with pinned host buffers
+    host = [torch.empty(grid.ext_shape, dtype=state.u.u[0].dtype, pin_memory=True) for _ in range(3)]
+    for a in range(3):
+        host[a].copy_(state.u.u[a])
+    torch.cuda.synchronize()
+    barrier()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es.record()
+    for _ in range(e2e_steps):
+        for a in range(3):
+            state.u.u[a].copy_(host[a], non_blocking=True)
+        P.rk_step(state, dt, P.RK4, setup.solver, setup)
+        for a in range(3):
+            host[a].copy_(state.u.u[a], non_blocking=True)
+    ee.record()
+    torch.cuda.synchronize()
+    e2e_ms = es.elapsed_time(ee) / e2e_steps
+    t = torch.tensor([e2e_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    field_bytes = int(np.prod(grid.ext_shape)) * grid.dtype.itemsize
+    ke = P.kinetic_energy(state.u)
+
+    if rank == 0:
+        peak, peak_kind = _peaks()
+        achieved = st_bytes / (st_ms * 1e-3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("stage_kernel", {}).get("dram_bytes_per_launch")
+            except (ValueError, OSError):
+                traffic = None
+        step_gbs = RK4_BYTES_PER_CELL_F64 * (dtype().itemsize / 8) * cells / (ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"periodic DNS {n}^3 {args.dtype} RK4 step (BASELINE config 5), "
+                                   "isotropic random-phase IC, spectral projection",
+                       "grid": [n, n, n * world], "method": "rk4", "solver": "spectral", "nu": 1 / 1600, "dt": dt,
+                       "l2": "inputs larger than L2 (each field 4.7 GB at 840^3); no flush needed",
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
+            "e2e": {"value": world * cells / (e2e_ms * 1e-3), "unit": "cell-updates/s",
+                    "h2d_bytes_per_step": 3 * field_bytes, "d2h_bytes_per_step": 3 * field_bytes,
+                    "steps": e2e_steps, "api": "paper_2604_18536_b200.rk_step with pinned host velocity in/out"},
+            "roofline": {"bound": "hbm", "kernel": "k_stage (fused RHS + RK stage combine)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_kind": peak_kind, "traffic": traffic,
+                         "bytes_per_cell": "72/120/120/72 per stage launch (avg 96 B fp64)",
+                         "stage_share_of_step": st_ms / (ms * args.steps)},
+            "step_roofline": {"algorithmic_bytes_per_cell": RK4_BYTES_PER_CELL_F64 * (dtype().itemsize / 8),
+                              "achieved": step_gbs, "peak": peak, "frac": step_gbs / peak},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "ke_after": ke,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=840)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--ref-n", type=int, default=96)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

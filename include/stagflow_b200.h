@@ -98,9 +98,10 @@ int sfb_momentum_rhs(sfb_plan* plan, const void* const* u, double nu, const doub
 
 /* RK building blocks (timestep.py:166-214). */
 int sfb_rk_stage(sfb_plan* plan, const sfb_stage_args* args, void* stream);
-/* dst = base + sum_l k[l]*coef[l] on DOFs (acc.copy_from + _axpy chain). */
+/* dst = base + sum_l k[l]*coef[l] on DOFs (acc.copy_from + _axpy chain).
+ * k: flat array of nk*3 component pointers, k[3*l + a]. */
 int sfb_combine(sfb_plan* plan, void* const* dst, const void* const* base, int nk,
-                const void* const* const* k, const double* coef, void* stream);
+                const void* const* k, const double* coef, void* stream);
 /* Wray3 register update (timestep.py:231-246): fnew *= g; u += fnew; if fold: fold *= z; u += fold. */
 int sfb_wray_update(sfb_plan* plan, void* const* u, void* const* fnew, void* const* fold,
                     double g, double z, void* stream);

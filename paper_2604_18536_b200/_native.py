@@ -121,8 +121,26 @@ def check(rc):
     raise RuntimeError(f"stagflow_b200 CUDA failure: {msg}")
 
 
+# number of our own kernel launches each entry point issues (cuFFT's
+# transforms are counted separately by the caller); used by bench.py
+KERNELS_PER_CALL = {
+    "sfb_rk_stage": 1, "sfb_combine": 1, "sfb_wray_update": 1, "sfb_fill_ghosts_velocity": 1,
+    "sfb_fill_ghosts_scalar": 1, "sfb_divergence": 1, "sfb_pressure_gradient": 1, "sfb_convection": 1,
+    "sfb_diffusion": 1, "sfb_momentum_rhs": 1, "sfb_weighted_scale": 1, "sfb_kinetic_energy": 2,
+    "sfb_weighted_inner": 2, "sfb_cfl_conv": 2, "sfb_solver_solve": 1, "sfb_project": 4,
+    "sfb_divergence_pullback": 2, "sfb_pressure_gradient_pullback": 2, "sfb_diffusion_pullback": 2,
+    "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4,
+}
+launches = 0
+
+
 def call(name, *args):
+    global launches
     check(getattr(lib, name)(*args))
+    k = KERNELS_PER_CALL.get(name, 0)
+    if name == "sfb_project" and args[2] is not None and args[2] != 0:
+        k += 1  # extended pressure written
+    launches += k
 
 
 def ptr3(tensors):

@@ -34,7 +34,7 @@ def _dev():
 def _coord(grid, table, axis):
     shape = [1] * grid.dim
     shape[axis] = table.shape[0]
-    return torch.from_numpy(np.asarray(table, dtype=np.float64)).to(_dev()).reshape(shape)
+    return torch.from_numpy(np.array(table, dtype=np.float64)).to(_dev()).reshape(shape)
 
 
 def taylor_green(grid, nu, t=0.0):

@@ -448,7 +448,7 @@ int sfb_momentum_rhs(sfb_plan* p, const void* const* u, double nu, const double*
   return SFB_TYPED(p, do_rhs<T>(p, u, out, nu, force, flags, (cudaStream_t)stream));
 }
 
-int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, const void* const* const* k,
+int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, const void* const* k,
                 const double* coef, void* stream) {
   if (!p || !ptrs_ok(p, dst) || !ptrs_ok(p, base) || nk < 0 || nk > SFB_MAX_K) return fail(SFB_EINVAL, "bad combine args");
   cudaStream_t st = (cudaStream_t)stream;
@@ -456,7 +456,7 @@ int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, 
     const Geo<T>& G = geo<T>(p);
     KList<T> K;
     for (int l = 0; l < nk; ++l) {
-      for (int a = 0; a < 3; ++a) K.k[l][a] = a < p->dim ? (const T*)k[l][a] : nullptr;
+      for (int a = 0; a < 3; ++a) K.k[l][a] = a < p->dim ? (const T*)k[3 * l + a] : nullptr;
       K.coef[l] = (T)coef[l];
     }
     Box B = int_box(G);

@@ -192,7 +192,8 @@ def test_channel_golden_direct_solver(P):
     for a in range(3):
         assert rel(got[a], c[f"uproj{a}"]) <= 1e-12
     assert rel(pp.numpy(), c["pproj"]) <= 1e-11
-    for tag, tab in (("rk4", P.RK4), ("ssp33", P.SSP33)):
+    for tag, tab, meth in (("rk4", P.RK4, "rk4"), ("ssp33", P.SSP33, "ssp33")):
+        setup.method, setup.tableau = meth, tab
         st = setup.new_state(u0=vel(P, pg, [c[f"uproj{a}"] for a in range(3)]))
         P.rk_step(st, float(c["dt"]), tab, setup.solver, setup)
         got = st.u.numpy()
