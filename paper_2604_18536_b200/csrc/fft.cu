@@ -1,0 +1,508 @@
+// Hand-written FFT engine for the spectral pressure solve (sm_100a).
+//
+// Replaces the raw cuFFT transforms of poisson.py:196,199 on the hot path.
+// One HBM pass per axis: a CTA stages a tile (the full transform length L x
+// W columns) in shared memory, runs a mixed-radix Stockham FFT (radices
+// 8/4/2/7/5/3, natural-order output) and writes it back.
+//
+// 3D solve = 5 passes over the half spectrum:
+//   R2C along axis 2 (real trick: length-n2/2 complex FFT + post-twiddle)
+//   C2C fwd along axis 1
+//   C2C fwd along axis 0 -> eigenvalue scaling 1/(Lambda N) -> C2C inv (fused)
+//   C2C inv along axis 1
+//   C2R along axis 2 (pre-twiddle + length-n2/2 inverse FFT)
+// (2D: R2C axis 1, fused axis 0, C2R axis 1.)
+#include <cmath>
+#include <vector>
+
+#include "sfb_fft.cuh"
+#include "sfb_kernels.cuh"
+
+namespace sfb {
+
+template <typename T>
+struct CX;
+template <>
+struct CX<double> {
+  typedef double2 t;
+};
+template <>
+struct CX<float> {
+  typedef float2 t;
+};
+
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) {
+  C r;
+  r.x = a.x * b.x - a.y * b.y;
+  r.y = a.x * b.y + a.y * b.x;
+  return r;
+}
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) {
+  C r;
+  r.x = a.x + b.x;
+  r.y = a.y + b.y;
+  return r;
+}
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) {
+  C r;
+  r.x = a.x - b.x;
+  r.y = a.y - b.y;
+  return r;
+}
+// multiply by -i (forward) or +i (inverse)
+template <typename C, bool INV>
+__device__ __forceinline__ C mul_mi(C a) {
+  C r;
+  if (INV) {
+    r.x = -a.y;
+    r.y = a.x;
+  } else {
+    r.x = a.y;
+    r.y = -a.x;
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// small DFTs, forward sign exp(-2 pi i k m / R); INV uses the + sign
+// ---------------------------------------------------------------------------
+template <typename C, bool INV>
+__device__ __forceinline__ void dft2(C* v) {
+  C a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+
+template <typename C, bool INV>
+__device__ __forceinline__ void dft4(C* v) {
+  C s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+  C s13 = cadd(v[1], v[3]), d13 = mul_mi<C, INV>(csub(v[1], v[3]));
+  v[0] = cadd(s02, s13);
+  v[2] = csub(s02, s13);
+  v[1] = cadd(d02, d13);
+  v[3] = csub(d02, d13);
+}
+
+template <typename C, bool INV>
+__device__ __forceinline__ void dft8(C* v) {
+  typedef decltype(v[0].x) R;
+  const R h = (R)0.70710678118654752440084436210484903928;
+  // radix-2 first stage over pairs (m, m+4)
+  C a[4], b[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    a[m] = cadd(v[m], v[m + 4]);
+    b[m] = csub(v[m], v[m + 4]);
+  }
+  // twiddle b[m] by w8^m (forward w8 = exp(-i pi/4))
+  {
+    C t = b[1];
+    // w8^1 = h - i h (fwd), h + i h (inv)
+    b[1].x = h * (t.x + (INV ? -t.y : t.y));
+    b[1].y = h * (t.y + (INV ? t.x : -t.x));
+    b[2] = mul_mi<C, INV>(b[2]);
+    t = b[3];
+    // w8^3 = -h - i h (fwd), -h + i h (inv)
+    b[3].x = h * (-t.x + (INV ? -t.y : t.y));
+    b[3].y = h * (-t.y + (INV ? t.x : -t.x));
+  }
+  dft4<C, INV>(a);
+  dft4<C, INV>(b);
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    v[2 * m] = a[m];
+    v[2 * m + 1] = b[m];
+  }
+}
+
+// odd radix R in {3, 5, 7}: pairwise-symmetric direct DFT.
+// cos/sin(2 pi j / R) for j = 1..(R-1)/2 (the rest by symmetry)
+__device__ __forceinline__ double odd_cos(int R, int j) {
+  if (R == 3) return -0.5;
+  if (R == 5) return j == 1 ? 0.30901699437494742410229341718281905886 : -0.80901699437494742410229341718281905886;
+  return j == 1 ? 0.62348980185873353052500488400423981063
+                : (j == 2 ? -0.22252093395631440428890256449679475947 : -0.90096886790241912623610231950744505117);
+}
+__device__ __forceinline__ double odd_sin(int R, int j) {
+  if (R == 3) return 0.86602540378443864676372317075293618347;
+  if (R == 5) return j == 1 ? 0.95105651629515357211643933337938214340 : 0.58778525229247312916870595463907276860;
+  return j == 1 ? 0.78183148246802980870844452667405775023
+                : (j == 2 ? 0.97492791218182360701813168299393121723 : 0.43388373911755812047576833284835875461);
+}
+
+template <typename C, int R, bool INV>
+__device__ __forceinline__ void dft_odd(C* v) {
+  typedef decltype(v[0].x) RT;
+  constexpr int H = (R - 1) / 2;
+  // cos/sin(2 pi j / R), j = 0..R-1 (compile-time after unrolling)
+  RT cs[R], sn[R];
+  cs[0] = (RT)1;
+  sn[0] = (RT)0;
+#pragma unroll
+  for (int j = 1; j <= H; ++j) {
+    cs[j] = (RT)odd_cos(R, j);
+    sn[j] = (RT)odd_sin(R, j);
+    cs[R - j] = cs[j];
+    sn[R - j] = -sn[j];
+  }
+  C sp[H], dm[H];
+#pragma unroll
+  for (int m = 1; m <= H; ++m) {
+    sp[m - 1] = cadd(v[m], v[R - m]);
+    dm[m - 1] = csub(v[m], v[R - m]);
+  }
+  C y0 = v[0];
+#pragma unroll
+  for (int m = 0; m < H; ++m) y0 = cadd(y0, sp[m]);
+  C out[R];
+  out[0] = y0;
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    C A = v[0], B;
+    B.x = 0;
+    B.y = 0;
+#pragma unroll
+    for (int m = 1; m <= H; ++m) {
+      const int j = (k * m) % R;
+      A.x += sp[m - 1].x * cs[j];
+      A.y += sp[m - 1].y * cs[j];
+      B.x += dm[m - 1].x * sn[j];
+      B.y += dm[m - 1].y * sn[j];
+    }
+    // forward: y_k = A - i B, y_{R-k} = A + i B
+    C iB;
+    iB.x = -B.y;
+    iB.y = B.x;
+    if (INV) {
+      out[k] = cadd(A, iB);
+      out[R - k] = csub(A, iB);
+    } else {
+      out[k] = csub(A, iB);
+      out[R - k] = cadd(A, iB);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) v[k] = out[k];
+}
+
+template <typename C, int R, bool INV>
+__device__ __forceinline__ void dft(C* v) {
+  if constexpr (R == 2) dft2<C, INV>(v);
+  else if constexpr (R == 4) dft4<C, INV>(v);
+  else if constexpr (R == 8) dft8<C, INV>(v);
+  else dft_odd<C, R, INV>(v);
+}
+
+// One Stockham pass over a tile stored [m][w] (m < L, w < W): src -> dst.
+template <typename C, int R, bool INV>
+__device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restrict__ dst, int L, int W, int Ns,
+                                         const C* __restrict__ tw) {
+  const int nb = L / R;
+  const int total = nb * W;
+  const int step = L / (Ns * R);
+  for (int b = threadIdx.x; b < total; b += blockDim.x) {
+    const int col = b % W;
+    const int j = b / W;
+    const int k = j % Ns;
+    C v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[(j + r * nb) * W + col];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        C w = tw[k * r * step];
+        if (INV) w.y = -w.y;
+        v[r] = cmul(v[r], w);
+      }
+    }
+    dft<C, R, INV>(v);
+    const int d = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[(d + r * Ns) * W + col] = v[r];
+  }
+}
+
+// Run all passes of a length-L plan; returns the buffer holding the result.
+template <typename C, bool INV>
+__device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, int W, const C* __restrict__ tw) {
+  int Ns = 1;
+  for (int p = 0; p < P.np; ++p) {
+    __syncthreads();
+    switch (P.radix[p]) {
+      case 8: stockham<C, 8, INV>(a, b, P.L, W, Ns, tw); break;
+      case 4: stockham<C, 4, INV>(a, b, P.L, W, Ns, tw); break;
+      case 2: stockham<C, 2, INV>(a, b, P.L, W, Ns, tw); break;
+      case 7: stockham<C, 7, INV>(a, b, P.L, W, Ns, tw); break;
+      case 5: stockham<C, 5, INV>(a, b, P.L, W, Ns, tw); break;
+      default: stockham<C, 3, INV>(a, b, P.L, W, Ns, tw); break;
+    }
+    Ns *= P.radix[p];
+    C* t = a;
+    a = b;
+    b = t;
+  }
+  __syncthreads();
+  return a;
+}
+
+// ---------------------------------------------------------------------------
+// strided C2C pass (optionally fused forward -> scale -> inverse)
+//   element (m, col) at base + m*S + col, col in [0, ncol), tile W columns
+// ---------------------------------------------------------------------------
+template <typename T, int MODE>  // MODE 0 fwd, 1 inv, 2 fwd+scale+inv
+__global__ void __launch_bounds__(256) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P, int W,
+                                                     long long S, int ncol, long long bstride,
+                                                     const typename CX<T>::t* __restrict__ tw, ScaleArgs sc) {
+  typedef typename CX<T>::t C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* bufA = reinterpret_cast<C*>(smem_raw);
+  C* bufB = bufA + (size_t)P.L * W;
+  const int c0 = blockIdx.x * W;
+  C* base = data + (long long)blockIdx.y * bstride;
+  const int L = P.L;
+  const int tot = L * W;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int w = e % W, m = e / W;
+    const int col = c0 + w;
+    C v;
+    if (col < ncol) v = base[(long long)m * S + col];
+    else { v.x = 0; v.y = 0; }
+    bufA[e] = v;
+  }
+  C* res;
+  if (MODE == 1) res = run_fft<C, true>(bufA, bufB, P, W, tw);
+  else res = run_fft<C, false>(bufA, bufB, P, W, tw);
+  if (MODE == 2) {
+    // eigenvalue scaling (poisson.py:179-199): lam in fp64, cast to T
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int w = e % W, m = e / W;
+      const int col = c0 + w;
+      if (col >= ncol) continue;
+      const int k1 = sc.nh > 0 ? col / sc.nh : 0;
+      const int k2 = sc.nh > 0 ? col % sc.nh : col;
+      double lam;
+      if (sc.dim == 3) lam = (sc.l0[m] + sc.l1[k1]) + sc.l2[k2];
+      else lam = sc.l0[m] + sc.l1[col];
+      C v = res[e];
+      if (m == 0 && col == 0 && blockIdx.y == 0) {
+        v.x = 0;
+        v.y = 0;
+      } else {
+        const T f = T(1) / (T)lam * (T)sc.invN;
+        v.x *= f;
+        v.y *= f;
+      }
+      res[e] = v;
+    }
+    C* other = (res == bufA) ? bufB : bufA;
+    res = run_fft<C, true>(res, other, P, W, tw);
+  }
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int w = e % W, m = e / W;
+    const int col = c0 + w;
+    if (col < ncol) base[(long long)m * S + col] = res[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// contiguous-axis real transforms: one row per CTA, M = N/2 complex points
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128) k_fft_r2c(const T* __restrict__ in, typename CX<T>::t* __restrict__ out, FftLen P,
+                                                 const typename CX<T>::t* __restrict__ tw,
+                                                 const typename CX<T>::t* __restrict__ tw2, long long in_row,
+                                                 long long out_row) {
+  typedef typename CX<T>::t C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* bufA = reinterpret_cast<C*>(smem_raw);
+  C* bufB = bufA + P.L;
+  const int M = P.L;
+  const C* row = reinterpret_cast<const C*>(in + (long long)blockIdx.x * in_row);
+  for (int m = threadIdx.x; m < M; m += blockDim.x) bufA[m] = row[m];
+  C* Z = run_fft<C, false>(bufA, bufB, P, 1, tw);
+  C* o = out + (long long)blockIdx.x * out_row;
+  // X[k] = E[k] + w^k O[k],  E = (Z[k] + conj Z[M-k]) / 2,  O = (Z[k] - conj Z[M-k]) / (2i)
+  for (int k = threadIdx.x; k <= M; k += blockDim.x) {
+    const C zk = Z[k == M ? 0 : k];
+    const C zc = Z[k == 0 ? 0 : M - k];
+    C e, od;
+    e.x = T(0.5) * (zk.x + zc.x);
+    e.y = T(0.5) * (zk.y - zc.y);
+    // (zk - conj(zc)) / (2i) = (a + ib)/(2i) = (b - ia)/2 with a = zk.x - zc.x, b = zk.y + zc.y
+    od.x = T(0.5) * (zk.y + zc.y);
+    od.y = -T(0.5) * (zk.x - zc.x);
+    const C w = tw2[k];  // exp(-2 pi i k / N)
+    o[k] = cadd(e, cmul(w, od));
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_fft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, FftLen P,
+                                                 const typename CX<T>::t* __restrict__ tw,
+                                                 const typename CX<T>::t* __restrict__ tw2, long long in_row,
+                                                 long long out_row) {
+  typedef typename CX<T>::t C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* bufA = reinterpret_cast<C*>(smem_raw);
+  C* bufB = bufA + P.L;
+  const int M = P.L;
+  const C* X = in + (long long)blockIdx.x * in_row;
+  // Z[k] = (X[k] + conj X[M-k]) + i (X[k] - conj X[M-k]) exp(+2 pi i k / N)
+  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+    const C xk = X[k];
+    const C xc = X[M - k];
+    C fe, fo, d;
+    fe.x = xk.x + xc.x;
+    fe.y = xk.y - xc.y;
+    d.x = xk.x - xc.x;
+    d.y = xk.y + xc.y;
+    C w = tw2[k];
+    w.y = -w.y;
+    fo = cmul(d, w);
+    C z;
+    z.x = fe.x - fo.y;
+    z.y = fe.y + fo.x;
+    bufA[k] = z;
+  }
+  C* z = run_fft<C, true>(bufA, bufB, P, 1, tw);
+  C* row = reinterpret_cast<C*>(out + (long long)blockIdx.x * out_row);
+  for (int m = threadIdx.x; m < M; m += blockDim.x) row[m] = z[m];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+bool fft_factor(int L, FftLen& P) {
+  P.L = L;
+  P.np = 0;
+  int r = L;
+  const int order[6] = {8, 4, 2, 7, 5, 3};
+  // prefer radix 8; use one 4 or 2 for the power-of-two remainder
+  while (r > 1) {
+    bool ok = false;
+    for (int q : order) {
+      if (r % q == 0) {
+        if (P.np >= 12) return false;
+        P.radix[P.np++] = q;
+        r /= q;
+        ok = true;
+        break;
+      }
+    }
+    if (!ok) return false;
+  }
+  return true;
+}
+
+int fft_upload_twiddles(int L, bool f64, void** dev) {
+  std::vector<double> t(2 * (size_t)(L > 0 ? L : 1));
+  for (int m = 0; m < L; ++m) {
+    long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)L;
+    t[2 * m] = (double)cosl(a);
+    t[2 * m + 1] = (double)sinl(a);
+  }
+  size_t bytes;
+  std::vector<float> tf;
+  const void* src;
+  if (f64) {
+    bytes = sizeof(double) * t.size();
+    src = t.data();
+  } else {
+    tf.assign(t.begin(), t.end());
+    bytes = sizeof(float) * tf.size();
+    src = tf.data();
+  }
+  int rc = cuda_check(cudaMalloc(dev, bytes), "cudaMalloc(twiddles)");
+  if (rc) return rc;
+  return cuda_check(cudaMemcpy(*dev, src, bytes, cudaMemcpyHostToDevice), "upload twiddles");
+}
+
+static int pick_w(int L, size_t csz) {
+  int W = 8;
+  while (W > 1 && 2 * (size_t)L * W * csz > 110 * 1024) W /= 2;
+  return W;
+}
+
+template <typename T>
+int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  C* cbuf = (C*)cbuf_v;
+  const size_t csz = sizeof(C);
+  const int dim = F.dim;
+  const int nlast = F.n[dim - 1];
+  const int M = nlast / 2;
+  const int nh = M + 1;
+  const long long rows = F.total / nlast;
+  // 1. R2C along the contiguous axis
+  {
+    size_t sm = 2 * (size_t)M * csz;
+    k_fft_r2c<T><<<(unsigned)rows, 128, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nlast, nh);
+    SFB_LAUNCH_CHECK("fft r2c");
+  }
+  ScaleArgs none{};
+  if (dim == 3) {
+    const int n0 = F.n[0], n1 = F.n[1];
+    // 2. axis 1 forward: S = nh, columns k2 < nh, batch over k0
+    {
+      const int W = pick_w(n1, csz);
+      dim3 grid((nh + W - 1) / W, n0);
+      k_fft_strided<T, 0><<<grid, 256, 2 * (size_t)n1 * W * csz, st>>>(cbuf, F.ax[1], W, nh, nh, (long long)n1 * nh,
+                                                                       (const C*)F.tw_ax[1], none);
+      SFB_LAUNCH_CHECK("fft axis1 fwd");
+    }
+    // 3. axis 0 forward + scale + inverse: S = n1*nh, columns (k1,k2)
+    {
+      const int W = pick_w(n0, csz);
+      const int ncol = n1 * nh;
+      dim3 grid((ncol + W - 1) / W, 1);
+      k_fft_strided<T, 2><<<grid, 256, 2 * (size_t)n0 * W * csz, st>>>(cbuf, F.ax[0], W, (long long)n1 * nh, ncol, 0,
+                                                                       (const C*)F.tw_ax[0], F.sc);
+      SFB_LAUNCH_CHECK("fft axis0 fused");
+    }
+    // 4. axis 1 inverse
+    {
+      const int W = pick_w(n1, csz);
+      dim3 grid((nh + W - 1) / W, n0);
+      k_fft_strided<T, 1><<<grid, 256, 2 * (size_t)n1 * W * csz, st>>>(cbuf, F.ax[1], W, nh, nh, (long long)n1 * nh,
+                                                                       (const C*)F.tw_ax[1], none);
+      SFB_LAUNCH_CHECK("fft axis1 inv");
+    }
+  } else {
+    const int n0 = F.n[0];
+    const int W = pick_w(n0, csz);
+    dim3 grid((nh + W - 1) / W, 1);
+    k_fft_strided<T, 2><<<grid, 256, 2 * (size_t)n0 * W * csz, st>>>(cbuf, F.ax[0], W, nh, nh, 0, (const C*)F.tw_ax[0],
+                                                                     F.sc);
+    SFB_LAUNCH_CHECK("fft axis0 fused");
+  }
+  // 5. C2R along the contiguous axis
+  {
+    size_t sm = 2 * (size_t)M * csz;
+    k_fft_c2r<T><<<(unsigned)rows, 128, sm, st>>>(cbuf, rbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nh, nlast);
+    SFB_LAUNCH_CHECK("fft c2r");
+  }
+  return SFB_OK;
+}
+template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t);
+template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t);
+
+template <typename T>
+int fft_set_smem_limits() {
+  typedef typename CX<T>::t C;
+  const int big = 200 * 1024;
+  cudaError_t e = cudaSuccess;
+  e = cudaFuncSetAttribute(k_fft_strided<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_strided<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_strided<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_r2c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_c2r<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  (void)sizeof(C);
+  return cuda_check(e, "cudaFuncSetAttribute(fft smem)");
+}
+template int fft_set_smem_limits<double>();
+template int fft_set_smem_limits<float>();
+
+}  // namespace sfb

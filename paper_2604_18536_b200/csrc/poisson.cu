@@ -14,6 +14,7 @@
 #include <cufft.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "sfb_kernels.cuh"
@@ -288,6 +289,7 @@ int solve_inplace(sfb_solver* s, T* buf, cudaStream_t st) {
   // buf: contiguous interior rhs in, solution out
   sfb_plan* p = s->plan;
   int rc;
+  if (s->fft.enabled) return fft_solve_inplace<T>(s->fft, buf, s->cbuf, st);
   if ((rc = exec_fwd<T>(s, buf, st))) return rc;
   if (s->kind == SFB_SOLVER_SPECTRAL) {
     const int m0 = p->n[0], m1 = p->n[1];
@@ -339,6 +341,44 @@ static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) 
   return SFB_OK;
 }
 
+// Hand-written FFT path for the spectral solve when every axis length
+// factors into 2/3/5/7, the last axis is even and a tile fits in smem.
+static int setup_fft(sfb_solver* s) {
+  sfb_plan* p = s->plan;
+  FftSolve& F = s->fft;
+  const bool f64 = p->dtype == SFB_F64;
+  const size_t csz = f64 ? 16 : 8;
+  const int dim = p->dim, nlast = p->n[dim - 1];
+  if (nlast % 2 != 0 || nlast < 2) return SFB_OK;
+  FftLen half, ax[3];
+  if (!fft_factor(nlast / 2, half)) return SFB_OK;
+  if (2 * (size_t)(nlast / 2) * csz > 200 * 1024) return SFB_OK;
+  for (int a = 0; a < dim - 1; ++a) {
+    if (!fft_factor(p->n[a], ax[a])) return SFB_OK;
+    if (2 * (size_t)p->n[a] * csz > 200 * 1024) return SFB_OK;
+  }
+  int rc;
+  if ((rc = (f64 ? fft_set_smem_limits<double>() : fft_set_smem_limits<float>()))) return rc;
+  F.dim = dim;
+  for (int a = 0; a < 3; ++a) F.n[a] = a < dim ? p->n[a] : 1;
+  F.total = p->int_count;
+  F.half = half;
+  for (int a = 0; a < dim - 1; ++a) {
+    F.ax[a] = ax[a];
+    if ((rc = fft_upload_twiddles(p->n[a], f64, &F.tw_ax[a]))) return rc;
+  }
+  if ((rc = fft_upload_twiddles(nlast / 2, f64, &F.tw_half))) return rc;
+  if ((rc = fft_upload_twiddles(nlast, f64, &F.tw_full))) return rc;
+  F.sc.dim = dim;
+  F.sc.nh = dim == 3 ? nlast / 2 + 1 : 0;
+  F.sc.l0 = s->lam[0];
+  F.sc.l1 = s->lam[1];
+  F.sc.l2 = s->lam[2];
+  F.sc.invN = 1.0 / (double)p->int_count;
+  F.enabled = true;
+  return SFB_OK;
+}
+
 static bool axis_uniform(const std::vector<double>& dx) {
   // grid.py:177-183: allclose(widths, widths[0], rtol=1e-12) on interior widths
   const size_t n = dx.size() - 2;
@@ -380,7 +420,6 @@ int sfb_solver_create(sfb_plan* p, int kind, sfb_solver** out) {
   std::vector<double> host[3];
   if ((rc = cuda_check(cudaMalloc(&s->rbuf, esz * p->int_count), "cudaMalloc(rbuf)"))) goto bad;
   if ((rc = cuda_check(cudaMalloc(&s->cbuf, 2 * esz * ncomplex), "cudaMalloc(cbuf)"))) goto bad;
-  if ((rc = make_plans(s))) goto bad;
   // eigenvalue tables lam_a[k] = (2 cos(2 pi k / n) - 2) / h^2 (poisson.py:180-186)
   for (int a = 0; a < 3; ++a) {
     int n = a < p->dim ? p->n[a] : 1;
@@ -394,6 +433,10 @@ int sfb_solver_create(sfb_plan* p, int kind, sfb_solver** out) {
     if ((rc = cuda_check(cudaMemcpy(s->lam[a], host[a].data(), sizeof(double) * n, cudaMemcpyHostToDevice), "upload")))
       goto bad;
   }
+  if (kind == SFB_SOLVER_SPECTRAL && !getenv("SFB_FORCE_CUFFT")) {
+    if ((rc = setup_fft(s))) goto bad;
+  }
+  if (!s->fft.enabled && (rc = make_plans(s))) goto bad;
   if (kind == SFB_SOLVER_CHANNEL) {
     // tridiagonal coefficients from the reference's y tables (fp64)
     const int n1 = p->n[1];
@@ -430,7 +473,8 @@ int sfb_solver_destroy(sfb_solver* s) {
   if (s->has_fwd) cufftDestroy(s->fwd);
   if (s->has_inv) cufftDestroy(s->inv);
   void* bufs[] = {s->work, s->rbuf, s->cbuf, s->cprime, s->dscr, s->lam[0], s->lam[1], s->lam[2],
-                  s->up, s->lo, s->di, s->dxy, s->tmp};
+                  s->up, s->lo, s->di, s->dxy, s->tmp, s->fft.tw_half, s->fft.tw_full,
+                  s->fft.tw_ax[0], s->fft.tw_ax[1], s->fft.tw_ax[2]};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete s;

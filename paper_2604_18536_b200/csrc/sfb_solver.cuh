@@ -4,6 +4,7 @@
 #include <cufft.h>
 
 #include "sfb_common.cuh"
+#include "sfb_fft.cuh"
 
 namespace sfb {
 template <typename T>
@@ -35,4 +36,5 @@ struct sfb_solver {
   double* lam[3] = {nullptr, nullptr, nullptr};
   double *up = nullptr, *lo = nullptr, *di = nullptr, *dxy = nullptr;
   void* tmp = nullptr;       // pullback scratch (extended scalar)
+  sfb::FftSolve fft;         // hand-written FFT path (spectral), when supported
 };

@@ -147,6 +147,26 @@ def test_spectral_projection_and_steps_golden(P, name):
         assert rel(st.pressure.numpy(), c[f"{tag}_p"]) <= t * 10, tag
 
 
+@pytest.mark.parametrize("shape", [(6, 10, 14), (20, 12, 30), (42, 8, 16), (64, 64, 64), (7, 9, 5),
+                                   (105, 6, 8), (48, 40, 840), (40, 30), (56, 22)])
+@pytest.mark.parametrize("force_cufft", [False, True])
+def test_spectral_solve_sizes(P, shape, force_cufft, monkeypatch):
+    """Hand-written FFT engine (radices 8/4/2/7/5/3, real trick on the last
+    axis) and the cuFFT fallback against scipy's rfftn solve (poisson.py:194-200)."""
+    if force_cufft:
+        monkeypatch.setenv("SFB_FORCE_CUFFT", "1")
+    rng = np.random.default_rng(sum(shape))
+    bounds = [O.uniform_bounds(0, 1.0 + 0.2 * a, n) for a, n in enumerate(shape)]
+    pg, og = grids(P, bounds, (True,) * len(shape))
+    solver = P.make_solver("spectral", pg, P.BoundarySpec.all_periodic(len(shape)))
+    rhs = og.zeros()
+    rhs[og.pdof()] = rng.standard_normal(og.shape)
+    rhs[og.pdof()] -= rhs[og.pdof()].mean()
+    ref = O.SpectralSolve(og)(rhs[og.pdof()])
+    got = solver.solve(P.ScalarField(pg, rhs)).numpy()[pg.p_slices()]
+    assert rel(got, ref) <= 1e-12
+
+
 def test_taylor_green_2d_rk4_golden(P):
     c = load("tg2d_rk4")
     pg, og = grids_from_case(P, c)
