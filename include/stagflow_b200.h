@@ -121,6 +121,8 @@ int sfb_cfl_conv(sfb_plan* plan, const void* const* u, double* out, void* stream
  *           tridiagonal(y) with the weighted zero-mean gauge. */
 int sfb_solver_create(sfb_plan* plan, int kind, sfb_solver** out);
 int sfb_solver_destroy(sfb_solver* s);
+/* 1 if the solver runs the hand-written FFT engine, 0 if it uses cuFFT. */
+int sfb_solver_uses_own_fft(const sfb_solver* s);
 /* rhs, out: contiguous interior arrays (n0, n1[, n2]); may alias. */
 int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream);
 /* Full projection of u in place; p_ext (extended, ghosts filled) optional. */

@@ -72,6 +72,7 @@ _SIGS = {
     "sfb_cfl_conv": [vp, VP3, ctypes.POINTER(ctypes.c_double), vp],
     "sfb_solver_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
     "sfb_solver_destroy": [vp],
+    "sfb_solver_uses_own_fft": [vp],
     "sfb_solver_solve": [vp, vp, vp, vp],
     "sfb_project": [vp, VP3, vp, vp],
     "sfb_divergence_pullback": [vp, vp, VP3, vp],
@@ -138,6 +139,9 @@ def call(name, *args):
     global launches
     check(getattr(lib, name)(*args))
     k = KERNELS_PER_CALL.get(name, 0)
+    if name in ("sfb_project", "sfb_project_pullback", "sfb_solver_solve"):
+        own = lib.sfb_solver_uses_own_fft(args[0])
+        k += (4 if own else 0) if name != "sfb_solver_solve" else (4 if own else 0)
     if name == "sfb_project" and args[2] is not None and args[2] != 0:
         k += 1  # extended pressure written
     launches += k

@@ -31,6 +31,22 @@ struct CX<float> {
   typedef float2 t;
 };
 
+// cp.async (LDGSTS) of one complex element into shared memory; pred=false
+// zero-fills.  All loads of a tile are issued back to back, then waited on.
+template <typename C>
+__device__ __forceinline__ void cp_async_elem(C* smem, const C* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? (int)sizeof(C) : 0;
+  if constexpr (sizeof(C) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 template <typename C>
 __device__ __forceinline__ C cmul(C a, C b) {
   C r;
@@ -213,7 +229,7 @@ __device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restric
     if (Ns > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        C w = tw[k * r * step];
+        C w = __ldg(tw + k * r * step);
         if (INV) w.y = -w.y;
         v[r] = cmul(v[r], w);
       }
@@ -253,7 +269,7 @@ __device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, int W, const 
 //   element (m, col) at base + m*S + col, col in [0, ncol), tile W columns
 // ---------------------------------------------------------------------------
 template <typename T, int MODE>  // MODE 0 fwd, 1 inv, 2 fwd+scale+inv
-__global__ void __launch_bounds__(256) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P, int W,
+__global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P, int W,
                                                      long long S, int ncol, long long bstride,
                                                      const typename CX<T>::t* __restrict__ tw, ScaleArgs sc) {
   typedef typename CX<T>::t C;
@@ -267,11 +283,10 @@ __global__ void __launch_bounds__(256) k_fft_strided(typename CX<T>::t* __restri
   for (int e = threadIdx.x; e < tot; e += blockDim.x) {
     const int w = e % W, m = e / W;
     const int col = c0 + w;
-    C v;
-    if (col < ncol) v = base[(long long)m * S + col];
-    else { v.x = 0; v.y = 0; }
-    bufA[e] = v;
+    const bool ok = col < ncol;
+    cp_async_elem(bufA + e, base + (ok ? (long long)m * S + col : 0), ok);
   }
+  cp_async_wait_all();
   C* res;
   if (MODE == 1) res = run_fft<C, true>(bufA, bufB, P, W, tw);
   else res = run_fft<C, false>(bufA, bufB, P, W, tw);
@@ -321,7 +336,8 @@ __global__ void __launch_bounds__(128) k_fft_r2c(const T* __restrict__ in, typen
   C* bufB = bufA + P.L;
   const int M = P.L;
   const C* row = reinterpret_cast<const C*>(in + (long long)blockIdx.x * in_row);
-  for (int m = threadIdx.x; m < M; m += blockDim.x) bufA[m] = row[m];
+  for (int m = threadIdx.x; m < M; m += blockDim.x) cp_async_elem(bufA + m, row + m, true);
+  cp_async_wait_all();
   C* Z = run_fft<C, false>(bufA, bufB, P, 1, tw);
   C* o = out + (long long)blockIdx.x * out_row;
   // X[k] = E[k] + w^k O[k],  E = (Z[k] + conj Z[M-k]) / 2,  O = (Z[k] - conj Z[M-k]) / (2i)
@@ -349,7 +365,11 @@ __global__ void __launch_bounds__(128) k_fft_c2r(const typename CX<T>::t* __rest
   C* bufA = reinterpret_cast<C*>(smem_raw);
   C* bufB = bufA + P.L;
   const int M = P.L;
-  const C* X = in + (long long)blockIdx.x * in_row;
+  const C* Xg = in + (long long)blockIdx.x * in_row;
+  C* X = bufB;  // staged row (M+1 values; the smem allocation has 2M+2)
+  for (int k = threadIdx.x; k <= M; k += blockDim.x) cp_async_elem(X + k, Xg + k, true);
+  cp_async_wait_all();
+  __syncthreads();
   // Z[k] = (X[k] + conj X[M-k]) + i (X[k] - conj X[M-k]) exp(+2 pi i k / N)
   for (int k = threadIdx.x; k < M; k += blockDim.x) {
     const C xk = X[k];
@@ -480,7 +500,7 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   }
   // 5. C2R along the contiguous axis
   {
-    size_t sm = 2 * (size_t)M * csz;
+    size_t sm = (2 * (size_t)M + 2) * csz;
     k_fft_c2r<T><<<(unsigned)rows, 128, sm, st>>>(cbuf, rbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nh, nlast);
     SFB_LAUNCH_CHECK("fft c2r");
   }

@@ -468,6 +468,8 @@ bad:
   return rc;
 }
 
+int sfb_solver_uses_own_fft(const sfb_solver* s) { return s && s->fft.enabled ? 1 : 0; }
+
 int sfb_solver_destroy(sfb_solver* s) {
   if (!s) return SFB_OK;
   if (s->has_fwd) cufftDestroy(s->fwd);

@@ -9,6 +9,8 @@
 // sum and the next stage state can be produced while k_j is still in
 // registers -- k_j is never stored.  Four velocity registers suffice
 // (u0, s, y, y_next), which is what lets 840^3 fp64 fit on one B200.
+#include <cstdlib>
+
 #include "sfb_kernels.cuh"
 
 namespace sfb {
@@ -40,8 +42,182 @@ __global__ void __launch_bounds__(256) k_stage_generic(Geo<T> G, StageArgs<T> A,
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3D marching kernel: a CTA owns a TJ x TK column tile of the (j, k) plane and
+// marches along axis 0 (the slowest, plane stride).  The three components of
+// the stage state y stream through a 4-slot shared-memory ring of planes
+// (i-1, i, i+1 in use, i+2 landing) filled with cp.async, each plane with a
+// one-cell halo in j and k; every y value is read from HBM once per CTA and
+// the stencil's 27 reads per cell come from shared memory.  u0 / s are read
+// and s / y_next written once, coalesced, at the centre.
+// ---------------------------------------------------------------------------
 template <typename T>
-int stage_fast_3d(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st);
+__device__ __forceinline__ void cp_async_val(T* smem, const T* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? (int)sizeof(T) : 0;
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int TJ, int TK>
+struct RingGeom {
+  static constexpr int PW = TK + 2, PH = TJ + 2, PS = PW * PH, NT = TJ * TK;
+};
+
+// momentum RHS of component A at the CTA's current cell from the smem ring
+// (same arithmetic and order as rhs_comp, sfb_kernels.cuh)
+template <typename T, int A, int TJ, int TK>
+__device__ __forceinline__ T rhs_ring(const Geo<T>& G, const T* const* pl, int c0, int i, int j, int k, bool diff, T nu,
+                                      T fa) {
+  typedef RingGeom<TJ, TK> RG;
+  // pl[d] = plane i-1+d base (component 0); component c at + c*PS; centre c0
+  auto Y = [&](int c, int di, int dj, int dk) -> T { return pl[1 + di][c * RG::PS + c0 + dj * RG::PW + dk]; };
+  const int Ic[3] = {i, j, k};
+  const T uc = Y(A, 0, 0, 0);
+  T up[3], um[3];
+  up[0] = Y(A, 1, 0, 0);
+  um[0] = Y(A, -1, 0, 0);
+  up[1] = Y(A, 0, 1, 0);
+  um[1] = Y(A, 0, -1, 0);
+  up[2] = Y(A, 0, 0, 1);
+  um[2] = Y(A, 0, 0, -1);
+  T v = T(0);
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const T tp = (uc + up[b]) * T(0.5);
+    const T tm = (um[b] + uc) * T(0.5);
+    T fl;
+    if (b == A) {
+      fl = (tp * tp - tm * tm) * tab(G, A, T_RDU, Ic[A]);
+    } else {
+      const T wl = tab(G, A, T_WLO, Ic[A]);
+      const T wh = tab(G, A, T_WHI, Ic[A]);
+      // offsets +e_A, -e_b, -e_b+e_A
+      const int eA0 = A == 0, eA1 = A == 1, eA2 = A == 2;
+      const int eb0 = b == 0, eb1 = b == 1, eb2 = b == 2;
+      const T vp = Y(b, 0, 0, 0) * wl + Y(b, eA0, eA1, eA2) * wh;
+      const T vm = Y(b, -eb0, -eb1, -eb2) * wl + Y(b, eA0 - eb0, eA1 - eb1, eA2 - eb2) * wh;
+      fl = (tp * vp - tm * vm) * tab(G, b, T_RDX, Ic[b]);
+    }
+    v -= fl;
+  }
+  if (diff) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      T khi, klo;
+      if (b == A) {
+        khi = tab(G, A, T_OHI, Ic[A]);
+        klo = tab(G, A, T_OLO, Ic[A]);
+      } else {
+        khi = tab(G, b, T_THI, Ic[b]);
+        klo = tab(G, b, T_TLO, Ic[b]);
+      }
+      v += nu * ((up[b] - uc) * khi - (uc - um[b]) * klo);
+    }
+  }
+  if (fa != T(0)) v += fa;
+  return v;
+}
+
+template <typename T, int TJ, int TK>
+__global__ void __launch_bounds__(TJ* TK) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
+  typedef RingGeom<TJ, TK> RG;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);  // [4 slots][3 comps][PS]
+  const int tk = threadIdx.x, tj = threadIdx.y, tid = tj * TK + tk;
+  const int k0 = 1 + blockIdx.x * TK, j0 = 1 + blockIdx.y * TJ;
+  const int ib = 1 + blockIdx.z * chunk;
+  const int ie = min(ib + chunk, G.n[0] + 1);
+  const int k = k0 + tk, j = j0 + tj;
+  const bool inside = (k <= G.n[2]) && (j <= G.n[1]);
+  const long long s0 = G.s[0], s1 = G.s[1];
+
+  auto load_plane = [&](int ip) {
+    if (ip < 0 || ip >= G.E[0]) return;
+    T* dst = ring + (ip & 3) * 3 * RG::PS;
+    for (int e = tid; e < 3 * RG::PS; e += RG::NT) {
+      const int c = e / RG::PS;
+      const int r = e - c * RG::PS;
+      const int jj = r / RG::PW;
+      const int kk = r - jj * RG::PW;
+      const int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
+      const bool ok = gj < G.E[1] && gk < G.E[2];
+      const T* src = A.y.c[c] + (ok ? (long long)ip * s0 + (long long)gj * s1 + gk : 0);
+      cp_async_val(dst + e, src, ok);
+    }
+  };
+
+  load_plane(ib - 1);
+  load_plane(ib);
+  load_plane(ib + 1);
+  cp_commit();
+  load_plane(ib + 2);
+  cp_commit();
+  const int c0 = (tj + 1) * RG::PW + (tk + 1);
+  const int I3[3] = {0, j, k};
+  for (int i = ib; i < ie; ++i) {
+    const long long x = (long long)i * s0 + (long long)j * s1 + k;
+    const int I[3] = {i, I3[1], I3[2]};
+    // epilogue operands first: their latency overlaps the ring wait
+    T b0[3], bs[3];
+    bool dof[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      dof[a] = inside && is_udof<T, 3>(G, I, a);
+      b0[a] = T(0);
+      bs[a] = T(0);
+      if (dof[a]) {
+        if (A.has_next || (A.has_s && A.s_from_u0)) b0[a] = A.u0.c[a][x];
+        if (A.has_s && !A.s_from_u0) bs[a] = A.s_in.c[a][x];
+      }
+    }
+    cp_wait<1>();
+    __syncthreads();
+    const T* pl[3] = {ring + ((i - 1) & 3) * 3 * RG::PS, ring + (i & 3) * 3 * RG::PS, ring + ((i + 1) & 3) * 3 * RG::PS};
+    T kv[3];
+    kv[0] = dof[0] ? rhs_ring<T, 0, TJ, TK>(G, pl, c0, i, j, k, A.diff, A.nu, A.F.f[0]) : T(0);
+    kv[1] = dof[1] ? rhs_ring<T, 1, TJ, TK>(G, pl, c0, i, j, k, A.diff, A.nu, A.F.f[1]) : T(0);
+    kv[2] = dof[2] ? rhs_ring<T, 2, TJ, TK>(G, pl, c0, i, j, k, A.diff, A.nu, A.F.f[2]) : T(0);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (!dof[a]) continue;
+      if (A.has_k) A.k_out.c[a][x] = kv[a];
+      if (A.has_s) A.s_out.c[a][x] = (A.s_from_u0 ? b0[a] : bs[a]) + kv[a] * A.cb;
+      if (A.has_next) A.y_next.c[a][x] = b0[a] + kv[a] * A.ca;
+    }
+    __syncthreads();
+    load_plane(i + 3);
+    cp_commit();
+  }
+  cp_wait<0>();
+}
+
+constexpr int kTJ = 8, kTK = 32;
+
+template <typename T>
+static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
+  typedef RingGeom<kTJ, kTK> RG;
+  const size_t smem = 4 * 3 * RG::PS * sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_stage_march<T, kTJ, kTK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int bx = (G.n[2] + kTK - 1) / kTK, by = (G.n[1] + kTJ - 1) / kTJ;
+  const long long bps = (long long)bx * by;
+  long long want = (4LL * 148 * 6 + bps - 1) / bps;  // ~4 waves of resident CTAs
+  int chunk = (int)((G.n[0] + want - 1) / want);
+  if (chunk < 16) chunk = 16;
+  const int bz = (G.n[0] + chunk - 1) / chunk;
+  k_stage_march<T, kTJ, kTK><<<dim3(bx, by, bz), dim3(kTK, kTJ), smem, st>>>(G, A, chunk);
+  SFB_LAUNCH_CHECK("rk stage (march)");
+  return SFB_OK;
+}
 
 template <typename T>
 static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
@@ -67,6 +243,7 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
   A.s_from_u0 = a->s_in[0] == nullptr;
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
+  if (G.dim == 3 && !getenv("SFB_STAGE_GENERIC")) return stage_march<T>(G, A, st);
   Box B = int_box(G);
   SFB_DISPATCH_DIM(G.dim, D, (k_stage_generic<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, A, B)));
   SFB_LAUNCH_CHECK("rk stage");
