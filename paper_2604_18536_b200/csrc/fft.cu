@@ -212,48 +212,64 @@ __device__ __forceinline__ void dft(C* v) {
   else dft_odd<C, R, INV>(v);
 }
 
+// j / Ns and j % Ns for j < 2^24 without an integer divide
+__device__ __forceinline__ void divmod_ns(int j, int Ns, float inv, int& q, int& r) {
+  q = __float2int_rz(__int2float_rn(j) * inv);
+  r = j - q * Ns;
+  if (r < 0) {
+    --q;
+    r += Ns;
+  } else if (r >= Ns) {
+    ++q;
+    r -= Ns;
+  }
+}
+
 // One Stockham pass over a tile stored [m][w] (m < L, w < W): src -> dst.
-template <typename C, int R, bool INV>
-__device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restrict__ dst, int L, int W, int Ns,
+// Thread t owns column t % W and butterflies j = t / W + s * (NT / W).
+template <typename C, int R, bool INV, int W>
+__device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restrict__ dst, int L, int Ns,
                                          const C* __restrict__ tw) {
   const int nb = L / R;
-  const int total = nb * W;
   const int step = L / (Ns * R);
-  for (int b = threadIdx.x; b < total; b += blockDim.x) {
-    const int col = b % W;
-    const int j = b / W;
-    const int k = j % Ns;
+  const int col = threadIdx.x % W;
+  const int jstride = blockDim.x / W;
+  const float inv = 1.0f / (float)Ns;
+  for (int j = threadIdx.x / W; j < nb; j += jstride) {
+    int g, k;
+    divmod_ns(j, Ns, inv, g, k);
     C v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = src[(j + r * nb) * W + col];
     if (Ns > 1) {
+      const int kstep = k * step;
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        C w = __ldg(tw + k * r * step);
+        C w = __ldg(tw + kstep * r);
         if (INV) w.y = -w.y;
         v[r] = cmul(v[r], w);
       }
     }
     dft<C, R, INV>(v);
-    const int d = (j / Ns) * Ns * R + k;
+    const int d = g * Ns * R + k;
 #pragma unroll
     for (int r = 0; r < R; ++r) dst[(d + r * Ns) * W + col] = v[r];
   }
 }
 
 // Run all passes of a length-L plan; returns the buffer holding the result.
-template <typename C, bool INV>
-__device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, int W, const C* __restrict__ tw) {
+template <typename C, bool INV, int W>
+__device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, const C* __restrict__ tw) {
   int Ns = 1;
   for (int p = 0; p < P.np; ++p) {
     __syncthreads();
     switch (P.radix[p]) {
-      case 8: stockham<C, 8, INV>(a, b, P.L, W, Ns, tw); break;
-      case 4: stockham<C, 4, INV>(a, b, P.L, W, Ns, tw); break;
-      case 2: stockham<C, 2, INV>(a, b, P.L, W, Ns, tw); break;
-      case 7: stockham<C, 7, INV>(a, b, P.L, W, Ns, tw); break;
-      case 5: stockham<C, 5, INV>(a, b, P.L, W, Ns, tw); break;
-      default: stockham<C, 3, INV>(a, b, P.L, W, Ns, tw); break;
+      case 8: stockham<C, 8, INV, W>(a, b, P.L, Ns, tw); break;
+      case 4: stockham<C, 4, INV, W>(a, b, P.L, Ns, tw); break;
+      case 2: stockham<C, 2, INV, W>(a, b, P.L, Ns, tw); break;
+      case 7: stockham<C, 7, INV, W>(a, b, P.L, Ns, tw); break;
+      case 5: stockham<C, 5, INV, W>(a, b, P.L, Ns, tw); break;
+      default: stockham<C, 3, INV, W>(a, b, P.L, Ns, tw); break;
     }
     Ns *= P.radix[p];
     C* t = a;
@@ -268,8 +284,8 @@ __device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, int W, const 
 // strided C2C pass (optionally fused forward -> scale -> inverse)
 //   element (m, col) at base + m*S + col, col in [0, ncol), tile W columns
 // ---------------------------------------------------------------------------
-template <typename T, int MODE>  // MODE 0 fwd, 1 inv, 2 fwd+scale+inv
-__global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P, int W,
+template <typename T, int MODE, int W>  // MODE 0 fwd, 1 inv, 2 fwd+scale+inv
+__global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P,
                                                      long long S, int ncol, long long bstride,
                                                      const typename CX<T>::t* __restrict__ tw, ScaleArgs sc) {
   typedef typename CX<T>::t C;
@@ -288,8 +304,8 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
   }
   cp_async_wait_all();
   C* res;
-  if (MODE == 1) res = run_fft<C, true>(bufA, bufB, P, W, tw);
-  else res = run_fft<C, false>(bufA, bufB, P, W, tw);
+  if (MODE == 1) res = run_fft<C, true, W>(bufA, bufB, P, tw);
+  else res = run_fft<C, false, W>(bufA, bufB, P, tw);
   if (MODE == 2) {
     // eigenvalue scaling (poisson.py:179-199): lam in fp64, cast to T
     for (int e = threadIdx.x; e < tot; e += blockDim.x) {
@@ -313,7 +329,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
       res[e] = v;
     }
     C* other = (res == bufA) ? bufB : bufA;
-    res = run_fft<C, true>(res, other, P, W, tw);
+    res = run_fft<C, true, W>(res, other, P, tw);
   }
   for (int e = threadIdx.x; e < tot; e += blockDim.x) {
     const int w = e % W, m = e / W;
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(128) k_fft_r2c(const T* __restrict__ in, typen
   const C* row = reinterpret_cast<const C*>(in + (long long)blockIdx.x * in_row);
   for (int m = threadIdx.x; m < M; m += blockDim.x) cp_async_elem(bufA + m, row + m, true);
   cp_async_wait_all();
-  C* Z = run_fft<C, false>(bufA, bufB, P, 1, tw);
+  C* Z = run_fft<C, false, 1>(bufA, bufB, P, tw);
   C* o = out + (long long)blockIdx.x * out_row;
   // X[k] = E[k] + w^k O[k],  E = (Z[k] + conj Z[M-k]) / 2,  O = (Z[k] - conj Z[M-k]) / (2i)
   for (int k = threadIdx.x; k <= M; k += blockDim.x) {
@@ -387,7 +403,7 @@ __global__ void __launch_bounds__(128) k_fft_c2r(const typename CX<T>::t* __rest
     z.y = fe.y + fo.x;
     bufA[k] = z;
   }
-  C* z = run_fft<C, true>(bufA, bufB, P, 1, tw);
+  C* z = run_fft<C, true, 1>(bufA, bufB, P, tw);
   C* row = reinterpret_cast<C*>(out + (long long)blockIdx.x * out_row);
   for (int m = threadIdx.x; m < M; m += blockDim.x) row[m] = z[m];
 }
@@ -446,6 +462,22 @@ static int pick_w(int L, size_t csz) {
   return W;
 }
 
+template <typename T, int MODE>
+static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long long S, int ncol, long long bstride,
+                          int nbatch, const typename CX<T>::t* tw, const ScaleArgs& sc, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  dim3 grid((ncol + W - 1) / W, nbatch);
+  const size_t sm = 2 * (size_t)P.L * W * sizeof(C);
+  switch (W) {
+    case 8: k_fft_strided<T, MODE, 8><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 4: k_fft_strided<T, MODE, 4><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 2: k_fft_strided<T, MODE, 2><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    default: k_fft_strided<T, MODE, 1><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+  }
+  SFB_LAUNCH_CHECK("fft strided pass");
+  return SFB_OK;
+}
+
 template <typename T>
 int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   typedef typename CX<T>::t C;
@@ -466,37 +498,23 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   if (dim == 3) {
     const int n0 = F.n[0], n1 = F.n[1];
     // 2. axis 1 forward: S = nh, columns k2 < nh, batch over k0
-    {
-      const int W = pick_w(n1, csz);
-      dim3 grid((nh + W - 1) / W, n0);
-      k_fft_strided<T, 0><<<grid, 256, 2 * (size_t)n1 * W * csz, st>>>(cbuf, F.ax[1], W, nh, nh, (long long)n1 * nh,
-                                                                       (const C*)F.tw_ax[1], none);
-      SFB_LAUNCH_CHECK("fft axis1 fwd");
-    }
+    int rc;
+    if ((rc = launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, csz), nh, nh, (long long)n1 * nh, n0,
+                                   (const C*)F.tw_ax[1], none, st)))
+      return rc;
     // 3. axis 0 forward + scale + inverse: S = n1*nh, columns (k1,k2)
-    {
-      const int W = pick_w(n0, csz);
-      const int ncol = n1 * nh;
-      dim3 grid((ncol + W - 1) / W, 1);
-      k_fft_strided<T, 2><<<grid, 256, 2 * (size_t)n0 * W * csz, st>>>(cbuf, F.ax[0], W, (long long)n1 * nh, ncol, 0,
-                                                                       (const C*)F.tw_ax[0], F.sc);
-      SFB_LAUNCH_CHECK("fft axis0 fused");
-    }
+    if ((rc = launch_strided<T, 2>(cbuf, F.ax[0], pick_w(n0, csz), (long long)n1 * nh, n1 * nh, 0, 1,
+                                   (const C*)F.tw_ax[0], F.sc, st)))
+      return rc;
     // 4. axis 1 inverse
-    {
-      const int W = pick_w(n1, csz);
-      dim3 grid((nh + W - 1) / W, n0);
-      k_fft_strided<T, 1><<<grid, 256, 2 * (size_t)n1 * W * csz, st>>>(cbuf, F.ax[1], W, nh, nh, (long long)n1 * nh,
-                                                                       (const C*)F.tw_ax[1], none);
-      SFB_LAUNCH_CHECK("fft axis1 inv");
-    }
+    if ((rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, csz), nh, nh, (long long)n1 * nh, n0,
+                                   (const C*)F.tw_ax[1], none, st)))
+      return rc;
   } else {
     const int n0 = F.n[0];
-    const int W = pick_w(n0, csz);
-    dim3 grid((nh + W - 1) / W, 1);
-    k_fft_strided<T, 2><<<grid, 256, 2 * (size_t)n0 * W * csz, st>>>(cbuf, F.ax[0], W, nh, nh, 0, (const C*)F.tw_ax[0],
-                                                                     F.sc);
-    SFB_LAUNCH_CHECK("fft axis0 fused");
+    int rc;
+    if ((rc = launch_strided<T, 2>(cbuf, F.ax[0], pick_w(n0, csz), nh, nh, 0, 1, (const C*)F.tw_ax[0], F.sc, st)))
+      return rc;
   }
   // 5. C2R along the contiguous axis
   {
@@ -511,15 +529,25 @@ template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t);
 
 template <typename T>
 int fft_set_smem_limits() {
-  typedef typename CX<T>::t C;
   const int big = 200 * 1024;
   cudaError_t e = cudaSuccess;
-  e = cudaFuncSetAttribute(k_fft_strided<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_strided<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_strided<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_r2c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fft_c2r<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  (void)sizeof(C);
+#define SFB_SMEM(K) \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, big)
+  SFB_SMEM((k_fft_strided<T, 0, 1>));
+  SFB_SMEM((k_fft_strided<T, 0, 2>));
+  SFB_SMEM((k_fft_strided<T, 0, 4>));
+  SFB_SMEM((k_fft_strided<T, 0, 8>));
+  SFB_SMEM((k_fft_strided<T, 1, 1>));
+  SFB_SMEM((k_fft_strided<T, 1, 2>));
+  SFB_SMEM((k_fft_strided<T, 1, 4>));
+  SFB_SMEM((k_fft_strided<T, 1, 8>));
+  SFB_SMEM((k_fft_strided<T, 2, 1>));
+  SFB_SMEM((k_fft_strided<T, 2, 2>));
+  SFB_SMEM((k_fft_strided<T, 2, 4>));
+  SFB_SMEM((k_fft_strided<T, 2, 8>));
+  SFB_SMEM(k_fft_r2c<T>);
+  SFB_SMEM(k_fft_c2r<T>);
+#undef SFB_SMEM
   return cuda_check(e, "cudaFuncSetAttribute(fft smem)");
 }
 template int fft_set_smem_limits<double>();

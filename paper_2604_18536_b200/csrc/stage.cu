@@ -69,15 +69,32 @@ struct RingGeom {
   static constexpr int PW = TK + 2, PH = TJ + 2, PS = PW * PH, NT = TJ * TK;
 };
 
-// momentum RHS of component A at the CTA's current cell from the smem ring
-// (same arithmetic and order as rhs_comp, sfb_kernels.cuh)
+// Coefficients of one axis at one index (operators.py:47-84 tables).
+template <typename T>
+struct Coef {
+  T rdu, wlo, whi, ohi, olo, rdx, thi, tlo;
+};
+template <typename T>
+__device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
+  Coef<T> c;
+  c.rdu = tab(G, axis, T_RDU, i);
+  c.wlo = tab(G, axis, T_WLO, i);
+  c.whi = tab(G, axis, T_WHI, i);
+  c.ohi = tab(G, axis, T_OHI, i);
+  c.olo = tab(G, axis, T_OLO, i);
+  c.rdx = tab(G, axis, T_RDX, i);
+  c.thi = tab(G, axis, T_THI, i);
+  c.tlo = tab(G, axis, T_TLO, i);
+  return c;
+}
+
+// Momentum RHS of component A at the thread's cell from the smem ring, same
+// arithmetic and order as rhs_comp (sfb_kernels.cuh).  P[d] points at the
+// component-0 centre of plane i-1+d; component c sits at +c*PS.
 template <typename T, int A, int TJ, int TK>
-__device__ __forceinline__ T rhs_ring(const Geo<T>& G, const T* const* pl, int c0, int i, int j, int k, bool diff, T nu,
-                                      T fa) {
+__device__ __forceinline__ T rhs_ring(const T* const (&P)[3], const Coef<T> (&C)[3], bool diff, T nu, T fa) {
   typedef RingGeom<TJ, TK> RG;
-  // pl[d] = plane i-1+d base (component 0); component c at + c*PS; centre c0
-  auto Y = [&](int c, int di, int dj, int dk) -> T { return pl[1 + di][c * RG::PS + c0 + dj * RG::PW + dk]; };
-  const int Ic[3] = {i, j, k};
+  auto Y = [&](int c, int di, int dj, int dk) -> T { return P[1 + di][c * RG::PS + dj * RG::PW + dk]; };
   const T uc = Y(A, 0, 0, 0);
   T up[3], um[3];
   up[0] = Y(A, 1, 0, 0);
@@ -93,30 +110,22 @@ __device__ __forceinline__ T rhs_ring(const Geo<T>& G, const T* const* pl, int c
     const T tm = (um[b] + uc) * T(0.5);
     T fl;
     if (b == A) {
-      fl = (tp * tp - tm * tm) * tab(G, A, T_RDU, Ic[A]);
+      fl = (tp * tp - tm * tm) * C[A].rdu;
     } else {
-      const T wl = tab(G, A, T_WLO, Ic[A]);
-      const T wh = tab(G, A, T_WHI, Ic[A]);
-      // offsets +e_A, -e_b, -e_b+e_A
+      const T wl = C[A].wlo, wh = C[A].whi;
       const int eA0 = A == 0, eA1 = A == 1, eA2 = A == 2;
       const int eb0 = b == 0, eb1 = b == 1, eb2 = b == 2;
       const T vp = Y(b, 0, 0, 0) * wl + Y(b, eA0, eA1, eA2) * wh;
       const T vm = Y(b, -eb0, -eb1, -eb2) * wl + Y(b, eA0 - eb0, eA1 - eb1, eA2 - eb2) * wh;
-      fl = (tp * vp - tm * vm) * tab(G, b, T_RDX, Ic[b]);
+      fl = (tp * vp - tm * vm) * C[b].rdx;
     }
     v -= fl;
   }
   if (diff) {
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      T khi, klo;
-      if (b == A) {
-        khi = tab(G, A, T_OHI, Ic[A]);
-        klo = tab(G, A, T_OLO, Ic[A]);
-      } else {
-        khi = tab(G, b, T_THI, Ic[b]);
-        klo = tab(G, b, T_TLO, Ic[b]);
-      }
+      const T khi = b == A ? C[A].ohi : C[b].thi;
+      const T klo = b == A ? C[A].olo : C[b].tlo;
       v += nu * ((up[b] - uc) * khi - (uc - um[b]) * klo);
     }
   }
@@ -124,65 +133,93 @@ __device__ __forceinline__ T rhs_ring(const Geo<T>& G, const T* const* pl, int c
   return v;
 }
 
-template <typename T, int TJ, int TK>
-__global__ void __launch_bounds__(TJ* TK) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
+constexpr int kRing = 5;  // planes i-1, i, i+1 in use, i+2 landing, i+3 issued
+
+template <typename T, int TJ, int TK, int MINB>
+__global__ void __launch_bounds__(TJ* TK, MINB) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
   typedef RingGeom<TJ, TK> RG;
+  constexpr int NE = 3 * RG::PS;                    // values per plane slot
+  constexpr int NQ = (NE + RG::NT - 1) / RG::NT;    // fill copies per thread
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw);  // [4 slots][3 comps][PS]
+  T* ring = reinterpret_cast<T*>(smem_raw);  // [kRing][3][PS]
   const int tk = threadIdx.x, tj = threadIdx.y, tid = tj * TK + tk;
   const int k0 = 1 + blockIdx.x * TK, j0 = 1 + blockIdx.y * TJ;
   const int ib = 1 + blockIdx.z * chunk;
   const int ie = min(ib + chunk, G.n[0] + 1);
   const int k = k0 + tk, j = j0 + tj;
   const bool inside = (k <= G.n[2]) && (j <= G.n[1]);
-  const long long s0 = G.s[0], s1 = G.s[1];
+  const long long s0 = G.s[0];
 
-  auto load_plane = [&](int ip) {
+  // plane-invariant fill descriptors: source pointer into plane 0 and slot offset
+  const T* fsrc[NQ];
+  bool fok[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int e = tid + q * RG::NT;
+    const int c = e / RG::PS;
+    const int r = e - c * RG::PS;
+    const int jj = r / RG::PW;
+    const int kk = r - jj * RG::PW;
+    const int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
+    fok[q] = e < NE && gj < G.E[1] && gk < G.E[2];
+    fsrc[q] = A.y.c[c < 3 ? c : 0] + (fok[q] ? (long long)gj * G.s[1] + gk : 0);
+  }
+  auto load_plane = [&](int ip, int slot) {
     if (ip < 0 || ip >= G.E[0]) return;
-    T* dst = ring + (ip & 3) * 3 * RG::PS;
-    for (int e = tid; e < 3 * RG::PS; e += RG::NT) {
-      const int c = e / RG::PS;
-      const int r = e - c * RG::PS;
-      const int jj = r / RG::PW;
-      const int kk = r - jj * RG::PW;
-      const int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
-      const bool ok = gj < G.E[1] && gk < G.E[2];
-      const T* src = A.y.c[c] + (ok ? (long long)ip * s0 + (long long)gj * s1 + gk : 0);
-      cp_async_val(dst + e, src, ok);
+    T* dst = ring + slot * NE + tid;
+    const long long base = (long long)ip * s0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (q < NQ - 1 || tid + q * RG::NT < NE) cp_async_val(dst + q * RG::NT, fsrc[q] + (fok[q] ? base : 0), fok[q]);
     }
   };
+  // thread-invariant coefficient sets for axes 1 (j) and 2 (k)
+  Coef<T> C[3];
+  C[1] = coef_at(G, 1, inside ? j : 1);
+  C[2] = coef_at(G, 2, inside ? k : 1);
 
-  load_plane(ib - 1);
-  load_plane(ib);
-  load_plane(ib + 1);
+  int sl_m = (ib - 1) % kRing;  // slot of plane i-1
+  load_plane(ib - 1, sl_m);
+  load_plane(ib, (sl_m + 1) % kRing);
+  load_plane(ib + 1, (sl_m + 2) % kRing);
   cp_commit();
-  load_plane(ib + 2);
+  load_plane(ib + 2, (sl_m + 3) % kRing);
   cp_commit();
   const int c0 = (tj + 1) * RG::PW + (tk + 1);
-  const int I3[3] = {0, j, k};
-  for (int i = ib; i < ie; ++i) {
-    const long long x = (long long)i * s0 + (long long)j * s1 + k;
-    const int I[3] = {i, I3[1], I3[2]};
+  const bool wall1 = !G.per[1], wall2 = !G.per[2], wall0 = !G.per[0];
+  const T* const u0c[3] = {A.u0.c[0], A.u0.c[1], A.u0.c[2]};
+  long long x = (long long)ib * s0 + (long long)j * G.s[1] + k;
+  for (int i = ib; i < ie; ++i, x += s0) {
+    bool dof[3];
+    dof[0] = inside && !(wall0 && i == G.n[0]);
+    dof[1] = inside && !(wall1 && j == G.n[1]);
+    dof[2] = inside && !(wall2 && k == G.n[2]);
     // epilogue operands first: their latency overlaps the ring wait
     T b0[3], bs[3];
-    bool dof[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      dof[a] = inside && is_udof<T, 3>(G, I, a);
       b0[a] = T(0);
       bs[a] = T(0);
       if (dof[a]) {
-        if (A.has_next || (A.has_s && A.s_from_u0)) b0[a] = A.u0.c[a][x];
+        if (A.has_next || (A.has_s && A.s_from_u0)) b0[a] = u0c[a][x];
         if (A.has_s && !A.s_from_u0) bs[a] = A.s_in.c[a][x];
       }
     }
+    C[0] = coef_at(G, 0, i);
     cp_wait<1>();
     __syncthreads();
-    const T* pl[3] = {ring + ((i - 1) & 3) * 3 * RG::PS, ring + (i & 3) * 3 * RG::PS, ring + ((i + 1) & 3) * 3 * RG::PS};
+    int sl_l = sl_m + 4;
+    if (sl_l >= kRing) sl_l -= kRing;
+    load_plane(i + 3, sl_l);
+    cp_commit();
+    int s1i = sl_m + 1, s2i = sl_m + 2;
+    if (s1i >= kRing) s1i -= kRing;
+    if (s2i >= kRing) s2i -= kRing;
+    const T* const P[3] = {ring + sl_m * NE + c0, ring + s1i * NE + c0, ring + s2i * NE + c0};
     T kv[3];
-    kv[0] = dof[0] ? rhs_ring<T, 0, TJ, TK>(G, pl, c0, i, j, k, A.diff, A.nu, A.F.f[0]) : T(0);
-    kv[1] = dof[1] ? rhs_ring<T, 1, TJ, TK>(G, pl, c0, i, j, k, A.diff, A.nu, A.F.f[1]) : T(0);
-    kv[2] = dof[2] ? rhs_ring<T, 2, TJ, TK>(G, pl, c0, i, j, k, A.diff, A.nu, A.F.f[2]) : T(0);
+    kv[0] = dof[0] ? rhs_ring<T, 0, TJ, TK>(P, C, A.diff, A.nu, A.F.f[0]) : T(0);
+    kv[1] = dof[1] ? rhs_ring<T, 1, TJ, TK>(P, C, A.diff, A.nu, A.F.f[1]) : T(0);
+    kv[2] = dof[2] ? rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]) : T(0);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (!dof[a]) continue;
@@ -190,33 +227,38 @@ __global__ void __launch_bounds__(TJ* TK) k_stage_march(Geo<T> G, StageArgs<T> A
       if (A.has_s) A.s_out.c[a][x] = (A.s_from_u0 ? b0[a] : bs[a]) + kv[a] * A.cb;
       if (A.has_next) A.y_next.c[a][x] = b0[a] + kv[a] * A.ca;
     }
-    __syncthreads();
-    load_plane(i + 3);
-    cp_commit();
+    sl_m = s1i;
   }
   cp_wait<0>();
 }
 
 constexpr int kTJ = 8, kTK = 32;
 
-template <typename T>
-static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
+template <typename T, int MINB>
+static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
   typedef RingGeom<kTJ, kTK> RG;
-  const size_t smem = 4 * 3 * RG::PS * sizeof(T);
+  const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_stage_march<T, kTJ, kTK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_stage_march<T, kTJ, kTK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const int bx = (G.n[2] + kTK - 1) / kTK, by = (G.n[1] + kTJ - 1) / kTJ;
   const long long bps = (long long)bx * by;
-  long long want = (4LL * 148 * 6 + bps - 1) / bps;  // ~4 waves of resident CTAs
+  long long want = (4LL * 148 * MINB * 2 + bps - 1) / bps;  // ~4 waves of resident CTAs
   int chunk = (int)((G.n[0] + want - 1) / want);
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;
-  k_stage_march<T, kTJ, kTK><<<dim3(bx, by, bz), dim3(kTK, kTJ), smem, st>>>(G, A, chunk);
+  k_stage_march<T, kTJ, kTK, MINB><<<dim3(bx, by, bz), dim3(kTK, kTJ), smem, st>>>(G, A, chunk);
   SFB_LAUNCH_CHECK("rk stage (march)");
   return SFB_OK;
+}
+
+template <typename T>
+static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
+  static int minb = getenv("SFB_STAGE_MINB") ? atoi(getenv("SFB_STAGE_MINB")) : 2;
+  if (minb >= 3) return stage_march_launch<T, 3>(G, A, st);
+  return stage_march_launch<T, 2>(G, A, st);
 }
 
 template <typename T>
