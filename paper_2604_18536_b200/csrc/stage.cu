@@ -135,27 +135,32 @@ __device__ __forceinline__ T rhs_ring(const T* const (&P)[3], const Coef<T> (&C)
 
 constexpr int kRing = 5;  // planes i-1, i, i+1 in use, i+2 landing, i+3 issued
 
-template <typename T, int TJ, int TK, int MINB>
-__global__ void __launch_bounds__(TJ* TK, MINB) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
+// epilogue variants (compile-time): bit 1 k_out, bit 2 s_out, bit 4 s from
+// u0 (else s_in), bit 8 y_next
+enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8 };
+
+template <typename T, int TJ, int TK, int CPT, int FL, int MINB>
+__global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
   typedef RingGeom<TJ, TK> RG;
+  constexpr int NTH = TJ / CPT * TK;                // threads per CTA
   constexpr int NE = 3 * RG::PS;                    // values per plane slot
-  constexpr int NQ = (NE + RG::NT - 1) / RG::NT;    // fill copies per thread
+  constexpr int NQ = (NE + NTH - 1) / NTH;          // fill copies per thread
+  constexpr int RS = TJ / CPT;                      // row stride between a thread's cells
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw);  // [kRing][3][PS]
-  const int tk = threadIdx.x, tj = threadIdx.y, tid = tj * TK + tk;
+  T* ring = reinterpret_cast<T*>(smem_raw);         // [kRing][3][PS]
+  Coef<T>* cj = reinterpret_cast<Coef<T>*>(ring + kRing * NE);  // axis-1 coefficients of the tile rows
+  const int tk = threadIdx.x, tq = threadIdx.y, tid = tq * TK + tk;
   const int k0 = 1 + blockIdx.x * TK, j0 = 1 + blockIdx.y * TJ;
   const int ib = 1 + blockIdx.z * chunk;
   const int ie = min(ib + chunk, G.n[0] + 1);
-  const int k = k0 + tk, j = j0 + tj;
-  const bool inside = (k <= G.n[2]) && (j <= G.n[1]);
+  const int k = k0 + tk;
   const long long s0 = G.s[0];
 
-  // plane-invariant fill descriptors: source pointer into plane 0 and slot offset
   const T* fsrc[NQ];
   bool fok[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    const int e = tid + q * RG::NT;
+    const int e = tid + q * NTH;
     const int c = e / RG::PS;
     const int r = e - c * RG::PS;
     const int jj = r / RG::PW;
@@ -169,40 +174,48 @@ __global__ void __launch_bounds__(TJ* TK, MINB) k_stage_march(Geo<T> G, StageArg
     T* dst = ring + slot * NE + tid;
     const long long base = (long long)ip * s0;
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      if (q < NQ - 1 || tid + q * RG::NT < NE) cp_async_val(dst + q * RG::NT, fsrc[q] + (fok[q] ? base : 0), fok[q]);
-    }
+    for (int q = 0; q < NQ; ++q)
+      if (q < NQ - 1 || tid + q * NTH < NE) cp_async_val(dst + q * NTH, fsrc[q] + (fok[q] ? base : 0), fok[q]);
   };
-  // thread-invariant coefficient sets for axes 1 (j) and 2 (k)
+  if (tid < TJ) cj[tid] = coef_at(G, 1, min(j0 + tid, G.n[1]));
   Coef<T> C[3];
-  C[1] = coef_at(G, 1, inside ? j : 1);
-  C[2] = coef_at(G, 2, inside ? k : 1);
+  C[2] = coef_at(G, 2, min(k, G.n[2]));
 
-  int sl_m = (ib - 1) % kRing;  // slot of plane i-1
+  int sl_m = (ib - 1) % kRing;
   load_plane(ib - 1, sl_m);
   load_plane(ib, (sl_m + 1) % kRing);
   load_plane(ib + 1, (sl_m + 2) % kRing);
   cp_commit();
   load_plane(ib + 2, (sl_m + 3) % kRing);
   cp_commit();
-  const int c0 = (tj + 1) * RG::PW + (tk + 1);
-  const bool wall1 = !G.per[1], wall2 = !G.per[2], wall0 = !G.per[0];
-  const T* const u0c[3] = {A.u0.c[0], A.u0.c[1], A.u0.c[2]};
-  long long x = (long long)ib * s0 + (long long)j * G.s[1] + k;
-  for (int i = ib; i < ie; ++i, x += s0) {
-    bool dof[3];
-    dof[0] = inside && !(wall0 && i == G.n[0]);
-    dof[1] = inside && !(wall1 && j == G.n[1]);
-    dof[2] = inside && !(wall2 && k == G.n[2]);
-    // epilogue operands first: their latency overlaps the ring wait
-    T b0[3], bs[3];
+
+  bool inside[CPT];
+  int jr[CPT];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      b0[a] = T(0);
-      bs[a] = T(0);
-      if (dof[a]) {
-        if (A.has_next || (A.has_s && A.s_from_u0)) b0[a] = u0c[a][x];
-        if (A.has_s && !A.s_from_u0) bs[a] = A.s_in.c[a][x];
+  for (int r = 0; r < CPT; ++r) {
+    jr[r] = j0 + tq + r * RS;
+    inside[r] = (k <= G.n[2]) && (jr[r] <= G.n[1]);
+  }
+  const bool wall0 = !G.per[0], wall1 = !G.per[1], wall2 = !G.per[2];
+  long long x0 = (long long)ib * s0 + (long long)jr[0] * G.s[1] + k;
+  const long long rstep = (long long)RS * G.s[1];
+  for (int i = ib; i < ie; ++i, x0 += s0) {
+    T b0[CPT][3], bs[CPT][3];
+    bool dof[CPT][3];
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+      const long long x = x0 + r * rstep;
+      dof[r][0] = inside[r] && !(wall0 && i == G.n[0]);
+      dof[r][1] = inside[r] && !(wall1 && jr[r] == G.n[1]);
+      dof[r][2] = inside[r] && !(wall2 && k == G.n[2]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        b0[r][a] = T(0);
+        bs[r][a] = T(0);
+        if (dof[r][a]) {
+          if ((FL & FL_NEXT) || ((FL & FL_S) && (FL & FL_SU0))) b0[r][a] = A.u0.c[a][x];
+          if ((FL & FL_S) && !(FL & FL_SU0)) bs[r][a] = A.s_in.c[a][x];
+        }
       }
     }
     C[0] = coef_at(G, 0, i);
@@ -215,50 +228,66 @@ __global__ void __launch_bounds__(TJ* TK, MINB) k_stage_march(Geo<T> G, StageArg
     int s1i = sl_m + 1, s2i = sl_m + 2;
     if (s1i >= kRing) s1i -= kRing;
     if (s2i >= kRing) s2i -= kRing;
-    const T* const P[3] = {ring + sl_m * NE + c0, ring + s1i * NE + c0, ring + s2i * NE + c0};
-    T kv[3];
-    kv[0] = dof[0] ? rhs_ring<T, 0, TJ, TK>(P, C, A.diff, A.nu, A.F.f[0]) : T(0);
-    kv[1] = dof[1] ? rhs_ring<T, 1, TJ, TK>(P, C, A.diff, A.nu, A.F.f[1]) : T(0);
-    kv[2] = dof[2] ? rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]) : T(0);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (!dof[a]) continue;
-      if (A.has_k) A.k_out.c[a][x] = kv[a];
-      if (A.has_s) A.s_out.c[a][x] = (A.s_from_u0 ? b0[a] : bs[a]) + kv[a] * A.cb;
-      if (A.has_next) A.y_next.c[a][x] = b0[a] + kv[a] * A.ca;
+    for (int r = 0; r < CPT; ++r) {
+      const int c0 = (tq + r * RS + 1) * RG::PW + (tk + 1);
+      const T* const P[3] = {ring + sl_m * NE + c0, ring + s1i * NE + c0, ring + s2i * NE + c0};
+      C[1] = cj[tq + r * RS];
+      T kv[3];
+      kv[0] = dof[r][0] ? rhs_ring<T, 0, TJ, TK>(P, C, A.diff, A.nu, A.F.f[0]) : T(0);
+      kv[1] = dof[r][1] ? rhs_ring<T, 1, TJ, TK>(P, C, A.diff, A.nu, A.F.f[1]) : T(0);
+      kv[2] = dof[r][2] ? rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]) : T(0);
+      const long long x = x0 + r * rstep;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (!dof[r][a]) continue;
+        if (FL & FL_K) A.k_out.c[a][x] = kv[a];
+        if (FL & FL_S) A.s_out.c[a][x] = ((FL & FL_SU0) ? b0[r][a] : bs[r][a]) + kv[a] * A.cb;
+        if (FL & FL_NEXT) A.y_next.c[a][x] = b0[r][a] + kv[a] * A.ca;
+      }
     }
     sl_m = s1i;
   }
   cp_wait<0>();
 }
 
-constexpr int kTJ = 8, kTK = 32;
+constexpr int kTJ = 8, kTK = 32, kCPT = 2;
 
-template <typename T, int MINB>
+template <typename T, int FL>
 static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
   typedef RingGeom<kTJ, kTK> RG;
-  const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T);
+  constexpr int MINB = 4;
+  const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T) + kTJ * sizeof(Coef<T>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_stage_march<T, kTJ, kTK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_stage_march<T, kTJ, kTK, kCPT, FL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
   const int bx = (G.n[2] + kTK - 1) / kTK, by = (G.n[1] + kTJ - 1) / kTJ;
   const long long bps = (long long)bx * by;
-  long long want = (4LL * 148 * MINB * 2 + bps - 1) / bps;  // ~4 waves of resident CTAs
+  long long want = (4LL * 148 * MINB + bps - 1) / bps;  // ~4 waves of resident CTAs
   int chunk = (int)((G.n[0] + want - 1) / want);
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;
-  k_stage_march<T, kTJ, kTK, MINB><<<dim3(bx, by, bz), dim3(kTK, kTJ), smem, st>>>(G, A, chunk);
+  k_stage_march<T, kTJ, kTK, kCPT, FL, MINB><<<dim3(bx, by, bz), dim3(kTK, kTJ / kCPT), smem, st>>>(G, A, chunk);
   SFB_LAUNCH_CHECK("rk stage (march)");
   return SFB_OK;
 }
 
 template <typename T>
 static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
-  static int minb = getenv("SFB_STAGE_MINB") ? atoi(getenv("SFB_STAGE_MINB")) : 2;
-  if (minb >= 3) return stage_march_launch<T, 3>(G, A, st);
-  return stage_march_launch<T, 2>(G, A, st);
+  const int fl = (A.has_k ? FL_K : 0) | (A.has_s ? FL_S : 0) | (A.has_s && A.s_from_u0 ? FL_SU0 : 0) |
+                 (A.has_next ? FL_NEXT : 0);
+  switch (fl) {
+    case FL_S | FL_SU0 | FL_NEXT: return stage_march_launch<T, FL_S | FL_SU0 | FL_NEXT>(G, A, st);
+    case FL_S | FL_NEXT: return stage_march_launch<T, FL_S | FL_NEXT>(G, A, st);
+    case FL_S: return stage_march_launch<T, FL_S>(G, A, st);
+    case FL_S | FL_SU0: return stage_march_launch<T, FL_S | FL_SU0>(G, A, st);
+    case FL_K: return stage_march_launch<T, FL_K>(G, A, st);
+    case FL_NEXT: return stage_march_launch<T, FL_NEXT>(G, A, st);
+    default: return -1;  // uncommon combination: generic kernel
+  }
 }
 
 template <typename T>
@@ -285,7 +314,10 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
   A.s_from_u0 = a->s_in[0] == nullptr;
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
-  if (G.dim == 3 && !getenv("SFB_STAGE_GENERIC")) return stage_march<T>(G, A, st);
+  if (G.dim == 3 && !getenv("SFB_STAGE_GENERIC")) {
+    const int rc = stage_march<T>(G, A, st);
+    if (rc >= 0) return rc;
+  }
   Box B = int_box(G);
   SFB_DISPATCH_DIM(G.dim, D, (k_stage_generic<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, A, B)));
   SFB_LAUNCH_CHECK("rk stage");
