@@ -225,115 +225,100 @@ __device__ __forceinline__ void divmod_ns(int j, int Ns, float inv, int& q, int&
   }
 }
 
-// One register-staged Stockham pass, in place on a single smem tile stored
-// [m][w] (m < L, w < W): every thread loads the inputs of its butterflies
-// into registers, the CTA synchronises, then the outputs are written back to
-// their Stockham positions.  Thread t owns column t % W and butterflies
-// j = t / W + s * (NT / W), s < MB.  CAP bounds L*W (the tile capacity).
-template <typename C, int R, bool INV, int W, int NT, int CAP>
-__device__ __forceinline__ void pass_rs(C* buf, int L, int Ns, const C* __restrict__ tw) {
-  constexpr int MB = (CAP + R * NT - 1) / (R * NT);
+// One Stockham pass over a tile stored [m][w] (m < L, w < W): src -> dst.
+// Thread t owns column t % W and butterflies j = t / W + s * (NT / W).
+template <typename C, int R, bool INV, int W>
+__device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restrict__ dst, int L, int Ns,
+                                         const C* __restrict__ tw) {
   const int nb = L / R;
   const int step = L / (Ns * R);
   const int col = threadIdx.x % W;
-  const int jb = threadIdx.x / W;
-  constexpr int JS = NT / W;
-  C v[MB][R];
-#pragma unroll
-  for (int s = 0; s < MB; ++s) {
-    const int j = jb + s * JS;
-    if (j < nb) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[s][r] = buf[(j + r * nb) * W + col];
-    }
-  }
-  __syncthreads();
+  const int jstride = blockDim.x / W;
   const float inv = 1.0f / (float)Ns;
+  for (int j = threadIdx.x / W; j < nb; j += jstride) {
+    int g, k;
+    divmod_ns(j, Ns, inv, g, k);
+    C v[R];
 #pragma unroll
-  for (int s = 0; s < MB; ++s) {
-    const int j = jb + s * JS;
-    if (j < nb) {
-      int g, k;
-      divmod_ns(j, Ns, inv, g, k);
-      if (Ns > 1) {
-        const int kstep = k * step;
+    for (int r = 0; r < R; ++r) v[r] = src[(j + r * nb) * W + col];
+    if (Ns > 1) {
+      const int kstep = k * step;
 #pragma unroll
-        for (int r = 1; r < R; ++r) {
-          C w = __ldg(tw + kstep * r);
-          if (INV) w.y = -w.y;
-          v[s][r] = cmul(v[s][r], w);
-        }
+      for (int r = 1; r < R; ++r) {
+        C w = __ldg(tw + kstep * r);
+        if (INV) w.y = -w.y;
+        v[r] = cmul(v[r], w);
       }
-      dft<C, R, INV>(v[s]);
-      const int d = g * Ns * R + k;
-#pragma unroll
-      for (int r = 0; r < R; ++r) buf[(d + r * Ns) * W + col] = v[s][r];
     }
+    dft<C, R, INV>(v);
+    const int d = g * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[(d + r * Ns) * W + col] = v[r];
   }
-  __syncthreads();
 }
 
-// All passes of a length-L plan, in place (callers synchronise before).
-template <typename C, bool INV, int W, int NT, int CAP>
-__device__ __forceinline__ void run_fft(C* buf, const FftLen& P, const C* __restrict__ tw) {
+// Run all passes of a length-L plan; returns the buffer holding the result.
+template <typename C, bool INV, int W>
+__device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, const C* __restrict__ tw) {
   int Ns = 1;
   for (int p = 0; p < P.np; ++p) {
+    __syncthreads();
     switch (P.radix[p]) {
-      case 8: pass_rs<C, 8, INV, W, NT, CAP>(buf, P.L, Ns, tw); break;
-      case 4: pass_rs<C, 4, INV, W, NT, CAP>(buf, P.L, Ns, tw); break;
-      case 2: pass_rs<C, 2, INV, W, NT, CAP>(buf, P.L, Ns, tw); break;
-      case 7: pass_rs<C, 7, INV, W, NT, CAP>(buf, P.L, Ns, tw); break;
-      case 5: pass_rs<C, 5, INV, W, NT, CAP>(buf, P.L, Ns, tw); break;
-      default: pass_rs<C, 3, INV, W, NT, CAP>(buf, P.L, Ns, tw); break;
+      case 8: stockham<C, 8, INV, W>(a, b, P.L, Ns, tw); break;
+      case 4: stockham<C, 4, INV, W>(a, b, P.L, Ns, tw); break;
+      case 2: stockham<C, 2, INV, W>(a, b, P.L, Ns, tw); break;
+      case 7: stockham<C, 7, INV, W>(a, b, P.L, Ns, tw); break;
+      case 5: stockham<C, 5, INV, W>(a, b, P.L, Ns, tw); break;
+      default: stockham<C, 3, INV, W>(a, b, P.L, Ns, tw); break;
     }
     Ns *= P.radix[p];
+    C* t = a;
+    a = b;
+    b = t;
   }
+  __syncthreads();
+  return a;
 }
-
-constexpr int kStrNT = 512, kStrCAP = 3584;   // strided tiles: L*W <= 3584
-constexpr int kRowNT = 128, kRowCAP = 512;    // rows: M <= 512 (n_last <= 1024)
-constexpr int kRowNT2 = 256, kRowCAP2 = 2048; // rows: M <= 2048
 
 // ---------------------------------------------------------------------------
 // strided C2C pass (optionally fused forward -> scale -> inverse)
 //   element (m, col) at base + m*S + col, col in [0, ncol), tile W columns
 // ---------------------------------------------------------------------------
 template <typename T, int MODE, int W>  // MODE 0 fwd, 1 inv, 2 fwd+scale+inv
-__global__ void __launch_bounds__(kStrNT, 1) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P, long long S,
-                                                     int ncol, long long bstride,
+__global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P,
+                                                     long long S, int ncol, long long bstride,
                                                      const typename CX<T>::t* __restrict__ tw, ScaleArgs sc) {
   typedef typename CX<T>::t C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* buf = reinterpret_cast<C*>(smem_raw);
+  C* bufA = reinterpret_cast<C*>(smem_raw);
+  C* bufB = bufA + (size_t)P.L * W;
   const int c0 = blockIdx.x * W;
   C* base = data + (long long)blockIdx.y * bstride;
   const int L = P.L;
   const int tot = L * W;
-  for (int e = threadIdx.x; e < tot; e += kStrNT) {
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
     const int w = e % W, m = e / W;
     const int col = c0 + w;
     const bool ok = col < ncol;
-    cp_async_elem(buf + e, base + (ok ? (long long)m * S + col : 0), ok);
+    cp_async_elem(bufA + e, base + (ok ? (long long)m * S + col : 0), ok);
   }
   cp_async_wait_all();
-  __syncthreads();
-  if (MODE == 1) run_fft<C, true, W, kStrNT, kStrCAP>(buf, P, tw);
-  else run_fft<C, false, W, kStrNT, kStrCAP>(buf, P, tw);
+  C* res;
+  if (MODE == 1) res = run_fft<C, true, W>(bufA, bufB, P, tw);
+  else res = run_fft<C, false, W>(bufA, bufB, P, tw);
   if (MODE == 2) {
     // eigenvalue scaling (poisson.py:179-199): lam in fp64, cast to T
-    for (int e = threadIdx.x; e < tot; e += kStrNT) {
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
       const int w = e % W, m = e / W;
       const int col = c0 + w;
       if (col >= ncol) continue;
+      const int k1 = sc.nh > 0 ? col / sc.nh : 0;
+      const int k2 = sc.nh > 0 ? col % sc.nh : col;
       double lam;
-      if (sc.dim == 3) {
-        const int k1 = col / sc.nh, k2 = col - (col / sc.nh) * sc.nh;
-        lam = (sc.l0[m] + sc.l1[k1]) + sc.l2[k2];
-      } else {
-        lam = sc.l0[m] + sc.l1[col];
-      }
-      C v = buf[e];
-      if (m == 0 && col == 0) {
+      if (sc.dim == 3) lam = (sc.l0[m] + sc.l1[k1]) + sc.l2[k2];
+      else lam = sc.l0[m] + sc.l1[col];
+      C v = res[e];
+      if (m == 0 && col == 0 && blockIdx.y == 0) {
         v.x = 0;
         v.y = 0;
       } else {
@@ -341,94 +326,86 @@ __global__ void __launch_bounds__(kStrNT, 1) k_fft_strided(typename CX<T>::t* __
         v.x *= f;
         v.y *= f;
       }
-      buf[e] = v;
+      res[e] = v;
     }
-    __syncthreads();
-    run_fft<C, true, W, kStrNT, kStrCAP>(buf, P, tw);
+    C* other = (res == bufA) ? bufB : bufA;
+    res = run_fft<C, true, W>(res, other, P, tw);
   }
-  for (int e = threadIdx.x; e < tot; e += kStrNT) {
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
     const int w = e % W, m = e / W;
     const int col = c0 + w;
-    if (col < ncol) base[(long long)m * S + col] = buf[e];
+    if (col < ncol) base[(long long)m * S + col] = res[e];
   }
 }
 
 // ---------------------------------------------------------------------------
 // contiguous-axis real transforms: one row per CTA, M = N/2 complex points
 // ---------------------------------------------------------------------------
-template <typename T, int NT, int CAP>
-__global__ void __launch_bounds__(NT) k_fft_r2c(const T* __restrict__ in, typename CX<T>::t* __restrict__ out, FftLen P,
-                                                const typename CX<T>::t* __restrict__ tw,
-                                                const typename CX<T>::t* __restrict__ tw2, long long in_row,
-                                                long long out_row) {
+template <typename T>
+__global__ void __launch_bounds__(128) k_fft_r2c(const T* __restrict__ in, typename CX<T>::t* __restrict__ out, FftLen P,
+                                                 const typename CX<T>::t* __restrict__ tw,
+                                                 const typename CX<T>::t* __restrict__ tw2, long long in_row,
+                                                 long long out_row) {
   typedef typename CX<T>::t C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* Z = reinterpret_cast<C*>(smem_raw);
+  C* bufA = reinterpret_cast<C*>(smem_raw);
+  C* bufB = bufA + P.L;
   const int M = P.L;
   const C* row = reinterpret_cast<const C*>(in + (long long)blockIdx.x * in_row);
-  for (int m = threadIdx.x; m < M; m += NT) cp_async_elem(Z + m, row + m, true);
+  for (int m = threadIdx.x; m < M; m += blockDim.x) cp_async_elem(bufA + m, row + m, true);
   cp_async_wait_all();
-  __syncthreads();
-  run_fft<C, false, 1, NT, CAP>(Z, P, tw);
+  C* Z = run_fft<C, false, 1>(bufA, bufB, P, tw);
   C* o = out + (long long)blockIdx.x * out_row;
   // X[k] = E[k] + w^k O[k],  E = (Z[k] + conj Z[M-k]) / 2,  O = (Z[k] - conj Z[M-k]) / (2i)
-  for (int k = threadIdx.x; k <= M; k += NT) {
+  for (int k = threadIdx.x; k <= M; k += blockDim.x) {
     const C zk = Z[k == M ? 0 : k];
     const C zc = Z[k == 0 ? 0 : M - k];
     C e, od;
     e.x = T(0.5) * (zk.x + zc.x);
     e.y = T(0.5) * (zk.y - zc.y);
+    // (zk - conj(zc)) / (2i) = (a + ib)/(2i) = (b - ia)/2 with a = zk.x - zc.x, b = zk.y + zc.y
     od.x = T(0.5) * (zk.y + zc.y);
     od.y = -T(0.5) * (zk.x - zc.x);
-    const C w = __ldg(tw2 + k);  // exp(-2 pi i k / N)
+    const C w = tw2[k];  // exp(-2 pi i k / N)
     o[k] = cadd(e, cmul(w, od));
   }
 }
 
-template <typename T, int NT, int CAP>
-__global__ void __launch_bounds__(NT) k_fft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, FftLen P,
-                                                const typename CX<T>::t* __restrict__ tw,
-                                                const typename CX<T>::t* __restrict__ tw2, long long in_row,
-                                                long long out_row) {
+template <typename T>
+__global__ void __launch_bounds__(128) k_fft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, FftLen P,
+                                                 const typename CX<T>::t* __restrict__ tw,
+                                                 const typename CX<T>::t* __restrict__ tw2, long long in_row,
+                                                 long long out_row) {
   typedef typename CX<T>::t C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* X = reinterpret_cast<C*>(smem_raw);  // M+1 staged values, Z overwrites X[0..M)
+  C* bufA = reinterpret_cast<C*>(smem_raw);
+  C* bufB = bufA + P.L;
   const int M = P.L;
   const C* Xg = in + (long long)blockIdx.x * in_row;
-  for (int k = threadIdx.x; k <= M; k += NT) cp_async_elem(X + k, Xg + k, true);
+  C* X = bufB;  // staged row (M+1 values; the smem allocation has 2M+2)
+  for (int k = threadIdx.x; k <= M; k += blockDim.x) cp_async_elem(X + k, Xg + k, true);
   cp_async_wait_all();
   __syncthreads();
   // Z[k] = (X[k] + conj X[M-k]) + i (X[k] - conj X[M-k]) exp(+2 pi i k / N)
-  constexpr int MB = (CAP + NT - 1) / NT;
-  C z[MB];
-#pragma unroll
-  for (int s = 0; s < MB; ++s) {
-    const int k = threadIdx.x + s * NT;
-    if (k < M) {
-      const C xk = X[k];
-      const C xc = X[M - k];
-      C fe, d;
-      fe.x = xk.x + xc.x;
-      fe.y = xk.y - xc.y;
-      d.x = xk.x - xc.x;
-      d.y = xk.y + xc.y;
-      C w = __ldg(tw2 + k);
-      w.y = -w.y;
-      const C fo = cmul(d, w);
-      z[s].x = fe.x - fo.y;
-      z[s].y = fe.y + fo.x;
-    }
+  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+    const C xk = X[k];
+    const C xc = X[M - k];
+    C fe, fo, d;
+    fe.x = xk.x + xc.x;
+    fe.y = xk.y - xc.y;
+    d.x = xk.x - xc.x;
+    d.y = xk.y + xc.y;
+    C w = tw2[k];
+    w.y = -w.y;
+    fo = cmul(d, w);
+    C z;
+    z.x = fe.x - fo.y;
+    z.y = fe.y + fo.x;
+    bufA[k] = z;
   }
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < MB; ++s) {
-    const int k = threadIdx.x + s * NT;
-    if (k < M) X[k] = z[s];
-  }
-  __syncthreads();
-  run_fft<C, true, 1, NT, CAP>(X, P, tw);
+  C* z = run_fft<C, true, 1>(bufA, bufB, P, tw);
   C* row = reinterpret_cast<C*>(out + (long long)blockIdx.x * out_row);
-  for (int m = threadIdx.x; m < M; m += NT) row[m] = X[m];
+  for (int m = threadIdx.x; m < M; m += blockDim.x) row[m] = z[m];
 }
 
 // ---------------------------------------------------------------------------
@@ -481,8 +458,7 @@ int fft_upload_twiddles(int L, bool f64, void** dev) {
 
 static int pick_w(int L, size_t csz) {
   int W = 8;
-  while (W > 1 && L * W > kStrCAP) W /= 2;
-  (void)csz;
+  while (W > 1 && 2 * (size_t)L * W * csz > 110 * 1024) W /= 2;
   return W;
 }
 
@@ -491,12 +467,12 @@ static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long 
                           int nbatch, const typename CX<T>::t* tw, const ScaleArgs& sc, cudaStream_t st) {
   typedef typename CX<T>::t C;
   dim3 grid((ncol + W - 1) / W, nbatch);
-  const size_t sm = (size_t)P.L * W * sizeof(C);
+  const size_t sm = 2 * (size_t)P.L * W * sizeof(C);
   switch (W) {
-    case 8: k_fft_strided<T, MODE, 8><<<grid, kStrNT, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
-    case 4: k_fft_strided<T, MODE, 4><<<grid, kStrNT, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
-    case 2: k_fft_strided<T, MODE, 2><<<grid, kStrNT, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
-    default: k_fft_strided<T, MODE, 1><<<grid, kStrNT, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 8: k_fft_strided<T, MODE, 8><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 4: k_fft_strided<T, MODE, 4><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 2: k_fft_strided<T, MODE, 2><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    default: k_fft_strided<T, MODE, 1><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
   }
   SFB_LAUNCH_CHECK("fft strided pass");
   return SFB_OK;
@@ -514,13 +490,8 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   const long long rows = F.total / nlast;
   // 1. R2C along the contiguous axis
   {
-    size_t sm = (size_t)M * csz;
-    if (M <= kRowCAP)
-      k_fft_r2c<T, kRowNT, kRowCAP><<<(unsigned)rows, kRowNT, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half,
-                                                                      (const C*)F.tw_full, nlast, nh);
-    else
-      k_fft_r2c<T, kRowNT2, kRowCAP2><<<(unsigned)rows, kRowNT2, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half,
-                                                                         (const C*)F.tw_full, nlast, nh);
+    size_t sm = 2 * (size_t)M * csz;
+    k_fft_r2c<T><<<(unsigned)rows, 128, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nlast, nh);
     SFB_LAUNCH_CHECK("fft r2c");
   }
   ScaleArgs none{};
@@ -547,13 +518,8 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   }
   // 5. C2R along the contiguous axis
   {
-    size_t sm = ((size_t)M + 1) * csz;
-    if (M <= kRowCAP)
-      k_fft_c2r<T, kRowNT, kRowCAP><<<(unsigned)rows, kRowNT, sm, st>>>(cbuf, rbuf, F.half, (const C*)F.tw_half,
-                                                                      (const C*)F.tw_full, nh, nlast);
-    else
-      k_fft_c2r<T, kRowNT2, kRowCAP2><<<(unsigned)rows, kRowNT2, sm, st>>>(cbuf, rbuf, F.half, (const C*)F.tw_half,
-                                                                         (const C*)F.tw_full, nh, nlast);
+    size_t sm = (2 * (size_t)M + 2) * csz;
+    k_fft_c2r<T><<<(unsigned)rows, 128, sm, st>>>(cbuf, rbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nh, nlast);
     SFB_LAUNCH_CHECK("fft c2r");
   }
   return SFB_OK;
@@ -579,10 +545,8 @@ int fft_set_smem_limits() {
   SFB_SMEM((k_fft_strided<T, 2, 2>));
   SFB_SMEM((k_fft_strided<T, 2, 4>));
   SFB_SMEM((k_fft_strided<T, 2, 8>));
-  SFB_SMEM((k_fft_r2c<T, kRowNT, kRowCAP>));
-  SFB_SMEM((k_fft_c2r<T, kRowNT, kRowCAP>));
-  SFB_SMEM((k_fft_r2c<T, kRowNT2, kRowCAP2>));
-  SFB_SMEM((k_fft_c2r<T, kRowNT2, kRowCAP2>));
+  SFB_SMEM(k_fft_r2c<T>);
+  SFB_SMEM(k_fft_c2r<T>);
 #undef SFB_SMEM
   return cuda_check(e, "cudaFuncSetAttribute(fft smem)");
 }

@@ -352,12 +352,11 @@ static int setup_fft(sfb_solver* s) {
   if (nlast % 2 != 0 || nlast < 2) return SFB_OK;
   FftLen half, ax[3];
   if (!fft_factor(nlast / 2, half)) return SFB_OK;
-  if (nlast / 2 > 2048) return SFB_OK;
+  if (2 * (size_t)(nlast / 2) * csz > 200 * 1024) return SFB_OK;
   for (int a = 0; a < dim - 1; ++a) {
     if (!fft_factor(p->n[a], ax[a])) return SFB_OK;
-    if (p->n[a] > 3584) return SFB_OK;
+    if (2 * (size_t)p->n[a] * csz > 200 * 1024) return SFB_OK;
   }
-  (void)csz;
   int rc;
   if ((rc = (f64 ? fft_set_smem_limits<double>() : fft_set_smem_limits<float>()))) return rc;
   F.dim = dim;
