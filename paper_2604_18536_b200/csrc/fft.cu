@@ -13,7 +13,6 @@
 //   C2R along axis 2 (pre-twiddle + length-n2/2 inverse FFT)
 // (2D: R2C axis 1, fused axis 0, C2R axis 1.)
 #include <cmath>
-#include <cstdlib>
 #include <vector>
 
 #include "sfb_fft.cuh"
@@ -339,87 +338,6 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
   }
 }
 
-// Persistent variant: each CTA walks tiles t = blockIdx.x, +gridDim.x, ...
-// with three tile buffers -- the next tile's cp.async loads land in one while
-// the current tile ping-pongs between the other two -- so HBM traffic keeps
-// flowing during the shared-memory passes.
-template <typename T, int MODE, int W>
-__global__ void __launch_bounds__(512, 1) k_fft_strided_pf(typename CX<T>::t* __restrict__ data, FftLen P, long long S,
-                                                           int ncol, long long bstride, int nbatch,
-                                                           const typename CX<T>::t* __restrict__ tw, ScaleArgs sc) {
-  typedef typename CX<T>::t C;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int L = P.L;
-  const int tot = L * W;
-  C* bufs[3] = {reinterpret_cast<C*>(smem_raw), reinterpret_cast<C*>(smem_raw) + tot,
-                reinterpret_cast<C*>(smem_raw) + 2 * tot};
-  const int ntx = (ncol + W - 1) / W;
-  const int ntiles = ntx * nbatch;
-  auto issue = [&](int t, C* dst) {
-    const int bx = t % ntx, by = t / ntx;
-    const int c0 = bx * W;
-    const C* base = data + (long long)by * bstride;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int w = e % W, m = e / W;
-      const int col = c0 + w;
-      const bool ok = col < ncol;
-      cp_async_elem(dst + e, base + (ok ? (long long)m * S + col : 0), ok);
-    }
-  };
-  int cur = 0, pf = 1, oth = 2;
-  int t = blockIdx.x;
-  if (t < ntiles) issue(t, bufs[cur]);
-  asm volatile("cp.async.commit_group;\n" ::);
-  for (; t < ntiles; t += gridDim.x) {
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) issue(tn, bufs[pf]);
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 1;\n" ::);
-    C* res;
-    if (MODE == 1) res = run_fft<C, true, W>(bufs[cur], bufs[oth], P, tw);
-    else res = run_fft<C, false, W>(bufs[cur], bufs[oth], P, tw);
-    const int bx = t % ntx, by = t / ntx;
-    const int c0 = bx * W;
-    if (MODE == 2) {
-      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int w = e % W, m = e / W;
-        const int col = c0 + w;
-        if (col >= ncol) continue;
-        double lam;
-        if (sc.dim == 3) {
-          const int k1 = col / sc.nh, k2 = col - k1 * sc.nh;
-          lam = (sc.l0[m] + sc.l1[k1]) + sc.l2[k2];
-        } else {
-          lam = sc.l0[m] + sc.l1[col];
-        }
-        C v = res[e];
-        if (m == 0 && col == 0 && by == 0) {
-          v.x = 0;
-          v.y = 0;
-        } else {
-          const T f = T(1) / (T)lam * (T)sc.invN;
-          v.x *= f;
-          v.y *= f;
-        }
-        res[e] = v;
-      }
-      C* other = (res == bufs[cur]) ? bufs[oth] : bufs[cur];
-      res = run_fft<C, true, W>(res, other, P, tw);
-    }
-    C* base = data + (long long)by * bstride;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int w = e % W, m = e / W;
-      const int col = c0 + w;
-      if (col < ncol) base[(long long)m * S + col] = res[e];
-    }
-    __syncthreads();
-    const int tmp = cur;
-    cur = pf;
-    pf = tmp;
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-}
-
 // ---------------------------------------------------------------------------
 // contiguous-axis real transforms: one row per CTA, M = N/2 complex points
 // ---------------------------------------------------------------------------
@@ -548,21 +466,6 @@ template <typename T, int MODE>
 static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long long S, int ncol, long long bstride,
                           int nbatch, const typename CX<T>::t* tw, const ScaleArgs& sc, cudaStream_t st) {
   typedef typename CX<T>::t C;
-  const size_t sm3 = 3 * (size_t)P.L * W * sizeof(C);
-  if (sm3 <= 200 * 1024 && !getenv("SFB_FFT_NOPF")) {
-    static int nsm = 0;
-    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const long long ntiles = (long long)((ncol + W - 1) / W) * nbatch;
-    const int g = (int)(ntiles < nsm ? ntiles : nsm);
-    switch (W) {
-      case 8: k_fft_strided_pf<T, MODE, 8><<<g, 512, sm3, st>>>(data, P, S, ncol, bstride, nbatch, tw, sc); break;
-      case 4: k_fft_strided_pf<T, MODE, 4><<<g, 512, sm3, st>>>(data, P, S, ncol, bstride, nbatch, tw, sc); break;
-      case 2: k_fft_strided_pf<T, MODE, 2><<<g, 512, sm3, st>>>(data, P, S, ncol, bstride, nbatch, tw, sc); break;
-      default: k_fft_strided_pf<T, MODE, 1><<<g, 512, sm3, st>>>(data, P, S, ncol, bstride, nbatch, tw, sc); break;
-    }
-    SFB_LAUNCH_CHECK("fft strided pass (persistent)");
-    return SFB_OK;
-  }
   dim3 grid((ncol + W - 1) / W, nbatch);
   const size_t sm = 2 * (size_t)P.L * W * sizeof(C);
   switch (W) {
@@ -630,18 +533,6 @@ int fft_set_smem_limits() {
   cudaError_t e = cudaSuccess;
 #define SFB_SMEM(K) \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, big)
-  SFB_SMEM((k_fft_strided_pf<T, 0, 1>));
-  SFB_SMEM((k_fft_strided_pf<T, 0, 2>));
-  SFB_SMEM((k_fft_strided_pf<T, 0, 4>));
-  SFB_SMEM((k_fft_strided_pf<T, 0, 8>));
-  SFB_SMEM((k_fft_strided_pf<T, 1, 1>));
-  SFB_SMEM((k_fft_strided_pf<T, 1, 2>));
-  SFB_SMEM((k_fft_strided_pf<T, 1, 4>));
-  SFB_SMEM((k_fft_strided_pf<T, 1, 8>));
-  SFB_SMEM((k_fft_strided_pf<T, 2, 1>));
-  SFB_SMEM((k_fft_strided_pf<T, 2, 2>));
-  SFB_SMEM((k_fft_strided_pf<T, 2, 4>));
-  SFB_SMEM((k_fft_strided_pf<T, 2, 8>));
   SFB_SMEM((k_fft_strided<T, 0, 1>));
   SFB_SMEM((k_fft_strided<T, 0, 2>));
   SFB_SMEM((k_fft_strided<T, 0, 4>));
