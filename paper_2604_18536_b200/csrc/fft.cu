@@ -371,6 +371,60 @@ __global__ void __launch_bounds__(128) k_fft_r2c(const T* __restrict__ in, typen
   }
 }
 
+// R2C of one row of the divergence, computed on the fly from the velocity
+// (operators.py:108-122 fused into the first FFT pass of poisson.py:196):
+// the divergence field is never written to HBM.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) k_fft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, FftLen P,
+                                                     const typename CX<T>::t* __restrict__ tw,
+                                                     const typename CX<T>::t* __restrict__ tw2, long long out_row) {
+  typedef typename CX<T>::t C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* bufA = reinterpret_cast<C*>(smem_raw);
+  C* bufB = bufA + P.L;
+  T* xr = reinterpret_cast<T*>(bufA);
+  const int M = P.L;
+  const int nl = G.n[D - 1];
+  int I[3];
+  if (D == 3) {
+    I[0] = 1 + blockIdx.x / G.n[1];
+    I[1] = 1 + blockIdx.x % G.n[1];
+  } else {
+    I[0] = 1 + blockIdx.x;
+  }
+  const T rd0 = tab(G, 0, T_RDX, I[0]);
+  const T rd1 = D == 3 ? tab(G, 1, T_RDX, I[1]) : T(0);
+  long long rowx = (long long)I[0] * G.s[0] + (D == 3 ? (long long)I[1] * G.s[1] : 0);
+#pragma unroll 2
+  for (int m = threadIdx.x; m < nl; m += 128) {
+    int J[3] = {I[0], I[1], I[2]};
+    J[D - 1] = m + 1;
+    const long long x = rowx + (m + 1);
+    T acc = T(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      T cur, prev;
+      own_pair<T, D>(G, U.c[a], x, J, a, cur, prev);
+      const T r = (a == D - 1) ? tab(G, a, T_RDX, m + 1) : (a == 0 ? rd0 : rd1);
+      acc += (cur - prev) * r;
+    }
+    xr[m] = acc;
+  }
+  C* Z = run_fft<C, false, 1>(bufA, bufB, P, tw);
+  C* o = out + (long long)blockIdx.x * out_row;
+  for (int k = threadIdx.x; k <= M; k += blockDim.x) {
+    const C zk = Z[k == M ? 0 : k];
+    const C zc = Z[k == 0 ? 0 : M - k];
+    C e, od;
+    e.x = T(0.5) * (zk.x + zc.x);
+    e.y = T(0.5) * (zk.y - zc.y);
+    od.x = T(0.5) * (zk.y + zc.y);
+    od.y = -T(0.5) * (zk.x - zc.x);
+    const C w = tw2[k];
+    o[k] = cadd(e, cmul(w, od));
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(128) k_fft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, FftLen P,
                                                  const typename CX<T>::t* __restrict__ tw,
@@ -479,7 +533,7 @@ static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long 
 }
 
 template <typename T>
-int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
+int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u) {
   typedef typename CX<T>::t C;
   C* cbuf = (C*)cbuf_v;
   const size_t csz = sizeof(C);
@@ -491,8 +545,18 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   // 1. R2C along the contiguous axis
   {
     size_t sm = 2 * (size_t)M * csz;
-    k_fft_r2c<T><<<(unsigned)rows, 128, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nlast, nh);
-    SFB_LAUNCH_CHECK("fft r2c");
+    if (G) {
+      CV<T> U;
+      for (int a = 0; a < 3; ++a) U.c[a] = a < dim ? (const T*)u[a] : nullptr;
+      SFB_DISPATCH_DIM(dim, D,
+                       (k_fft_r2c_div<T, D><<<(unsigned)rows, 128, sm, st>>>(*G, U, cbuf, F.half, (const C*)F.tw_half,
+                                                                             (const C*)F.tw_full, nh)));
+      SFB_LAUNCH_CHECK("fft r2c (fused divergence)");
+    } else {
+      k_fft_r2c<T><<<(unsigned)rows, 128, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nlast,
+                                                    nh);
+      SFB_LAUNCH_CHECK("fft r2c");
+    }
   }
   ScaleArgs none{};
   if (dim == 3) {
@@ -524,8 +588,8 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   }
   return SFB_OK;
 }
-template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t);
-template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t);
+template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*);
+template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*);
 
 template <typename T>
 int fft_set_smem_limits() {
@@ -546,6 +610,8 @@ int fft_set_smem_limits() {
   SFB_SMEM((k_fft_strided<T, 2, 4>));
   SFB_SMEM((k_fft_strided<T, 2, 8>));
   SFB_SMEM(k_fft_r2c<T>);
+  SFB_SMEM((k_fft_r2c_div<T, 2>));
+  SFB_SMEM((k_fft_r2c_div<T, 3>));
   SFB_SMEM(k_fft_c2r<T>);
 #undef SFB_SMEM
   return cuda_check(e, "cudaFuncSetAttribute(fft smem)");

@@ -31,21 +31,6 @@ static int cufft_check(cufftResult r, const char* what) {
 // projection kernels
 // ---------------------------------------------------------------------------
 
-// u_a at I and I - e_a along its own axis with boundary entries resolved
-// inline (what fill_ghosts_velocity would have written, fields.py:110-133)
-template <typename T, int D>
-__device__ __forceinline__ void own_pair(const Geo<T>& G, const T* __restrict__ ua, long long x, const int I[3], int a,
-                                         T& cur, T& prev) {
-  const int n = G.n[a];
-  if (G.per[a]) {
-    cur = ua[x];
-    prev = I[a] == 1 ? ua[x + (long long)(n - 1) * G.s[a]] : ua[x - G.s[a]];
-  } else {
-    cur = I[a] == n ? (G.bc_hi[a] == SFB_BC_DIRICHLET ? G.vhi[a][a] : T(0)) : ua[x];
-    prev = I[a] == 1 ? (G.bc_lo[a] == SFB_BC_DIRICHLET ? G.vlo[a][a] : T(0)) : ua[x - G.s[a]];
-  }
-}
-
 // divergence into a contiguous interior array (operators.py:108-122)
 template <typename T, int D>
 __global__ void k_div_int(Geo<T> G, CV<T> U, T* __restrict__ out, Box B) {
@@ -326,10 +311,15 @@ static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) 
   }
   T* rb = (T*)s->rbuf;
   Box B = int_box(G);
-  SFB_DISPATCH_DIM(G.dim, D, (k_div_int<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, C, rb, B)));
-  SFB_LAUNCH_CHECK("projection divergence");
   int rc;
-  if ((rc = solve_inplace<T>(s, rb, st))) return rc;
+  if (s->fft.enabled && !getenv("SFB_NO_DIVFUSE")) {
+    // divergence fused into the first FFT pass
+    if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, (const void* const*)u))) return rc;
+  } else {
+    SFB_DISPATCH_DIM(G.dim, D, (k_div_int<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, C, rb, B)));
+    SFB_LAUNCH_CHECK("projection divergence");
+    if ((rc = solve_inplace<T>(s, rb, st))) return rc;
+  }
   SFB_DISPATCH_DIM(G.dim, D, (k_grad_sub<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, rb, U, B)));
   SFB_LAUNCH_CHECK("gradient subtract");
   if ((rc = launch_planes<T>(G, U, p->dim, 0, st))) return rc;

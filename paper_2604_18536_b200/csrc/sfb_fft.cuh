@@ -33,8 +33,11 @@ struct FftSolve {
 
 bool fft_factor(int L, FftLen& P);
 int fft_upload_twiddles(int L, bool f64, void** dev);
+// Spectral solve in place on rbuf.  When G/u are given, the right-hand side
+// is the divergence of u, computed inside the first (R2C) pass.
 template <typename T>
-int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st);
+int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const Geo<T>* G = nullptr,
+                      const void* const* u = nullptr);
 template <typename T>
 int fft_set_smem_limits();
 

@@ -79,6 +79,21 @@ __device__ __forceinline__ T rhs_comp(const Geo<T>& G, const CV<T>& U, long long
   return v;
 }
 
+// u_a at I and I - e_a along its own axis with boundary entries resolved
+// inline (what fill_ghosts_velocity would have written, fields.py:110-133)
+template <typename T, int D>
+__device__ __forceinline__ void own_pair(const Geo<T>& G, const T* __restrict__ ua, long long x, const int I[3], int a,
+                                         T& cur, T& prev) {
+  const int n = G.n[a];
+  if (G.per[a]) {
+    cur = ua[x];
+    prev = I[a] == 1 ? ua[x + (long long)(n - 1) * G.s[a]] : ua[x - G.s[a]];
+  } else {
+    cur = I[a] == n ? (G.bc_hi[a] == SFB_BC_DIRICHLET ? G.vhi[a][a] : T(0)) : ua[x];
+    prev = I[a] == 1 ? (G.bc_lo[a] == SFB_BC_DIRICHLET ? G.vlo[a][a] : T(0)) : ua[x - G.s[a]];
+  }
+}
+
 template <typename T>
 int launch_planes(const Geo<T>& G, MV<T> U, int ncomp, int mode, cudaStream_t st);
 
