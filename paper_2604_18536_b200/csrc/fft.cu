@@ -373,7 +373,18 @@ __global__ void __launch_bounds__(128) k_fft_r2c(const T* __restrict__ in, typen
 
 // R2C of one row of the divergence, computed on the fly from the velocity
 // (operators.py:108-122 fused into the first FFT pass of poisson.py:196):
-// the divergence field is never written to HBM.
+// the five velocity rows the row's divergence needs are staged into shared
+// memory with cp.async (all in flight at once), the divergence is formed
+// there, and the divergence field is never written to HBM.
+template <typename T>
+__device__ __forceinline__ void cp_async_scalar(T* smem, const T* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+
 template <typename T, int D>
 __global__ void __launch_bounds__(128) k_fft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, FftLen P,
                                                      const typename CX<T>::t* __restrict__ tw,
@@ -385,29 +396,71 @@ __global__ void __launch_bounds__(128) k_fft_r2c_div(Geo<T> G, CV<T> U, typename
   T* xr = reinterpret_cast<T*>(bufA);
   const int M = P.L;
   const int nl = G.n[D - 1];
-  int I[3];
+  T* rows = reinterpret_cast<T*>(bufB + P.L);  // [2*D-1][nl]: a=0 cur/prev, (a=1 cur/prev), last cur
+  int i0, i1 = 0;
   if (D == 3) {
-    I[0] = 1 + blockIdx.x / G.n[1];
-    I[1] = 1 + blockIdx.x % G.n[1];
+    i0 = 1 + blockIdx.x / G.n[1];
+    i1 = 1 + blockIdx.x % G.n[1];
   } else {
-    I[0] = 1 + blockIdx.x;
+    i0 = 1 + blockIdx.x;
   }
-  const T rd0 = tab(G, 0, T_RDX, I[0]);
-  const T rd1 = D == 3 ? tab(G, 1, T_RDX, I[1]) : T(0);
-  long long rowx = (long long)I[0] * G.s[0] + (D == 3 ? (long long)I[1] * G.s[1] : 0);
-#pragma unroll 2
-  for (int m = threadIdx.x; m < nl; m += 128) {
-    int J[3] = {I[0], I[1], I[2]};
-    J[D - 1] = m + 1;
-    const long long x = rowx + (m + 1);
-    T acc = T(0);
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      T cur, prev;
-      own_pair<T, D>(G, U.c[a], x, J, a, cur, prev);
-      const T r = (a == D - 1) ? tab(G, a, T_RDX, m + 1) : (a == 0 ? rd0 : rd1);
-      acc += (cur - prev) * r;
+  // source rows (element k=1 of each row); boundary rows resolved like own_pair
+  const long long sa0 = G.s[0];
+  const long long base = (long long)i0 * G.s[0] + (D == 3 ? (long long)i1 * G.s[1] : 0) + 1;
+  const T* src[5];
+  int nsrc = 0;
+  bool c0_const = false, p0_const = false, c1_const = false, p1_const = false;
+  // axis 0 (component 0)
+  {
+    const int n = G.n[0];
+    src[nsrc++] = U.c[0] + base;  // cur
+    if (G.per[0]) src[nsrc++] = U.c[0] + base + (i0 == 1 ? (long long)(n - 1) * sa0 : -sa0);
+    else src[nsrc++] = U.c[0] + base - sa0;
+    if (!G.per[0]) {
+      c0_const = i0 == n;
+      p0_const = i0 == 1;
     }
+  }
+  if (D == 3) {
+    const int n = G.n[1];
+    const long long sa1 = G.s[1];
+    src[nsrc++] = U.c[1] + base;
+    if (G.per[1]) src[nsrc++] = U.c[1] + base + (i1 == 1 ? (long long)(n - 1) * sa1 : -sa1);
+    else src[nsrc++] = U.c[1] + base - sa1;
+    if (!G.per[1]) {
+      c1_const = i1 == n;
+      p1_const = i1 == 1;
+    }
+  }
+  src[nsrc++] = U.c[D - 1] + base;  // last component along the row
+  for (int r = 0; r < nsrc; ++r)
+    for (int m = threadIdx.x; m < nl; m += 128) cp_async_scalar(rows + r * nl + m, src[r] + m);
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const T rd0 = tab(G, 0, T_RDX, i0);
+  const T rd1 = D == 3 ? tab(G, 1, T_RDX, i1) : T(0);
+  const T* rl = rows + (nsrc - 1) * nl;
+  const int al = D - 1;
+  for (int m = threadIdx.x; m < nl; m += 128) {
+    T c = c0_const ? (G.bc_hi[0] == SFB_BC_DIRICHLET ? G.vhi[0][0] : T(0)) : rows[m];
+    T pv = p0_const ? (G.bc_lo[0] == SFB_BC_DIRICHLET ? G.vlo[0][0] : T(0)) : rows[nl + m];
+    T acc = (c - pv) * rd0;
+    if (D == 3) {
+      c = c1_const ? (G.bc_hi[1] == SFB_BC_DIRICHLET ? G.vhi[1][1] : T(0)) : rows[2 * nl + m];
+      pv = p1_const ? (G.bc_lo[1] == SFB_BC_DIRICHLET ? G.vlo[1][1] : T(0)) : rows[3 * nl + m];
+      acc += (c - pv) * rd1;
+    }
+    // last axis: within the row
+    T cl, pl;
+    if (G.per[al]) {
+      cl = rl[m];
+      pl = rl[m == 0 ? nl - 1 : m - 1];
+    } else {
+      cl = m == nl - 1 ? (G.bc_hi[al] == SFB_BC_DIRICHLET ? G.vhi[al][al] : T(0)) : rl[m];
+      pl = m == 0 ? (G.bc_lo[al] == SFB_BC_DIRICHLET ? G.vlo[al][al] : T(0)) : rl[m - 1];
+    }
+    acc += (cl - pl) * tab(G, al, T_RDX, m + 1);
     xr[m] = acc;
   }
   C* Z = run_fft<C, false, 1>(bufA, bufB, P, tw);
@@ -548,9 +601,10 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
     if (G) {
       CV<T> U;
       for (int a = 0; a < 3; ++a) U.c[a] = a < dim ? (const T*)u[a] : nullptr;
+      const size_t smd = sm + (size_t)(2 * dim - 1) * nlast * sizeof(T);
       SFB_DISPATCH_DIM(dim, D,
-                       (k_fft_r2c_div<T, D><<<(unsigned)rows, 128, sm, st>>>(*G, U, cbuf, F.half, (const C*)F.tw_half,
-                                                                             (const C*)F.tw_full, nh)));
+                       (k_fft_r2c_div<T, D><<<(unsigned)rows, 128, smd, st>>>(*G, U, cbuf, F.half, (const C*)F.tw_half,
+                                                                              (const C*)F.tw_full, nh)));
       SFB_LAUNCH_CHECK("fft r2c (fused divergence)");
     } else {
       k_fft_r2c<T><<<(unsigned)rows, 128, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nlast,
