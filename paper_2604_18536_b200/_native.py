@@ -141,7 +141,7 @@ def call(name, *args):
     k = KERNELS_PER_CALL.get(name, 0)
     if name in ("sfb_project", "sfb_project_pullback", "sfb_solver_solve"):
         own = lib.sfb_solver_uses_own_fft(args[0])
-        k += (3 if own else 0) if name == "sfb_project" else (4 if own else 0)
+        k += 4 if own else 0
     if name == "sfb_project" and args[2] is not None and args[2] != 0:
         k += 1  # extended pressure written
     launches += k

@@ -13,6 +13,7 @@
 //   C2R along axis 2 (pre-twiddle + length-n2/2 inverse FFT)
 // (2D: R2C axis 1, fused axis 0, C2R axis 1.)
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "sfb_fft.cuh"
@@ -564,7 +565,8 @@ int fft_upload_twiddles(int L, bool f64, void** dev) {
 }
 
 static int pick_w(int L, size_t csz) {
-  int W = 8;
+  static int wmax = getenv("SFB_FFT_WMAX") ? atoi(getenv("SFB_FFT_WMAX")) : 8;
+  int W = wmax;
   while (W > 1 && 2 * (size_t)L * W * csz > 110 * 1024) W /= 2;
   return W;
 }
