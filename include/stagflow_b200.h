@@ -37,7 +37,9 @@ extern "C" {
 
 enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4 };
 enum { SFB_F64 = 0, SFB_F32 = 1 };
-enum { SFB_BC_PERIODIC = 0, SFB_BC_DIRICHLET = 1, SFB_BC_SYMMETRIC = 2 };
+/* SFB_BC_HALO: ghost planes of this axis are supplied by the caller (the
+ * neighbouring z-slab of a multi-GPU decomposition); DOFs as periodic. */
+enum { SFB_BC_PERIODIC = 0, SFB_BC_DIRICHLET = 1, SFB_BC_SYMMETRIC = 2, SFB_BC_HALO = 3 };
 enum { SFB_SOLVER_SPECTRAL = 0, SFB_SOLVER_CHANNEL = 1 };
 
 /* Per-axis host tables, packed axis by axis, each of length n[a]+2, in this
@@ -127,6 +129,23 @@ int sfb_solver_uses_own_fft(const sfb_solver* s);
 int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream);
 /* Full projection of u in place; p_ext (extended, ghosts filled) optional. */
 int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream);
+
+/* Slab-decomposed spectral solve (multi-GPU, axis 0 split over nranks; the
+ * plan's axis 0 is SFB_BC_HALO).  One projection =
+ *   sfb_slab_forward  : divergence -> R2C (axis 2) -> FFT axis 1   -> spec
+ *   caller            : all-to-all spec (m, n1, nh) -> trans (n0, n1/P, nh)
+ *   sfb_slab_axis0    : FFT axis 0 -> 1/(Lambda N) -> inverse FFT axis 0 on trans
+ *   caller            : all-to-all back trans -> spec
+ *   sfb_slab_inverse  : inverse FFT axis 1 -> C2R -> local pressure (m planes)
+ *   caller            : copy the next slab's first pressure plane into p_halo
+ *   sfb_slab_correct  : u -= G p (uses p_halo), fill non-halo ghosts, p_ext
+ * (poisson.py:167-200, 321-341 split at the two transposes.) */
+int sfb_slab_solver_create(sfb_plan* plan, int n0_global, int rank, int nranks, sfb_solver** out);
+int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** p_local, void** p_halo);
+int sfb_slab_forward(sfb_solver* s, void* const* u, void* stream);
+int sfb_slab_axis0(sfb_solver* s, void* stream);
+int sfb_slab_inverse(sfb_solver* s, void* stream);
+int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream);
 
 /* Pullbacks (adjoint.py:114-349), periodic grids. Mutating semantics of the
  * reference are kept: divergence_pullback zeroes pbar's ghosts;

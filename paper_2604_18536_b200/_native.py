@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libstagflow_b200.so")
 
 SFB_OK, SFB_EINVAL, SFB_ECONFIG, SFB_ENUMERIC, SFB_ECUDA = range(5)
 SFB_F64, SFB_F32 = 0, 1
-SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC = 0, 1, 2
+SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC, SFB_BC_HALO = 0, 1, 2, 3
 SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL = 0, 1
 SFB_NTAB = 10
 ABI_VERSION = 1
@@ -75,6 +75,12 @@ _SIGS = {
     "sfb_solver_uses_own_fft": [vp],
     "sfb_solver_solve": [vp, vp, vp, vp],
     "sfb_project": [vp, VP3, vp, vp],
+    "sfb_slab_solver_create": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
+    "sfb_slab_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
+    "sfb_slab_forward": [vp, VP3, vp],
+    "sfb_slab_axis0": [vp, vp],
+    "sfb_slab_inverse": [vp, vp],
+    "sfb_slab_correct": [vp, VP3, vp, vp],
     "sfb_divergence_pullback": [vp, vp, VP3, vp],
     "sfb_pressure_gradient_pullback": [vp, VP3, vp, vp],
     "sfb_diffusion_pullback": [vp, VP3, ctypes.c_double, VP3, vp],
@@ -131,6 +137,7 @@ KERNELS_PER_CALL = {
     "sfb_weighted_inner": 2, "sfb_cfl_conv": 2, "sfb_solver_solve": 1, "sfb_project": 4,
     "sfb_divergence_pullback": 2, "sfb_pressure_gradient_pullback": 2, "sfb_diffusion_pullback": 2,
     "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4,
+    "sfb_slab_forward": 3, "sfb_slab_axis0": 1, "sfb_slab_inverse": 2, "sfb_slab_correct": 2,
 }
 launches = 0
 

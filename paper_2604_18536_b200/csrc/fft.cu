@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
       if (sc.dim == 3) lam = (sc.l0[m] + sc.l1[k1]) + sc.l2[k2];
       else lam = sc.l0[m] + sc.l1[col];
       C v = res[e];
-      if (m == 0 && col == 0 && blockIdx.y == 0) {
+      if (m == 0 && col == 0 && blockIdx.y == 0 && sc.zero_ok) {
         v.x = 0;
         v.y = 0;
       } else {
@@ -646,6 +646,50 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
 }
 template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*);
 template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*);
+
+// ---- slab-decomposed pieces (multi-GPU): F.n = {m local planes, n1, n2},
+// F.ax[0] is the global axis-0 length, F.sc.l1 offset to this rank's k1 chunk.
+template <typename T>
+int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  C* cbuf = (C*)cbuf_v;
+  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], M = nlast / 2, nh = M + 1;
+  const long long rows = (long long)m * n1;
+  k_fft_r2c<T><<<(unsigned)rows, 128, 2 * (size_t)M * sizeof(C), st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half,
+                                                                       (const C*)F.tw_full, nlast, nh);
+  SFB_LAUNCH_CHECK("slab r2c");
+  ScaleArgs none{};
+  return launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                              (const C*)F.tw_ax[1], none, st);
+}
+template <typename T>
+int fft_slab_axis0(FftSolve& F, void* tbuf_v, int n1_chunk, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  const int nh = F.n[2] / 2 + 1;
+  const int ncol = n1_chunk * nh;
+  return launch_strided<T, 2>((C*)tbuf_v, F.ax[0], pick_w(F.ax[0].L, sizeof(C)), ncol, ncol, 0, 1,
+                              (const C*)F.tw_ax[0], F.sc, st);
+}
+template <typename T>
+int fft_slab_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  C* cbuf = (C*)cbuf_v;
+  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], M = nlast / 2, nh = M + 1;
+  ScaleArgs none{};
+  int rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                                (const C*)F.tw_ax[1], none, st);
+  if (rc) return rc;
+  k_fft_c2r<T><<<(unsigned)((long long)m * n1), 128, (2 * (size_t)M + 2) * sizeof(C), st>>>(
+      cbuf, rbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nh, nlast);
+  SFB_LAUNCH_CHECK("slab c2r");
+  return SFB_OK;
+}
+template int fft_slab_forward<double>(FftSolve&, double*, void*, cudaStream_t);
+template int fft_slab_forward<float>(FftSolve&, float*, void*, cudaStream_t);
+template int fft_slab_axis0<double>(FftSolve&, void*, int, cudaStream_t);
+template int fft_slab_axis0<float>(FftSolve&, void*, int, cudaStream_t);
+template int fft_slab_inverse<double>(FftSolve&, void*, double*, cudaStream_t);
+template int fft_slab_inverse<float>(FftSolve&, void*, float*, cudaStream_t);
 
 template <typename T>
 int fft_set_smem_limits() {

@@ -32,7 +32,8 @@ static void fill_geo(Geo<T>& G, const sfb_plan* p, const T* dtab) {
   for (int a = 0; a < 3; ++a) {
     G.n[a] = a < p->dim ? p->n[a] : 1;
     G.E[a] = a < p->dim ? p->n[a] + 2 : 1;
-    G.per[a] = a < p->dim ? (p->bc_lo[a] == SFB_BC_PERIODIC) : 1;
+    G.per[a] = a < p->dim ? (p->bc_lo[a] == SFB_BC_PERIODIC || p->bc_lo[a] == SFB_BC_HALO) : 1;
+    G.halo[a] = a < p->dim ? (p->bc_lo[a] == SFB_BC_HALO) : 0;
     G.bc_lo[a] = p->bc_lo[a];
     G.bc_hi[a] = p->bc_hi[a];
     for (int c = 0; c < 3; ++c) {
@@ -81,10 +82,13 @@ int sfb_plan_create(const sfb_grid_desc* d, sfb_plan** out) {
     if (d->n[a] < 1) return fail(SFB_EINVAL, "need at least one volume per axis");
     bool plo = d->bc_lo[a] == SFB_BC_PERIODIC, phi = d->bc_hi[a] == SFB_BC_PERIODIC;
     if (plo != phi) return fail(SFB_EINVAL, "periodic must be declared on both sides or neither");
-    if (!plo && d->n[a] < 2) return fail(SFB_ECONFIG, "a wall axis needs at least two volumes");
+    if ((d->bc_lo[a] == SFB_BC_HALO) != (d->bc_hi[a] == SFB_BC_HALO))
+      return fail(SFB_EINVAL, "halo must be declared on both sides or neither");
+    const bool wall = !plo && d->bc_lo[a] != SFB_BC_HALO;
+    if (wall && d->n[a] < 2) return fail(SFB_ECONFIG, "a wall axis needs at least two volumes");
     for (int s = 0; s < 2; ++s) {
       int k = s ? d->bc_hi[a] : d->bc_lo[a];
-      if (k < 0 || k > 2) return fail(SFB_EINVAL, "unknown boundary kind");
+      if (k < 0 || k > 3) return fail(SFB_EINVAL, "unknown boundary kind");
     }
   }
   if (!d->tables) return fail(SFB_EINVAL, "missing grid tables");

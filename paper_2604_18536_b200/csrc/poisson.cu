@@ -70,8 +70,9 @@ __global__ void k_grad_sub(Geo<T> G, const T* __restrict__ p, MV<T> U, Box B) {
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     if (!is_udof<T, D>(G, I, a)) continue;
-    // only periodic axes reach I_a = n for their own component
-    const long long on = I[a] == G.n[a] ? o - (long long)(G.n[a] - 1) * ps[a] : o + ps[a];
+    // only periodic axes reach I_a = n for their own component; a halo axis
+    // reads the next slab's first plane, stored after the local planes
+    const long long on = (I[a] == G.n[a] && !G.halo[a]) ? o - (long long)(G.n[a] - 1) * ps[a] : o + ps[a];
     const T g = (p[on] - pc) * tab(G, a, T_RDU, I[a]);
     U.c[a][x] -= g;
   }
@@ -87,6 +88,11 @@ __global__ void k_p_ext(Geo<T> G, const T* __restrict__ p, T* __restrict__ pe, B
   for (int a = 0; a < D; ++a) {
     const int n = G.n[a];
     int i = I[a];
+    if (G.halo[a]) {
+      if (i == 0) return;  // previous slab's plane: exchanged by the caller
+      J[a] = i - 1;        // i == n + 1 reads the halo plane stored after the slab
+      continue;
+    }
     if (i == 0) i = G.per[a] ? n : 1;
     else if (i == n + 1) i = G.per[a] ? 1 : n;
     J[a] = i - 1;
@@ -365,6 +371,7 @@ static int setup_fft(sfb_solver* s) {
   F.sc.l1 = s->lam[1];
   F.sc.l2 = s->lam[2];
   F.sc.invN = 1.0 / (double)p->int_count;
+  F.sc.zero_ok = 1;
   F.enabled = true;
   return SFB_OK;
 }
@@ -464,7 +471,7 @@ int sfb_solver_destroy(sfb_solver* s) {
   if (!s) return SFB_OK;
   if (s->has_fwd) cufftDestroy(s->fwd);
   if (s->has_inv) cufftDestroy(s->inv);
-  void* bufs[] = {s->work, s->rbuf, s->cbuf, s->cprime, s->dscr, s->lam[0], s->lam[1], s->lam[2],
+  void* bufs[] = {s->tbuf, s->work, s->rbuf, s->cbuf, s->cprime, s->dscr, s->lam[0], s->lam[1], s->lam[2],
                   s->up, s->lo, s->di, s->dxy, s->tmp, s->fft.tw_half, s->fft.tw_full,
                   s->fft.tw_ax[0], s->fft.tw_ax[1], s->fft.tw_ax[2]};
   for (void* b : bufs)
@@ -491,6 +498,150 @@ int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream) {
     if (!u[a]) return fail(SFB_EINVAL, "null velocity component");
   return s->plan->dtype == SFB_F64 ? project<double>(s, u, p_ext, (cudaStream_t)stream)
                                    : project<float>(s, u, p_ext, (cudaStream_t)stream);
+}
+
+
+// ---------------------------------------------------------------------------
+// slab-decomposed spectral solve (multi-GPU)
+// ---------------------------------------------------------------------------
+int sfb_slab_solver_create(sfb_plan* p, int n0g, int rank, int nranks, sfb_solver** out) {
+  if (!p || !out) return fail(SFB_EINVAL, "null argument");
+  *out = nullptr;
+  if (p->dim != 3 || p->bc_lo[0] != SFB_BC_HALO || p->bc_lo[1] != SFB_BC_PERIODIC || p->bc_lo[2] != SFB_BC_PERIODIC)
+    return fail(SFB_ECONFIG, "slab solver needs a 3D plan with a halo axis 0 and periodic axes 1, 2");
+  const int m = p->n[0], n1 = p->n[1], n2 = p->n[2];
+  if (nranks < 1 || rank < 0 || rank >= nranks || n0g != m * nranks || n1 % nranks != 0 || n2 % 2 != 0)
+    return fail(SFB_ECONFIG, "slab solver needs n0 = m*P, n1 % P == 0 and an even n2");
+  for (int a = 1; a < 3; ++a)
+    if (!axis_uniform(p->hdx[a])) return fail(SFB_ECONFIG, "spectral pressure solver requires uniform axes");
+  FftLen half, a0, a1;
+  if (!fft_factor(n2 / 2, half) || !fft_factor(n0g, a0) || !fft_factor(n1, a1) || n0g > 3584 || n1 > 3584 ||
+      n2 / 2 > 2048)
+    return fail(SFB_ECONFIG, "slab solver: axis lengths must factor into 2, 3, 5, 7");
+  sfb_solver* s = new sfb_solver();
+  s->plan = p;
+  s->kind = SFB_SOLVER_SPECTRAL;
+  s->slab = true;
+  s->n0g = n0g;
+  s->rank = rank;
+  s->nranks = nranks;
+  const bool f64 = p->dtype == SFB_F64;
+  const size_t esz = f64 ? 8 : 4;
+  const long long nh = n2 / 2 + 1;
+  const long long ncomplex = (long long)m * n1 * nh;
+  int rc;
+  double h[3] = {p->width0[0], p->width0[1], p->width0[2]};
+  int ng[3] = {n0g, n1, n2};
+  FftSolve& F = s->fft;
+  if ((rc = cuda_check(cudaMalloc(&s->rbuf, esz * (size_t)(m + 1) * n1 * n2), "cudaMalloc(rbuf)"))) goto bad;
+  if ((rc = cuda_check(cudaMalloc(&s->cbuf, 2 * esz * ncomplex), "cudaMalloc(spec)"))) goto bad;
+  if ((rc = cuda_check(cudaMalloc(&s->tbuf, 2 * esz * ncomplex), "cudaMalloc(trans)"))) goto bad;
+  for (int a = 0; a < 3; ++a) {
+    std::vector<double> lam(ng[a]);
+    for (int k = 0; k < ng[a]; ++k) lam[k] = (2.0 * std::cos(2.0 * M_PI * k / ng[a]) - 2.0) / (h[a] * h[a]);
+    if ((rc = cuda_check(cudaMalloc(&s->lam[a], sizeof(double) * ng[a]), "cudaMalloc(lam)"))) goto bad;
+    if ((rc = cuda_check(cudaMemcpy(s->lam[a], lam.data(), sizeof(double) * ng[a], cudaMemcpyHostToDevice), "upload")))
+      goto bad;
+  }
+  if ((rc = (f64 ? fft_set_smem_limits<double>() : fft_set_smem_limits<float>()))) goto bad;
+  F.dim = 3;
+  F.n[0] = m;
+  F.n[1] = n1;
+  F.n[2] = n2;
+  F.total = (long long)m * n1 * n2;
+  F.half = half;
+  F.ax[0] = a0;
+  F.ax[1] = a1;
+  if ((rc = fft_upload_twiddles(n0g, f64, &F.tw_ax[0]))) goto bad;
+  if ((rc = fft_upload_twiddles(n1, f64, &F.tw_ax[1]))) goto bad;
+  if ((rc = fft_upload_twiddles(n2 / 2, f64, &F.tw_half))) goto bad;
+  if ((rc = fft_upload_twiddles(n2, f64, &F.tw_full))) goto bad;
+  F.sc.dim = 3;
+  F.sc.nh = (int)nh;
+  F.sc.l0 = s->lam[0];
+  F.sc.l1 = s->lam[1] + (long long)rank * (n1 / nranks);
+  F.sc.l2 = s->lam[2];
+  F.sc.invN = 1.0 / ((double)n0g * n1 * n2);
+  F.sc.zero_ok = rank == 0;
+  F.enabled = true;
+  *out = s;
+  return SFB_OK;
+bad:
+  sfb_solver_destroy(s);
+  return rc;
+}
+
+int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** p_local, void** p_halo) {
+  if (!s || !s->slab) return fail(SFB_EINVAL, "not a slab solver");
+  sfb_plan* p = s->plan;
+  const size_t esz = p->dtype == SFB_F64 ? 8 : 4;
+  if (spec) *spec = s->cbuf;
+  if (trans) *trans = s->tbuf;
+  if (p_local) *p_local = s->rbuf;
+  if (p_halo) *p_halo = (char*)s->rbuf + esz * (size_t)p->n[0] * p->n[1] * p->n[2];
+  return SFB_OK;
+}
+
+}  // extern "C"
+
+namespace sfb {
+template <typename T>
+static int slab_forward(sfb_solver* s, void* const* u, cudaStream_t st) {
+  sfb_plan* p = s->plan;
+  const Geo<T>& G = geo<T>(p);
+  CV<T> C;
+  for (int a = 0; a < 3; ++a) C.c[a] = (const T*)u[a];
+  Box B = int_box(G);
+  k_div_int<T, 3><<<box_grid(3, B), box_block(3), 0, st>>>(G, C, (T*)s->rbuf, B);
+  SFB_LAUNCH_CHECK("slab divergence");
+  return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st);
+}
+
+template <typename T>
+static int slab_correct(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) {
+  sfb_plan* p = s->plan;
+  const Geo<T>& G = geo<T>(p);
+  MV<T> U;
+  for (int a = 0; a < 3; ++a) U.c[a] = (T*)u[a];
+  Box B = int_box(G);
+  k_grad_sub<T, 3><<<box_grid(3, B), box_block(3), 0, st>>>(G, (const T*)s->rbuf, U, B);
+  SFB_LAUNCH_CHECK("slab gradient subtract");
+  int rc = launch_planes<T>(G, U, 3, 0, st);
+  if (rc) return rc;
+  if (p_ext) {
+    Box E = ext_box(G);
+    k_p_ext<T, 3><<<box_grid(3, E), box_block(3), 0, st>>>(G, (const T*)s->rbuf, (T*)p_ext, E);
+    SFB_LAUNCH_CHECK("slab pressure");
+  }
+  return SFB_OK;
+}
+}  // namespace sfb
+
+extern "C" {
+
+int sfb_slab_forward(sfb_solver* s, void* const* u, void* stream) {
+  if (!s || !s->slab || !u || !u[0] || !u[1] || !u[2]) return fail(SFB_EINVAL, "bad slab call");
+  return s->plan->dtype == SFB_F64 ? slab_forward<double>(s, u, (cudaStream_t)stream)
+                                   : slab_forward<float>(s, u, (cudaStream_t)stream);
+}
+
+int sfb_slab_axis0(sfb_solver* s, void* stream) {
+  if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
+  const int chunk = s->plan->n[1] / s->nranks;
+  return s->plan->dtype == SFB_F64 ? fft_slab_axis0<double>(s->fft, s->tbuf, chunk, (cudaStream_t)stream)
+                                   : fft_slab_axis0<float>(s->fft, s->tbuf, chunk, (cudaStream_t)stream);
+}
+
+int sfb_slab_inverse(sfb_solver* s, void* stream) {
+  if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
+  return s->plan->dtype == SFB_F64 ? fft_slab_inverse<double>(s->fft, s->cbuf, (double*)s->rbuf, (cudaStream_t)stream)
+                                   : fft_slab_inverse<float>(s->fft, s->cbuf, (float*)s->rbuf, (cudaStream_t)stream);
+}
+
+int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream) {
+  if (!s || !s->slab || !u || !u[0] || !u[1] || !u[2]) return fail(SFB_EINVAL, "bad slab call");
+  return s->plan->dtype == SFB_F64 ? slab_correct<double>(s, u, p_ext, (cudaStream_t)stream)
+                                   : slab_correct<float>(s, u, p_ext, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -21,7 +21,8 @@ struct Geo {
   int n[3];        // interior extents
   int E[3];        // extended extents (n+2); unused axes = 1
   long long s[3];  // element strides of the extended array
-  int per[3];      // periodic flags
+  int per[3];      // periodic flags (DOF semantics; also set for halo axes)
+  int halo[3];     // ghost planes supplied externally (slab decomposition)
   int bc_lo[3], bc_hi[3];
   T c2lo[3][3], c2hi[3][3];  // (T)(2*val) for tangential reflections [axis][comp]
   T vlo[3][3], vhi[3][3];    // (T)val for normal boundary faces

@@ -16,6 +16,7 @@ struct ScaleArgs {
   int nh;                     // half-spectrum extent of the last axis (3D column split)
   const double *l0, *l1, *l2; // per-axis eigenvalue tables (fp64)
   double invN;                // 1 / (n0 n1 n2): the irfftn normalisation
+  int zero_ok;                // this chunk holds the k = 0 mode (zeroed)
 };
 
 struct FftSolve {
@@ -40,5 +41,11 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const G
                       const void* const* u = nullptr);
 template <typename T>
 int fft_set_smem_limits();
+template <typename T>
+int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st);
+template <typename T>
+int fft_slab_axis0(FftSolve& F, void* tbuf, int n1_chunk, cudaStream_t st);
+template <typename T>
+int fft_slab_inverse(FftSolve& F, void* cbuf, T* rbuf, cudaStream_t st);
 
 }  // namespace sfb

@@ -85,7 +85,10 @@ template <typename T, int D>
 __device__ __forceinline__ void own_pair(const Geo<T>& G, const T* __restrict__ ua, long long x, const int I[3], int a,
                                          T& cur, T& prev) {
   const int n = G.n[a];
-  if (G.per[a]) {
+  if (G.halo[a]) {
+    cur = ua[x];
+    prev = ua[x - G.s[a]];  // ghost plane supplied by the neighbouring slab
+  } else if (G.per[a]) {
     cur = ua[x];
     prev = I[a] == 1 ? ua[x + (long long)(n - 1) * G.s[a]] : ua[x - G.s[a]];
   } else {

@@ -37,4 +37,8 @@ struct sfb_solver {
   double *up = nullptr, *lo = nullptr, *di = nullptr, *dxy = nullptr;
   void* tmp = nullptr;       // pullback scratch (extended scalar)
   sfb::FftSolve fft;         // hand-written FFT path (spectral), when supported
+  // slab decomposition (multi-GPU)
+  bool slab = false;
+  int n0g = 0, rank = 0, nranks = 1;
+  void* tbuf = nullptr;      // transposed spectrum (n0 global, n1/P, nh)
 };

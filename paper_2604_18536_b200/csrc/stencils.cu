@@ -38,7 +38,9 @@ __device__ __forceinline__ T ghost_value(const Geo<T>& G, const T* __restrict__ 
     signed char s = 1;
     T k = T(0);
     bool tgt = false;
-    if (G.per[a]) {
+    if (G.halo[a]) {
+      // ghost planes supplied by the neighbouring slab: not a fill target
+    } else if (G.per[a]) {
       if (i == 0) { tgt = true; src = n; }
       else if (i == n + 1) { tgt = true; src = 1; }
     } else if (scalar) {
@@ -122,6 +124,7 @@ static PlaneSet make_planes(const Geo<T>& G, int ncomp, bool boundary_faces) {
   P.count = 0;
   for (int c = 0; c < ncomp; ++c)
     for (int a = 0; a < G.dim; ++a) {
+      if (G.halo[a]) continue;
       int idxs[3] = {0, G.n[a] + 1, G.n[a]};
       int ni = (boundary_faces && !G.per[a] && c == a) ? 3 : 2;
       int sz = 1;
@@ -141,6 +144,7 @@ static PlaneSet make_planes(const Geo<T>& G, int ncomp, bool boundary_faces) {
 template <typename T>
 int launch_planes(const Geo<T>& G, MV<T> U, int ncomp, int mode, cudaStream_t st) {
   PlaneSet P = make_planes(G, ncomp, mode != 1);
+  if (P.count == 0) return SFB_OK;
   int mx = 0;
   for (int i = 0; i < P.count; ++i) mx = P.size[i] > mx ? P.size[i] : mx;
   dim3 grid((mx + 255) / 256, P.count);

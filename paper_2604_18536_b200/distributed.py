@@ -1,0 +1,323 @@
+"""Multi-GPU z-slab decomposition of the RK4 time-step path.
+
+The periodic box is split along axis 0 (the slowest storage axis -- the
+survey's "z" in its [z][y][x] naming) into P slabs of m = n0/P planes, one
+process per GPU (``torch.distributed``, NCCL over NVLink).  Per projection:
+
+    halo(u)            exchange the +-1 ghost planes of u with the neighbours
+    forward            divergence -> R2C (axis 2) -> FFT axis 1 (local)
+    all_to_all         spectrum (m, n1, nh) -> transposed (n0, n1/P, nh)
+    axis0              FFT axis 0 -> 1/(Lambda N) -> inverse FFT axis 0
+    all_to_all         back to (m, n1, nh)
+    inverse            inverse FFT axis 1 -> C2R (local pressure)
+    p halo             next slab's first pressure plane
+    correct            u -= G p, ghost fill of axes 1, 2
+    halo(u)            for the next stencil
+
+The RHS stencils reach +-1 plane, so the fused RK-stage kernel only needs the
+ghost planes exchanged after every projection.  Kinetic energy and CFL use
+an all-reduce.  The reference is single-process; this
+is the paper's outlook built B200-first.
+
+The local compute is a ``backend`` object: ``CudaSlabBackend`` calls the C
+ABI (``sfb_slab_*``, ``sfb_rk_stage``); the CPU gloo tests plug in a numpy
+backend so the orchestration (slab bookkeeping, halo directions, all-to-all
+packing) is exercised with world_size 2 on CPU.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .fields import VelocityField
+from .grid import AxisCoords, Grid
+
+
+class SlabLayout:
+    """Which planes of axis 0 this rank owns (host bookkeeping only)."""
+
+    def __init__(self, n0, rank, size):
+        if n0 % size:
+            raise ValueError(f"n0={n0} must be divisible by the number of ranks {size}")
+        self.n0, self.rank, self.size = n0, rank, size
+        self.m = n0 // size
+        self.i0 = rank * self.m  # first owned interior plane is global index i0 + 1
+        self.prev = (rank - 1) % size
+        self.next = (rank + 1) % size
+
+    def global_planes(self):
+        return range(self.i0 + 1, self.i0 + self.m + 1)
+
+
+class SlabGrid(Grid):
+    """The local slab of a global grid: axis-0 tables sliced from the global
+    extended tables (ghost widths are the neighbours' widths)."""
+
+    def __init__(self, global_grid, layout):
+        g = global_grid
+        m, i0 = layout.m, layout.i0
+        b0 = g.axes[0].boundaries[i0:i0 + m + 1]
+        super().__init__((AxisCoords(b0),) + tuple(g.axes[1:]), g.periodic, dtype=g.dtype)
+        self.global_grid = g
+        self.layout = layout
+        sl = slice(i0, i0 + m + 2)
+        self.dx = [g.dx[0][sl].copy()] + list(g.dx[1:])
+        self.du = [g.du[0][sl].copy()] + list(g.du[1:])
+        self.xb = [g.xb[0][sl].copy()] + list(g.xb[1:])
+        self.xc = [g.xc[0][sl].copy()] + list(g.xc[1:])
+
+    def packed_tables(self):
+        if self._packed is None:
+            full = self.global_grid.packed_tables()
+            g = self.global_grid
+            E0 = g.shape[0] + 2
+            i0, m = self.layout.i0, self.layout.m
+            parts = [full[t * E0 + i0: t * E0 + i0 + m + 2] for t in range(N.SFB_NTAB)]
+            parts.append(full[N.SFB_NTAB * E0:])
+            self._packed = np.ascontiguousarray(np.concatenate(parts))
+        return self._packed
+
+
+# ---------------------------------------------------------------------------
+# communication
+# ---------------------------------------------------------------------------
+class Comm:
+    """Halo exchange, all-to-all and all-reduce over a process group.
+    ``stage_host=True`` stages CUDA tensors through host memory (gloo)."""
+
+    def __init__(self, layout, group=None, stage_host=False):
+        self.layout = layout
+        self.group = group
+        self.stage_host = stage_host
+
+    def _send_recv(self, send, recv, dst, src):
+        if self.layout.size == 1:
+            recv.copy_(send)
+            return
+        s = send.cpu() if self.stage_host else send.contiguous()
+        r = torch.empty_like(s) if self.stage_host else recv
+        ops = [dist.P2POp(dist.isend, s, dst, self.group), dist.P2POp(dist.irecv, r, src, self.group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        if self.stage_host:
+            recv.copy_(r)
+
+    def halo(self, tensors):
+        """Ghost planes along axis 0: plane 0 <- prev's last plane,
+        plane m+1 <- next's first plane."""
+        lay = self.layout
+        m = lay.m
+        for t in tensors:
+            self._send_recv(t[m], t[0], lay.next, lay.prev)
+            self._send_recv(t[1], t[m + 1], lay.prev, lay.next)
+
+    def plane_from_next(self, send_plane, recv_plane):
+        self._send_recv(send_plane, recv_plane, self.layout.prev, self.layout.next)
+
+    def all_to_all(self, out, inp):
+        if self.layout.size == 1:
+            out.copy_(inp)
+            return
+        if self.stage_host:
+            o = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, group=self.group)
+
+    def allreduce(self, value, op="sum"):
+        if self.layout.size == 1:
+            return value
+        t = torch.tensor([value], dtype=torch.float64)
+        if not self.stage_host and torch.cuda.is_available() and dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MIN, group=self.group)
+        return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CUDA backend (C ABI)
+# ---------------------------------------------------------------------------
+class _DevBuf:
+    """__cuda_array_interface__ view of a buffer owned by the native solver."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class CudaSlabBackend:
+    def __init__(self, slab_grid, nu, force):
+        from .bcs import BoundarySpec, Periodic
+
+        from .plan import Plan
+
+        g = slab_grid
+        lay = g.layout
+        n0, n1, n2 = g.global_grid.shape
+        if n1 % lay.size:
+            raise ValueError("n1 must be divisible by the number of ranks")
+        self.grid = g
+        self.nu = float(nu)
+        self.force = [float(g.dtype.type(f)) for f in (force or (0.0, 0.0, 0.0))]
+        bcs = BoundarySpec.all_periodic(3)
+        self.plan = Plan(g, bcs, halo_axis0=True)
+        h = ctypes.c_void_p()
+        N.call("sfb_slab_solver_create", self.plan.handle, n0, lay.rank, lay.size, ctypes.byref(h))
+        self.handle = h
+        spec, trans, pl, ph = (ctypes.c_void_p() for _ in range(4))
+        N.call("sfb_slab_buffers", h, ctypes.byref(spec), ctypes.byref(trans), ctypes.byref(pl), ctypes.byref(ph))
+        ts = "<f8" if g.dtype == np.float64 else "<f4"
+        m, nh = lay.m, n2 // 2 + 1
+        self.spec = torch.as_tensor(_DevBuf(spec.value, (m, n1, nh, 2), ts), device="cuda")
+        self.trans = torch.as_tensor(_DevBuf(trans.value, (n0, n1 // lay.size, nh, 2), ts), device="cuda")
+        self.p_local = torch.as_tensor(_DevBuf(pl.value, (m, n1, n2), ts), device="cuda")
+        self.p_halo = torch.as_tensor(_DevBuf(ph.value, (n1, n2), ts), device="cuda")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                N.lib.sfb_solver_destroy(h)
+            except Exception:  # pragma: no cover
+                pass
+
+    def _sp(self):
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0):
+        a = N.StageArgs()
+        a.y = N.ptr3(y.u)
+        a.u0 = N.ptr3(u0.u if u0 is not None else [None] * 3)
+        a.s_in = N.ptr3(s_in.u if s_in is not None else [None] * 3)
+        a.s_out = N.ptr3(s_out.u if s_out is not None else [None] * 3)
+        a.y_next = N.ptr3(y_next.u if y_next is not None else [None] * 3)
+        a.k_out = N.ptr3([None] * 3)
+        a.cb, a.ca, a.nu = float(cb), float(ca), self.nu
+        for i, f in enumerate(self.force):
+            a.force[i] = f
+        N.call("sfb_rk_stage", self.plan.handle, ctypes.byref(a), self._sp())
+
+    def forward(self, u):
+        N.call("sfb_slab_forward", self.handle, N.ptr3(u.u), self._sp())
+
+    def axis0(self):
+        N.call("sfb_slab_axis0", self.handle, self._sp())
+
+    def inverse(self):
+        N.call("sfb_slab_inverse", self.handle, self._sp())
+
+    def correct(self, u, p_ext=None):
+        N.call("sfb_slab_correct", self.handle, N.ptr3(u.u), None if p_ext is None else p_ext.data_ptr(), self._sp())
+
+    def kinetic_energy_local(self, u):
+        out = ctypes.c_double()
+        N.call("sfb_kinetic_energy", self.plan.handle, N.ptr3(u.u), ctypes.byref(out), self._sp())
+        return out.value
+
+    def new_field(self):
+        return VelocityField(self.grid)
+
+    def new_scalar(self):
+        from .fields import ScalarField
+
+        return ScalarField(self.grid)
+
+
+# ---------------------------------------------------------------------------
+# orchestration (backend-agnostic)
+# ---------------------------------------------------------------------------
+class SlabProjector:
+    def __init__(self, backend, comm):
+        self.b = backend
+        self.comm = comm
+        lay = comm.layout
+        sp = backend.spec
+        m, n1, nh = sp.shape[0], sp.shape[1], sp.shape[2]
+        P = lay.size
+        self.sendbuf = torch.empty((P, m, n1 // P, nh, 2), dtype=sp.dtype, device=sp.device)
+        self.recvbuf = torch.empty_like(self.sendbuf)
+
+    def project(self, u, p_ext=None):
+        b, comm = self.b, self.comm
+        lay = comm.layout
+        P, m = lay.size, lay.m
+        comm.halo(u.u)
+        b.forward(u)
+        sp = b.spec
+        n1, nh = sp.shape[1], sp.shape[2]
+        # pack (m, n1, nh) -> (P, m, n1/P, nh): chunk q goes to rank q
+        self.sendbuf.copy_(sp.view(m, P, n1 // P, nh, 2).permute(1, 0, 2, 3, 4))
+        # received chunks are ordered by source rank = global plane order
+        comm.all_to_all(b.trans.view(P, m, n1 // P, nh, 2), self.sendbuf)
+        b.axis0()
+        comm.all_to_all(self.recvbuf, b.trans.view(P, m, n1 // P, nh, 2))
+        sp.view(m, P, n1 // P, nh, 2).copy_(self.recvbuf.permute(1, 0, 2, 3, 4))
+        b.inverse()
+        comm.plane_from_next(b.p_local[0], b.p_halo)
+        b.correct(u, p_ext)
+        comm.halo(u.u)
+        if p_ext is not None:
+            comm.halo([p_ext.data])
+
+
+class SlabState:
+    def __init__(self, u, regs, p, t=0.0):
+        self.u = u
+        self.regs = regs
+        self.pressure = p
+        self.t = t
+        self.step = 0
+
+
+class SlabSimulation:
+    """RK4 on a slab-decomposed periodic box (the fused 4-register scheme of
+    timestep.rk_step, with the slab projector between stages)."""
+
+    def __init__(self, backend, comm):
+        self.b = backend
+        self.comm = comm
+        self.proj = SlabProjector(backend, comm)
+
+    def new_state(self, u_local):
+        regs = [self.b.new_field() for _ in range(3)]
+        p = self.b.new_scalar()
+        self.comm.halo(u_local.u)
+        return SlabState(u_local, regs, p)
+
+    def rk4_step(self, state, dt):
+        from .timestep import RK4
+
+        tab = RK4
+        u0 = state.u
+        acc, y, yn = state.regs
+        started = False
+        cur = u0
+        for j in range(tab.stages):
+            bj = tab.b[j]
+            nxt = j + 1 < tab.stages
+            self.b.stage(cur, u0=u0, s_in=acc if started else None, s_out=acc if bj != 0.0 else None,
+                         y_next=yn if nxt else None, cb=dt * bj, ca=dt * (tab.a[j + 1][j] if nxt else 0.0))
+            started = started or bj != 0.0
+            if nxt:
+                self.proj.project(yn)
+                y, yn = yn, y
+                cur = y
+        self.proj.project(acc, p_ext=state.pressure)
+        state.regs = [u0, y, yn]
+        state.u = acc
+        state.t += dt
+        state.step += 1
+        return state
+
+    def kinetic_energy(self, u):
+        return self.comm.allreduce(self.b.kinetic_energy_local(u), "sum")
+
+
+def scatter_field(global_arrays, layout):
+    """Local extended slabs (with ghost planes) of global extended arrays."""
+    m, i0 = layout.m, layout.i0
+    return [np.ascontiguousarray(a[i0:i0 + m + 2]) for a in global_arrays]

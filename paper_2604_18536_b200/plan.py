@@ -42,7 +42,7 @@ def bcs_signature(bcs):
 
 
 class Plan:
-    def __init__(self, grid, bcs):
+    def __init__(self, grid, bcs, halo_axis0=False):
         if bcs.dim != grid.dim:
             raise ValueError("axis count and boundary spec dimension differ")
         if tuple(bcs.periodic) != tuple(grid.periodic):
@@ -67,6 +67,9 @@ class Plan:
                 for k, v in enumerate(_dirichlet_values(hi, grid.dim)):
                     d.val_hi[a][k] = v
             d.width0[a] = float(grid.axes[a].widths[0])
+        if halo_axis0:
+            # ghost planes of axis 0 come from the neighbouring slab (distributed.py)
+            d.bc_lo[0] = d.bc_hi[0] = N.SFB_BC_HALO
         self._tables = grid.packed_tables()
         d.tables = self._tables.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         h = ctypes.c_void_p()

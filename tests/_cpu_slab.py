@@ -1,0 +1,126 @@
+"""Test-only numpy backend for the slab-decomposed RK4 path
+(paper_2604_18536_b200/distributed.py), so the multi-rank orchestration can be
+exercised with gloo on CPU.  Local compute follows the oracle restatement of
+the reference (oracle/stagflow_np.py); uniform periodic grids only."""
+
+import numpy as np
+import torch
+
+from oracle import stagflow_np as O
+
+
+class CpuField:
+    def __init__(self, shape, dtype, dim=3):
+        self.u = [torch.zeros(shape, dtype=dtype) for _ in range(dim)]
+
+
+class CpuScalar:
+    def __init__(self, shape, dtype):
+        self.data = torch.zeros(shape, dtype=dtype)
+
+
+class CpuSlabBackend:
+    def __init__(self, global_bounds, layout, nu, force):
+        self.lay = layout
+        m, i0 = layout.m, layout.i0
+        b0 = global_bounds[0][i0:i0 + m + 1]
+        self.og = O.OGrid([b0, global_bounds[1], global_bounds[2]], (True, True, True))
+        self.n0 = len(global_bounds[0]) - 1
+        self.n1 = len(global_bounds[1]) - 1
+        self.n2 = len(global_bounds[2]) - 1
+        self.nu = nu
+        self.force = force
+        nh = self.n2 // 2 + 1
+        P = layout.size
+        self.spec = torch.zeros((m, self.n1, nh, 2), dtype=torch.float64)
+        self.trans = torch.zeros((self.n0, self.n1 // P, nh, 2), dtype=torch.float64)
+        self.p_local = torch.zeros((m, self.n1, self.n2), dtype=torch.float64)
+        self.p_halo = torch.zeros((self.n1, self.n2), dtype=torch.float64)
+        lam = []
+        for bnd, n in ((global_bounds[0], self.n0), (global_bounds[1], self.n1), (global_bounds[2], self.n2)):
+            h = float(np.diff(bnd)[0])
+            k = np.arange(n)
+            lam.append((2.0 * np.cos(2.0 * np.pi * k / n) - 2.0) / h**2)
+        self.lam = lam
+        self.ext = self.og.ext_shape
+
+    # -- fields
+    def new_field(self):
+        return CpuField(self.ext, torch.float64)
+
+    def new_scalar(self):
+        return CpuScalar(self.ext, torch.float64)
+
+    def _np(self, f):
+        return [t.numpy() for t in f.u]
+
+    def _fill12(self, arrs):
+        """periodic ghost fill of axes 1 and 2 (axis 0 ghosts come from the halo)."""
+        for x in arrs:
+            for a in (1, 2):
+                n = x.shape[a] - 2
+                sl = [slice(None)] * 3
+                s2 = [slice(None)] * 3
+                sl[a], s2[a] = 0, n
+                x[tuple(sl)] = x[tuple(s2)]
+                sl[a], s2[a] = n + 1, 1
+                x[tuple(sl)] = x[tuple(s2)]
+
+    # -- compute
+    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0):
+        og = self.og
+        k = O.momentum_rhs(og, self._np(y), self.nu, self.force)
+        for a in range(3):
+            sl = og.udof(a)
+            if s_out is not None:
+                base = (s_in if s_in is not None else u0).u[a].numpy()
+                s_out.u[a].numpy()[sl] = base[sl] + k[a][sl] * cb
+            if y_next is not None:
+                y_next.u[a].numpy()[sl] = u0.u[a].numpy()[sl] + k[a][sl] * ca
+
+    def forward(self, u):
+        arrs = self._np(u)
+        self._fill12(arrs)
+        div = O.divergence(self.og, arrs)[self.og.pdof()]
+        s = np.fft.fft(np.fft.rfft(div, axis=2), axis=1)
+        self.spec.copy_(torch.view_as_real(torch.from_numpy(s)))
+
+    def axis0(self):
+        t = torch.view_as_complex(self.trans).numpy()
+        f = np.fft.fft(t, axis=0)
+        P, q = self.lay.size, self.lay.rank
+        c = self.n1 // P
+        k1 = np.arange(q * c, (q + 1) * c)
+        nh = self.n2 // 2 + 1
+        lam = (self.lam[0][:, None, None] + self.lam[1][k1][None, :, None]) + self.lam[2][:nh][None, None, :]
+        if q == 0:
+            lam[0, 0, 0] = 1.0
+        f = f / lam
+        if q == 0:
+            f[0, 0, 0] = 0.0
+        self.trans.copy_(torch.view_as_real(torch.from_numpy(np.fft.ifft(f, axis=0))))
+
+    def inverse(self):
+        s = torch.view_as_complex(self.spec).numpy()
+        p = np.fft.irfft(np.fft.ifft(s, axis=1), n=self.n2, axis=2)
+        self.p_local.copy_(torch.from_numpy(np.ascontiguousarray(p)))
+
+    def correct(self, u, p_ext=None):
+        og = self.og
+        m = self.lay.m
+        pe = np.zeros(og.ext_shape)
+        pe[1:m + 1, 1:-1, 1:-1] = self.p_local.numpy()
+        pe[m + 1, 1:-1, 1:-1] = self.p_halo.numpy()
+        self._fill12([pe])
+        arrs = self._np(u)
+        for a in range(3):
+            sl = og.udof(a)
+            t = np.subtract(pe[O._sh(sl, a, 1)], pe[sl])
+            t /= og.col(og.du[a], a, sl[a])
+            arrs[a][sl] -= t
+        self._fill12(arrs)
+        if p_ext is not None:
+            p_ext.data.numpy()[1:] = pe[1:]
+
+    def kinetic_energy_local(self, u):
+        return O.kinetic_energy(self.og, self._np(u))

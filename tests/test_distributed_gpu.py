@@ -1,0 +1,113 @@
+"""GPU tests of the z-slab path with the CUDA backend (C ABI sfb_slab_*):
+P = 1 on one GPU, and P = 2 as two processes sharing cuda:0 with gloo and
+host-staged communication (this environment exposes a single GPU; NCCL needs
+one GPU per rank)."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import stagflow_np as O
+
+pytestmark = pytest.mark.gpu
+
+SHAPE = (16, 12, 10)
+NU, DT, FORCE = 0.02, 5e-3, (0.1, 0.0, 0.0)
+
+
+def _case():
+    bounds = [O.uniform_bounds(0.0, 1.0 + 0.3 * a, n) for a, n in enumerate(SHAPE)]
+    g = O.OGrid(bounds, (True,) * 3)
+    rng = np.random.default_rng(11)
+    u = g.zeros_vel()
+    for a in range(3):
+        u[a][g.udof(a)] = rng.standard_normal(g.shape)
+    O.project_into(g, O.periodic_bcs(3), O.SpectralSolve(g), u)
+    return bounds, g, u
+
+
+def _run(rank, size, stage_host, nsteps):
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200.distributed import (Comm, CudaSlabBackend, SlabGrid, SlabLayout, SlabSimulation,
+                                                   scatter_field)
+
+    bounds, g, u = _case()
+    pg = P.Grid(tuple(P.AxisCoords(b) for b in bounds), (True,) * 3)
+    lay = SlabLayout(SHAPE[0], rank, size)
+    sg = SlabGrid(pg, lay)
+    be = CudaSlabBackend(sg, NU, FORCE)
+    sim = SlabSimulation(be, Comm(lay, stage_host=stage_host))
+    loc = be.new_field()
+    for a, arr in enumerate(scatter_field(u, lay)):
+        loc.u[a].copy_(torch.from_numpy(arr))
+    st = sim.new_state(loc)
+    for _ in range(nsteps):
+        sim.rk4_step(st, DT)
+    torch.cuda.synchronize()
+    m = lay.m
+    return [st.u.u[a][1:m + 1].cpu() for a in range(3)] + [st.pressure.data[1:m + 1].cpu()], sim.kinetic_energy(st.u)
+
+
+def _check(fields, ke, nsteps):
+    bounds, g, u = _case()
+    solve = O.SpectralSolve(g)
+    for _ in range(nsteps):
+        u, p = O.rk_step(g, O.periodic_bcs(3), solve, u, DT, O.RK4, NU, FORCE)
+    inner = tuple(slice(1, n + 1) for n in g.shape)
+    for a in range(3):
+        ref = u[a][inner]
+        got = fields[a][:, 1:-1, 1:-1]
+        assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref)), a
+    refp = p[inner]
+    assert np.max(np.abs(fields[3][:, 1:-1, 1:-1] - refp)) <= 1e-11 * np.max(np.abs(refp))
+    assert abs(ke - O.kinetic_energy(g, u)) <= 1e-12 * O.kinetic_energy(g, u)
+
+
+def test_slab_p1_cuda_matches_oracle():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    fields, ke = _run(0, 1, False, 2)
+    _check([f.numpy() for f in fields], ke, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, size, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        fields, ke = _run(rank, size, True, 2)
+        gathered = []
+        for t in fields:
+            t = t.contiguous()
+            buf = [torch.empty_like(t) for _ in range(size)] if rank == 0 else None
+            dist.gather(t, buf, dst=0)
+            gathered.append(buf)
+        if rank == 0:
+            np.savez(os.path.join(outdir, "out.npz"), ke=ke,
+                     **{f"f{i}": torch.cat(gathered[i], 0).numpy() for i in range(4)})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_p2_cuda_two_processes_matches_oracle():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        z = np.load(os.path.join(d, "out.npz"))
+        _check([z[f"f{i}"] for i in range(4)], float(z["ke"]), 2)
