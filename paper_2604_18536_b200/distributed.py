@@ -211,7 +211,7 @@ class CudaSlabBackend:
         N.call("sfb_slab_inverse", self.handle, self._sp())
 
     def correct(self, u, p_ext=None):
-        N.call("sfb_slab_correct", self.handle, N.ptr3(u.u), None if p_ext is None else p_ext.data_ptr(), self._sp())
+        N.call("sfb_slab_correct", self.handle, N.ptr3(u.u), None if p_ext is None else p_ext.data.data_ptr(), self._sp())
 
     def kinetic_energy_local(self, u):
         out = ctypes.c_double()
