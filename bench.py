@@ -166,6 +166,29 @@ def run_reference(args):
 METRIC = "fp64 cell-updates/s per RK4 step"
 
 
+WEAK_LADDER = {1: (840, 840, 840), 2: (1680, 840, 840), 4: (1680, 1680, 840), 8: (1680, 1680, 1680)}
+
+
+def _slab_tgv(local_grid, P):
+    """3D Taylor-Green vortex at the local slab's staggered points (ghosts
+    included; the domain is [0, 2 pi * n / n_ref] so the field is periodic)."""
+    import torch
+
+    u = P.VelocityField(local_grid)
+    dev = u.u[0].device
+
+    def c(tab, axis):
+        shp = [1, 1, 1]
+        shp[axis] = tab.shape[0]
+        return torch.from_numpy(tab.astype("float64")).to(dev).reshape(shp)
+
+    fc = [[c(local_grid.face_coords(a)[g], g) for g in range(3)] for a in range(3)]
+    ext = local_grid.ext_shape
+    u.u[0].copy_((torch.sin(fc[0][0]) * torch.cos(fc[0][1]) * torch.cos(fc[0][2])).expand(ext))
+    u.u[1].copy_((-torch.cos(fc[1][0]) * torch.sin(fc[1][1]) * torch.cos(fc[1][2])).expand(ext))
+    return u
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -187,18 +210,58 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    n = args.n
     dtype = np.float64 if args.dtype == "f64" else np.float32
-    grid = cases.periodic_box(n, dtype=dtype)
-    bcs = P.BoundarySpec.all_periodic(3)
-    setup = P.Setup(grid, bcs, nu=1 / 1600, solver="spectral", method="rk4")
-    u0 = cases.isotropic(grid, setup.solver, seed=rank)
-    state = setup.new_state(u0=u0)
-    del u0
     dt = 1e-3
-    cells = n**3
+    slab = world > 1 or args.slab
+    if not slab:
+        n = args.n
+        gshape = (n, n, n)
+        grid = cases.periodic_box(n, dtype=dtype)
+        bcs = P.BoundarySpec.all_periodic(3)
+        setup = P.Setup(grid, bcs, nu=1 / 1600, solver="spectral", method="rk4")
+        u0 = cases.isotropic(grid, setup.solver, seed=rank)
+        state = setup.new_state(u0=u0)
+        del u0
+        local_cells = n**3
+
+        def step():
+            P.rk_step(state, dt, P.RK4, setup.solver, setup)
+
+        def cur_u():
+            return state.u
+
+        def ke():
+            return P.kinetic_energy(state.u)
+
+        ic = "isotropic random-phase IC"
+    else:
+        from paper_2604_18536_b200.distributed import Comm, CudaSlabBackend, SlabGrid, SlabLayout, SlabSimulation
+
+        gshape = WEAK_LADDER.get(world) if args.n == 840 else (args.n * world, args.n, args.n)
+        if gshape is None:
+            gshape = (840 * world, 840, 840)
+        ref = 840 if args.n == 840 else args.n
+        gg = P.Grid(tuple(P.uniform_grid(0.0, 2 * np.pi * m / ref, m) for m in gshape), (True,) * 3, dtype=dtype)
+        lay = SlabLayout(gshape[0], rank, world)
+        sg = SlabGrid(gg, lay)
+        be = CudaSlabBackend(sg, 1 / 1600, None)
+        sim = SlabSimulation(be, Comm(lay, group=dist.group.WORLD if world > 1 else None))
+        st = sim.new_state(_slab_tgv(sg, P))
+        sim.proj.project(st.u)
+        local_cells = lay.m * gshape[1] * gshape[2]
+
+        def step():
+            sim.rk4_step(st, dt)
+
+        def cur_u():
+            return st.u
+
+        def ke():
+            return sim.kinetic_energy(st.u)
+
+        ic = "3D Taylor-Green IC"
     for _ in range(args.warmup):
-        P.rk_step(state, dt, P.RK4, setup.solver, setup)
+        step()
     torch.cuda.synchronize()
     barrier()
 
@@ -211,7 +274,7 @@ def run_ours(args):
         barrier()
         start.record()
         for _ in range(args.steps):
-            P.rk_step(state, dt, P.RK4, setup.solver, setup)
+            step()
         end.record()
         torch.cuda.synchronize()
     launches = N.launches - launches0
@@ -219,28 +282,33 @@ def run_ours(args):
     ev = TS.STAGE_EVENTS
     TS.STAGE_EVENTS = None
     st_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in ev)
-    st_bytes = sum(bpc for _, _, bpc in ev) * cells
+    st_bytes = sum(bpc for _, _, bpc in ev) * local_cells
     t = torch.tensor([ms], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * cells / (ms_max * 1e-3)
+    total_cells = int(np.prod(gshape))
+    value = total_cells / (ms_max * 1e-3)
 
     # ---- end to end through the public API with pinned host buffers
-    host = [torch.empty(grid.ext_shape, dtype=state.u.u[0].dtype, pin_memory=True) for _ in range(3)]
+    u = cur_u()
+    ext = u.u[0].shape
+    host = [torch.empty(ext, dtype=u.u[0].dtype, pin_memory=True) for _ in range(3)]
     for a in range(3):
-        host[a].copy_(state.u.u[a])
+        host[a].copy_(u.u[a])
     torch.cuda.synchronize()
     barrier()
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     es.record()
     for _ in range(e2e_steps):
+        u = cur_u()
         for a in range(3):
-            state.u.u[a].copy_(host[a], non_blocking=True)
-        P.rk_step(state, dt, P.RK4, setup.solver, setup)
+            u.u[a].copy_(host[a], non_blocking=True)
+        step()
+        u = cur_u()
         for a in range(3):
-            host[a].copy_(state.u.u[a], non_blocking=True)
+            host[a].copy_(u.u[a], non_blocking=True)
     ee.record()
     torch.cuda.synchronize()
     e2e_ms = es.elapsed_time(ee) / e2e_steps
@@ -248,8 +316,8 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
-    field_bytes = int(np.prod(grid.ext_shape)) * grid.dtype.itemsize
-    ke = P.kinetic_energy(state.u)
+    field_bytes = int(np.prod(ext)) * np.dtype(dtype).itemsize
+    ke_after = ke()
 
     if rank == 0:
         peak, peak_kind = _peaks()
@@ -261,29 +329,34 @@ def run_ours(args):
                 traffic = json.load(open(prof)).get("stage_kernel", {}).get("dram_bytes_per_launch")
             except (ValueError, OSError):
                 traffic = None
-        step_gbs = RK4_BYTES_PER_CELL_F64 * (dtype().itemsize / 8) * cells / (ms * 1e-3) / 1e9
+        bpc = RK4_BYTES_PER_CELL_F64 * (np.dtype(dtype).itemsize / 8)
+        step_gbs = bpc * local_cells / (ms * 1e-3) / 1e9
+        wl = (f"periodic DNS {gshape[0]}x{gshape[1]}x{gshape[2]} {args.dtype} RK4 step, "
+              + ("BASELINE config 5 (840^3 on one B200)" if world == 1 and not slab else
+                 f"z-slab decomposed over {world} GPU(s), {lay.m} planes per rank (weak ladder, SURVEY 7)")
+              + f", {ic}, spectral projection")
         line = {
             "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"periodic DNS {n}^3 {args.dtype} RK4 step (BASELINE config 5), "
-                                   "isotropic random-phase IC, spectral projection",
-                       "grid": [n, n, n * world], "method": "rk4", "solver": "spectral", "nu": 1 / 1600, "dt": dt,
-                       "l2": "inputs larger than L2 (each field 4.7 GB at 840^3); no flush needed",
-                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
-            "e2e": {"value": world * cells / (e2e_ms * 1e-3), "unit": "cell-updates/s",
-                    "h2d_bytes_per_step": 3 * field_bytes, "d2h_bytes_per_step": 3 * field_bytes,
-                    "steps": e2e_steps, "api": "paper_2604_18536_b200.rk_step with pinned host velocity in/out"},
-            "roofline": {"bound": "hbm", "kernel": "k_stage (fused RHS + RK stage combine)",
+            "config": {"workload": wl, "grid": list(gshape), "method": "rk4", "solver": "spectral",
+                       "nu": 1 / 1600, "dt": dt,
+                       "l2": "inputs larger than L2 (each field >= 4.7 GB at 840^3 per GPU); no flush needed",
+                       "parallelism": f"z-slab x{world}" if slab else "single GPU"},
+            "e2e": {"value": total_cells / (e2e_ms * 1e-3), "unit": "cell-updates/s",
+                    "h2d_bytes_per_step": 3 * field_bytes * world, "d2h_bytes_per_step": 3 * field_bytes * world,
+                    "steps": e2e_steps,
+                    "api": "rk_step (or the slab stepper) with pinned host velocity copied in and out every step"},
+            "roofline": {"bound": "hbm", "kernel": "k_stage_march (fused RHS + RK stage combine)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind, "traffic": traffic,
                          "bytes_per_cell": "72/120/120/72 per stage launch (avg 96 B fp64)",
                          "stage_share_of_step": st_ms / (ms * args.steps)},
-            "step_roofline": {"algorithmic_bytes_per_cell": RK4_BYTES_PER_CELL_F64 * (dtype().itemsize / 8),
-                              "achieved": step_gbs, "peak": peak, "frac": step_gbs / peak},
+            "step_roofline": {"algorithmic_bytes_per_cell": bpc, "achieved": step_gbs, "peak": peak,
+                              "frac": step_gbs / peak},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
-            "ke_after": ke,
+            "ke_after": ke_after,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
@@ -303,6 +376,7 @@ def main():
     ap.add_argument("--ref-n", type=int, default=96)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="use the z-slab path even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -199,7 +199,19 @@ class CudaSlabBackend:
         a.cb, a.ca, a.nu = float(cb), float(ca), self.nu
         for i, f in enumerate(self.force):
             a.force[i] = f
+        from . import timestep as TS
+
+        if TS.STAGE_EVENTS is None:
+            N.call("sfb_rk_stage", self.plan.handle, ctypes.byref(a), self._sp())
+            return
+        nfield = 1 + (s_out is not None) + (y_next is not None)
+        nfield += (u0 is not None and u0 is not y and (y_next is not None or (s_out is not None and s_in is None)))
+        nfield += (s_in is not None and s_out is not None)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         N.call("sfb_rk_stage", self.plan.handle, ctypes.byref(a), self._sp())
+        e1.record()
+        TS.STAGE_EVENTS.append((e0, e1, nfield * 3 * self.grid.dtype.itemsize))
 
     def forward(self, u):
         N.call("sfb_slab_forward", self.handle, N.ptr3(u.u), self._sp())
