@@ -1,0 +1,98 @@
+"""Secondary measurements for the other BASELINE.json configs (not the
+driver's bench line): prints one JSON object per case.
+
+  python bench_extra.py [--cases step512,step512f32,step840f32,vjp512,channel]
+
+* stepN / stepNf32 : RK4 step, periodic N^3 (isotropic IC), fp64 / fp32
+* vjpN             : unrolled RK4 gradient of the kinetic energy over one
+                     step (forward tape + backward), fp64
+* channel          : RK4 step of the Re_tau=180 channel (512x256x256,
+                     tanh y, FFT(x,z) x tridiagonal(y) pressure)
+Device time by CUDA events, median of the timed repetitions.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _time(fn, reps, warm):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def case_step(n, dtype):
+    import numpy as np
+
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200 import cases
+
+    g = cases.periodic_box(n, dtype=np.float64 if dtype == "f64" else np.float32)
+    setup = P.Setup(g, P.BoundarySpec.all_periodic(3), nu=1 / 1600, solver="spectral", method="rk4")
+    st = setup.new_state(u0=cases.isotropic(g, setup.solver, seed=0))
+    ms = _time(lambda: P.rk_step(st, 1e-3, P.RK4, setup.solver, setup), 5, 2)
+    return {"case": f"rk4 step {n}^3 {dtype}", "ms": ms, "cell_updates_per_s": n**3 / (ms * 1e-3)}
+
+
+def case_vjp(n):
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200 import cases
+
+    g = cases.periodic_box(n)
+    setup = P.Setup(g, P.BoundarySpec.all_periodic(3), nu=1 / 1600, solver="spectral", method="rk4")
+    u0 = cases.isotropic(g, setup.solver, seed=0)
+    loss = P.KineticEnergyLoss()
+    ms = _time(lambda: P.unrolled_gradient(loss, u0, 1, 1e-3, setup), 3, 1)
+    return {"case": f"unrolled RK4 gradient (1 step, tape + backward) {n}^3 f64", "ms": ms,
+            "cell_updates_per_s": n**3 / (ms * 1e-3)}
+
+
+def case_channel(nx=512, ny=256, nz=256):
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200 import cases
+
+    setup = cases.channel_setup(nx, ny, nz, gamma=2.0, solver="direct", method="rk4")
+    st = setup.new_state()
+    P.project_into(st.u, setup.solver, setup.bcs)
+    ms = _time(lambda: P.rk_step(st, 1e-3, P.RK4, setup.solver, setup), 5, 2)
+    return {"case": f"channel Re_tau=180 {nx}x{ny}x{nz} f64 rk4 step (fft-tridiag)", "ms": ms,
+            "cell_updates_per_s": nx * ny * nz / (ms * 1e-3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", default="step512,step512f32,step840f32,vjp512,channel")
+    args = ap.parse_args()
+    for c in args.cases.split(","):
+        if c.startswith("step"):
+            f32 = c.endswith("f32")
+            n = int(c[4:-3] if f32 else c[4:])
+            r = case_step(n, "f32" if f32 else "f64")
+        elif c.startswith("vjp"):
+            r = case_vjp(int(c[3:]))
+        elif c == "channel":
+            r = case_channel()
+        else:
+            continue
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
