@@ -236,6 +236,7 @@ __device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restric
   const int col = threadIdx.x % W;
   const int jstride = blockDim.x / W;
   const float inv = 1.0f / (float)Ns;
+#pragma unroll 2
   for (int j = threadIdx.x / W; j < nb; j += jstride) {
     int g, k;
     divmod_ns(j, Ns, inv, g, k);
@@ -297,6 +298,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
   C* base = data + (long long)blockIdx.y * bstride;
   const int L = P.L;
   const int tot = L * W;
+#pragma unroll 4
   for (int e = threadIdx.x; e < tot; e += blockDim.x) {
     const int w = e % W, m = e / W;
     const int col = c0 + w;
@@ -332,6 +334,7 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
     C* other = (res == bufA) ? bufB : bufA;
     res = run_fft<C, true, W>(res, other, P, tw);
   }
+#pragma unroll 4
   for (int e = threadIdx.x; e < tot; e += blockDim.x) {
     const int w = e % W, m = e / W;
     const int col = c0 + w;
