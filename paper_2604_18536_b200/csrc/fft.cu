@@ -228,50 +228,56 @@ __device__ __forceinline__ void divmod_ns(int j, int Ns, float inv, int& q, int&
 
 // One Stockham pass over a tile stored [m][w] (m < L, w < W): src -> dst.
 // Thread t owns column t % W and butterflies j = t / W + s * (NT / W).
+// twp: this pass's twiddles laid out [k][r-1] (contiguous per butterfly).
 template <typename C, int R, bool INV, int W>
 __device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restrict__ dst, int L, int Ns,
-                                         const C* __restrict__ tw) {
+                                         const C* __restrict__ twp) {
   const int nb = L / R;
-  const int step = L / (Ns * R);
   const int col = threadIdx.x % W;
   const int jstride = blockDim.x / W;
+  const int nbW = nb * W, NsW = Ns * W;
   const float inv = 1.0f / (float)Ns;
+  const C* s0 = src + col;
+  C* d0 = dst + col;
 #pragma unroll 2
   for (int j = threadIdx.x / W; j < nb; j += jstride) {
     int g, k;
     divmod_ns(j, Ns, inv, g, k);
+    const C* sp = s0 + j * W;
     C v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = src[(j + r * nb) * W + col];
+    for (int r = 0; r < R; ++r) v[r] = sp[r * nbW];
     if (Ns > 1) {
-      const int kstep = k * step;
+      const C* tp = twp + k * (R - 1);
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        C w = __ldg(tw + kstep * r);
+        C w = __ldg(tp + (r - 1));
         if (INV) w.y = -w.y;
         v[r] = cmul(v[r], w);
       }
     }
     dft<C, R, INV>(v);
-    const int d = g * Ns * R + k;
+    C* dp = d0 + (g * Ns * R + k) * W;
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[(d + r * Ns) * W + col] = v[r];
+    for (int r = 0; r < R; ++r) dp[r * NsW] = v[r];
   }
 }
 
 // Run all passes of a length-L plan; returns the buffer holding the result.
+// tw: plain table exp(-2 pi i m / L) followed by the per-pass tables.
 template <typename C, bool INV, int W>
 __device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, const C* __restrict__ tw) {
   int Ns = 1;
   for (int p = 0; p < P.np; ++p) {
     __syncthreads();
+    const C* twp = tw + P.twoff[p];
     switch (P.radix[p]) {
-      case 8: stockham<C, 8, INV, W>(a, b, P.L, Ns, tw); break;
-      case 4: stockham<C, 4, INV, W>(a, b, P.L, Ns, tw); break;
-      case 2: stockham<C, 2, INV, W>(a, b, P.L, Ns, tw); break;
-      case 7: stockham<C, 7, INV, W>(a, b, P.L, Ns, tw); break;
-      case 5: stockham<C, 5, INV, W>(a, b, P.L, Ns, tw); break;
-      default: stockham<C, 3, INV, W>(a, b, P.L, Ns, tw); break;
+      case 8: stockham<C, 8, INV, W>(a, b, P.L, Ns, twp); break;
+      case 4: stockham<C, 4, INV, W>(a, b, P.L, Ns, twp); break;
+      case 2: stockham<C, 2, INV, W>(a, b, P.L, Ns, twp); break;
+      case 7: stockham<C, 7, INV, W>(a, b, P.L, Ns, twp); break;
+      case 5: stockham<C, 5, INV, W>(a, b, P.L, Ns, twp); break;
+      default: stockham<C, 3, INV, W>(a, b, P.L, Ns, twp); break;
     }
     Ns *= P.radix[p];
     C* t = a;
@@ -298,12 +304,16 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
   C* base = data + (long long)blockIdx.y * bstride;
   const int L = P.L;
   const int tot = L * W;
+  // thread-fixed column; rows m = m0 + s*ms (strength-reduced addressing)
+  const int w = threadIdx.x % W, m0 = threadIdx.x / W, ms = blockDim.x / W;
+  const int col = c0 + w;
+  const bool ok = col < ncol;
+  {
+    const C* g = base + (ok ? (long long)m0 * S + col : 0);
+    const long long gs = ok ? (long long)ms * S : 0;
+    C* sd = bufA + m0 * W + w;
 #pragma unroll 4
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int w = e % W, m = e / W;
-    const int col = c0 + w;
-    const bool ok = col < ncol;
-    cp_async_elem(bufA + e, base + (ok ? (long long)m * S + col : 0), ok);
+    for (int m = m0; m < L; m += ms, g += gs, sd += ms * W) cp_async_elem(sd, g, ok);
   }
   cp_async_wait_all();
   C* res;
@@ -311,34 +321,51 @@ __global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __res
   else res = run_fft<C, false, W>(bufA, bufB, P, tw);
   if (MODE == 2) {
     // eigenvalue scaling (poisson.py:179-199): lam in fp64, cast to T
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int w = e % W, m = e / W;
-      const int col = c0 + w;
-      if (col >= ncol) continue;
-      const int k1 = sc.nh > 0 ? col / sc.nh : 0;
-      const int k2 = sc.nh > 0 ? col % sc.nh : col;
-      double lam;
-      if (sc.dim == 3) lam = (sc.l0[m] + sc.l1[k1]) + sc.l2[k2];
-      else lam = sc.l0[m] + sc.l1[col];
-      C v = res[e];
-      if (m == 0 && col == 0 && blockIdx.y == 0 && sc.zero_ok) {
-        v.x = 0;
-        v.y = 0;
+    if (ok) {
+      double lc;
+      if (sc.dim == 3) {
+        const int k1 = col / sc.nh, k2 = col - k1 * sc.nh;
+        lc = sc.l1[k1] + 0.0;
+        // (l0[m] + l1[k1]) + l2[k2], accumulated in axis order
+        for (int m = m0; m < L; m += ms) {
+          const double lam = (sc.l0[m] + lc) + sc.l2[k2];
+          C v = res[m * W + w];
+          if (m == 0 && col == 0 && blockIdx.y == 0 && sc.zero_ok) {
+            v.x = 0;
+            v.y = 0;
+          } else {
+            const T f = T(1) / (T)lam * (T)sc.invN;
+            v.x *= f;
+            v.y *= f;
+          }
+          res[m * W + w] = v;
+        }
       } else {
-        const T f = T(1) / (T)lam * (T)sc.invN;
-        v.x *= f;
-        v.y *= f;
+        lc = sc.l1[col];
+        for (int m = m0; m < L; m += ms) {
+          const double lam = sc.l0[m] + lc;
+          C v = res[m * W + w];
+          if (m == 0 && col == 0 && blockIdx.y == 0 && sc.zero_ok) {
+            v.x = 0;
+            v.y = 0;
+          } else {
+            const T f = T(1) / (T)lam * (T)sc.invN;
+            v.x *= f;
+            v.y *= f;
+          }
+          res[m * W + w] = v;
+        }
       }
-      res[e] = v;
     }
     C* other = (res == bufA) ? bufB : bufA;
     res = run_fft<C, true, W>(res, other, P, tw);
   }
+  if (ok) {
+    C* g = base + (long long)m0 * S + col;
+    const long long gs = (long long)ms * S;
+    const C* sd = res + m0 * W + w;
 #pragma unroll 4
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int w = e % W, m = e / W;
-    const int col = c0 + w;
-    if (col < ncol) base[(long long)m * S + col] = res[e];
+    for (int m = m0; m < L; m += ms, g += gs, sd += ms * W) *g = *sd;
   }
 }
 
@@ -544,13 +571,7 @@ bool fft_factor(int L, FftLen& P) {
   return true;
 }
 
-int fft_upload_twiddles(int L, bool f64, void** dev) {
-  std::vector<double> t(2 * (size_t)(L > 0 ? L : 1));
-  for (int m = 0; m < L; ++m) {
-    long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)L;
-    t[2 * m] = (double)cosl(a);
-    t[2 * m + 1] = (double)sinl(a);
-  }
+static int upload(const std::vector<double>& t, bool f64, void** dev) {
   size_t bytes;
   std::vector<float> tf;
   const void* src;
@@ -565,6 +586,36 @@ int fft_upload_twiddles(int L, bool f64, void** dev) {
   int rc = cuda_check(cudaMalloc(dev, bytes), "cudaMalloc(twiddles)");
   if (rc) return rc;
   return cuda_check(cudaMemcpy(*dev, src, bytes, cudaMemcpyHostToDevice), "upload twiddles");
+}
+
+static void push_root(std::vector<double>& t, long long num, long long den) {
+  const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)(num % den) / (long double)den;
+  t.push_back((double)cosl(a));
+  t.push_back((double)sinl(a));
+}
+
+int fft_upload_twiddles(int L, bool f64, void** dev) {
+  std::vector<double> t;
+  for (int m = 0; m < (L > 0 ? L : 1); ++m) push_root(t, m, L > 0 ? L : 1);
+  return upload(t, f64, dev);
+}
+
+// plain table (L entries) followed by per-pass tables [k][r-1]
+int fft_upload_pass_twiddles(FftLen& P, bool f64, void** dev) {
+  std::vector<double> t;
+  const int L = P.L > 0 ? P.L : 1;
+  for (int m = 0; m < L; ++m) push_root(t, m, L);
+  int Ns = 1;
+  for (int p = 0; p < P.np; ++p) {
+    const int R = P.radix[p];
+    P.twoff[p] = (int)(t.size() / 2);
+    const int step = L / (Ns * R);
+    if (Ns > 1)
+      for (int k = 0; k < Ns; ++k)
+        for (int r = 1; r < R; ++r) push_root(t, (long long)k * r * step, L);
+    Ns *= R;
+  }
+  return upload(t, f64, dev);
 }
 
 static int pick_w(int L, size_t csz) {

@@ -361,9 +361,9 @@ static int setup_fft(sfb_solver* s) {
   F.half = half;
   for (int a = 0; a < dim - 1; ++a) {
     F.ax[a] = ax[a];
-    if ((rc = fft_upload_twiddles(p->n[a], f64, &F.tw_ax[a]))) return rc;
+    if ((rc = fft_upload_pass_twiddles(F.ax[a], f64, &F.tw_ax[a]))) return rc;
   }
-  if ((rc = fft_upload_twiddles(nlast / 2, f64, &F.tw_half))) return rc;
+  if ((rc = fft_upload_pass_twiddles(F.half, f64, &F.tw_half))) return rc;
   if ((rc = fft_upload_twiddles(nlast, f64, &F.tw_full))) return rc;
   F.sc.dim = dim;
   F.sc.nh = dim == 3 ? nlast / 2 + 1 : 0;
@@ -552,9 +552,9 @@ int sfb_slab_solver_create(sfb_plan* p, int n0g, int rank, int nranks, sfb_solve
   F.half = half;
   F.ax[0] = a0;
   F.ax[1] = a1;
-  if ((rc = fft_upload_twiddles(n0g, f64, &F.tw_ax[0]))) goto bad;
-  if ((rc = fft_upload_twiddles(n1, f64, &F.tw_ax[1]))) goto bad;
-  if ((rc = fft_upload_twiddles(n2 / 2, f64, &F.tw_half))) goto bad;
+  if ((rc = fft_upload_pass_twiddles(F.ax[0], f64, &F.tw_ax[0]))) goto bad;
+  if ((rc = fft_upload_pass_twiddles(F.ax[1], f64, &F.tw_ax[1]))) goto bad;
+  if ((rc = fft_upload_pass_twiddles(F.half, f64, &F.tw_half))) goto bad;
   if ((rc = fft_upload_twiddles(n2, f64, &F.tw_full))) goto bad;
   F.sc.dim = 3;
   F.sc.nh = (int)nh;

@@ -9,6 +9,7 @@ struct FftLen {
   int L;          // complex transform length
   int np;         // number of Stockham passes
   int radix[12];  // radices in pass order
+  int twoff[12];  // offset of each pass's twiddle table (after the plain table)
 };
 
 struct ScaleArgs {
@@ -34,6 +35,7 @@ struct FftSolve {
 
 bool fft_factor(int L, FftLen& P);
 int fft_upload_twiddles(int L, bool f64, void** dev);
+int fft_upload_pass_twiddles(FftLen& P, bool f64, void** dev);
 // Spectral solve in place on rbuf.  When G/u are given, the right-hand side
 // is the divergence of u, computed inside the first (R2C) pass.
 template <typename T>
