@@ -239,7 +239,6 @@ __device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restric
   const float inv = 1.0f / (float)Ns;
   const C* s0 = src + col;
   C* d0 = dst + col;
-#pragma unroll 2
   for (int j = threadIdx.x / W; j < nb; j += jstride) {
     int g, k;
     divmod_ns(j, Ns, inv, g, k);
