@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   typedef RingGeom<TJ, TK> RG;
   constexpr int NTH = TJ / CPT * TK;                // threads per CTA
   constexpr int NE = 3 * RG::PS;                    // values per plane slot
+  constexpr int NQ = (NE + NTH - 1) / NTH;          // fill copies per thread
   constexpr int RS = TJ / CPT;                      // row stride between a thread's cells
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);         // [kRing][3][PS]
@@ -155,28 +156,26 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   const int k = k0 + tk;
   const long long s0 = G.s[0];
 
-  // ring fill: each warp copies whole halo rows (3 components x (TJ+2) rows
-  // of TK+2 contiguous values); the per-row work is warp-uniform
-  const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = NTH / 32;
-  constexpr int NROWS = 3 * RG::PH;
-  const int gk0 = k0 - 1 + lane, gk1 = k0 - 1 + 32 + lane;
-  const bool okk0 = gk0 < G.E[2], okk1 = (lane < RG::PW - 32) && gk1 < G.E[2];
+  const T* fsrc[NQ];
+  bool fok[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int e = tid + q * NTH;
+    const int c = e / RG::PS;
+    const int r = e - c * RG::PS;
+    const int jj = r / RG::PW;
+    const int kk = r - jj * RG::PW;
+    const int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
+    fok[q] = e < NE && gj < G.E[1] && gk < G.E[2];
+    fsrc[q] = A.y.c[c < 3 ? c : 0] + (fok[q] ? (long long)gj * G.s[1] + gk : 0);
+  }
   auto load_plane = [&](int ip, int slot) {
     if (ip < 0 || ip >= G.E[0]) return;
-    T* dst = ring + slot * NE;
+    T* dst = ring + slot * NE + tid;
     const long long base = (long long)ip * s0;
 #pragma unroll
-    for (int rr = warp; rr < NROWS; rr += NW) {
-      const int c = rr / RG::PH;
-      const int jj = rr - c * RG::PH;
-      const int gj = j0 - 1 + jj;
-      const bool okj = gj < G.E[1];
-      const T* src = A.y.c[c] + base + (long long)gj * G.s[1];
-      T* d = dst + c * RG::PS + jj * RG::PW;
-      cp_async_val(d + lane, okj && okk0 ? src + gk0 : A.y.c[0], okj && okk0);
-      if (lane < RG::PW - 32) cp_async_val(d + 32 + lane, okj && okk1 ? src + gk1 : A.y.c[0], okj && okk1);
-    }
+    for (int q = 0; q < NQ; ++q)
+      if (q < NQ - 1 || tid + q * NTH < NE) cp_async_val(dst + q * NTH, fsrc[q] + (fok[q] ? base : 0), fok[q]);
   };
   if (tid < TJ) cj[tid] = coef_at(G, 1, min(j0 + tid, G.n[1]));
   Coef<T> C[3];
@@ -257,7 +256,7 @@ constexpr int kTJ = 8, kTK = 32, kCPT = 2;
 template <typename T, int FL>
 static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
   typedef RingGeom<kTJ, kTK> RG;
-  constexpr int MINB = 5;
+  constexpr int MINB = 4;
   const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T) + kTJ * sizeof(Coef<T>);
   static bool attr = false;
   if (!attr) {
