@@ -51,7 +51,7 @@ __global__ void k_div_int(Geo<T> G, CV<T> U, T* __restrict__ out, Box B) {
 
 // u_a[DOF] -= (p[I+e_a] - p[I]) / du_a   (poisson.py:334-339), p interior
 template <typename T, int D>
-__global__ void k_grad_sub(Geo<T> G, const T* __restrict__ p, MV<T> U, Box B) {
+__global__ void k_grad_sub(Geo<T> G, const T* __restrict__ p, MV<T> U, Box B, T* __restrict__ pe) {
   int I[3];
   if (!box_coords<D>(B, I)) return;
   const long long x = lin<T, D>(G, I);
@@ -67,6 +67,7 @@ __global__ void k_grad_sub(Geo<T> G, const T* __restrict__ p, MV<T> U, Box B) {
     ps[1] = 1;
   }
   const T pc = p[o];
+  if (pe) pe[x] = pc;  // extended pressure interior (ghosts: scalar fill after)
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     if (!is_udof<T, D>(G, I, a)) continue;
@@ -326,13 +327,13 @@ static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) 
     SFB_LAUNCH_CHECK("projection divergence");
     if ((rc = solve_inplace<T>(s, rb, st))) return rc;
   }
-  SFB_DISPATCH_DIM(G.dim, D, (k_grad_sub<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, rb, U, B)));
+  SFB_DISPATCH_DIM(G.dim, D,
+                   (k_grad_sub<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, rb, U, B, (T*)p_ext)));
   SFB_LAUNCH_CHECK("gradient subtract");
   if ((rc = launch_planes<T>(G, U, p->dim, 0, st))) return rc;
   if (p_ext) {
-    Box E = ext_box(G);
-    SFB_DISPATCH_DIM(G.dim, D, (k_p_ext<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, (T*)p_ext, E)));
-    SFB_LAUNCH_CHECK("pressure ghosts");
+    // pressure ghosts (fields.py:81-93) from the interior just written
+    if ((rc = launch_planes<T>(G, MV<T>{{(T*)p_ext, nullptr, nullptr}}, 1, 1, st))) return rc;
   }
   return SFB_OK;
 }
@@ -604,15 +605,11 @@ static int slab_correct(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t
   MV<T> U;
   for (int a = 0; a < 3; ++a) U.c[a] = (T*)u[a];
   Box B = int_box(G);
-  k_grad_sub<T, 3><<<box_grid(3, B), box_block(3), 0, st>>>(G, (const T*)s->rbuf, U, B);
+  k_grad_sub<T, 3><<<box_grid(3, B), box_block(3), 0, st>>>(G, (const T*)s->rbuf, U, B, (T*)p_ext);
   SFB_LAUNCH_CHECK("slab gradient subtract");
   int rc = launch_planes<T>(G, U, 3, 0, st);
   if (rc) return rc;
-  if (p_ext) {
-    Box E = ext_box(G);
-    k_p_ext<T, 3><<<box_grid(3, E), box_block(3), 0, st>>>(G, (const T*)s->rbuf, (T*)p_ext, E);
-    SFB_LAUNCH_CHECK("slab pressure");
-  }
+  if (p_ext && (rc = launch_planes<T>(G, MV<T>{{(T*)p_ext, nullptr, nullptr}}, 1, 1, st))) return rc;
   return SFB_OK;
 }
 }  // namespace sfb
