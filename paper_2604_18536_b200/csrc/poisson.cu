@@ -49,6 +49,57 @@ __global__ void k_div_int(Geo<T> G, CV<T> U, T* __restrict__ out, Box B) {
   out[o] = acc;
 }
 
+// 3D marching divergence: a thread owns a (j, k) column and walks a chunk of
+// planes, carrying u_0 of the previous plane in a register (one fewer load per
+// cell, loads of consecutive planes in flight together).
+template <typename T>
+__global__ void __launch_bounds__(256) k_div_march(Geo<T> G, CV<T> U, T* __restrict__ out, int chunk) {
+  const int k = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = 1 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (k > G.n[2] || j > G.n[1]) return;
+  const int ib = 1 + blockIdx.z * chunk;
+  const int ie = min(ib + chunk, G.n[0] + 1);
+  const long long s0 = G.s[0], s1 = G.s[1];
+  const T* __restrict__ u0 = U.c[0];
+  const T* __restrict__ u1 = U.c[1];
+  const T* __restrict__ u2 = U.c[2];
+  const T r1 = tab(G, 1, T_RDX, j), r2 = tab(G, 2, T_RDX, k);
+  // axis-1 / axis-2 neighbour offsets with inline boundary resolution
+  const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
+  const bool w1lo = !G.per[1] && !G.halo[1] && j == 1, w1hi = !G.per[1] && !G.halo[1] && j == n1;
+  const bool w2lo = !G.per[2] && !G.halo[2] && k == 1, w2hi = !G.per[2] && !G.halo[2] && k == n2;
+  const long long o1m = (G.per[1] && !G.halo[1] && j == 1) ? (long long)(n1 - 1) * s1 : -s1;
+  const long long o2m = (G.per[2] && !G.halo[2] && k == 1) ? (long long)(n2 - 1) : -1;
+  const T v1lo = G.bc_lo[1] == SFB_BC_DIRICHLET ? G.vlo[1][1] : T(0), v1hi = G.bc_hi[1] == SFB_BC_DIRICHLET ? G.vhi[1][1] : T(0);
+  const T v2lo = G.bc_lo[2] == SFB_BC_DIRICHLET ? G.vlo[2][2] : T(0), v2hi = G.bc_hi[2] == SFB_BC_DIRICHLET ? G.vhi[2][2] : T(0);
+  const bool wall0 = !G.per[0] && !G.halo[0];
+  long long x = (long long)ib * s0 + (long long)j * s1 + k;
+  T prev0;
+  if (ib == 1) {
+    if (G.halo[0]) prev0 = u0[x - s0];
+    else if (G.per[0]) prev0 = u0[x + (long long)(n0 - 1) * s0];
+    else prev0 = G.bc_lo[0] == SFB_BC_DIRICHLET ? G.vlo[0][0] : T(0);
+  } else {
+    prev0 = u0[x - s0];
+  }
+  long long o = ((long long)(ib - 1) * n1 + (j - 1)) * n2 + (k - 1);
+  const long long os = (long long)n1 * n2;
+#pragma unroll 4
+  for (int i = ib; i < ie; ++i, x += s0, o += os) {
+    const T m0 = u0[x];
+    const T c0 = (wall0 && i == n0) ? (G.bc_hi[0] == SFB_BC_DIRICHLET ? G.vhi[0][0] : T(0)) : m0;
+    const T c1 = w1hi ? v1hi : u1[x];
+    const T p1 = w1lo ? v1lo : u1[x + o1m];
+    const T c2 = w2hi ? v2hi : u2[x];
+    const T p2 = w2lo ? v2lo : u2[x + o2m];
+    T acc = (c0 - prev0) * tab(G, 0, T_RDX, i);
+    acc += (c1 - p1) * r1;
+    acc += (c2 - p2) * r2;
+    out[o] = acc;
+    prev0 = m0;
+  }
+}
+
 // u_a[DOF] -= (p[I+e_a] - p[I]) / du_a   (poisson.py:334-339), p interior
 template <typename T, int D>
 __global__ void k_grad_sub(Geo<T> G, const T* __restrict__ p, MV<T> U, Box B, T* __restrict__ pe) {
@@ -79,6 +130,50 @@ __global__ void k_grad_sub(Geo<T> G, const T* __restrict__ p, MV<T> U, Box B, T*
   }
 }
 
+// 3D marching gradient-subtract (+ extended pressure interior): a thread owns
+// a (j, k) column and walks a chunk of planes carrying p of the next plane.
+template <typename T>
+__global__ void __launch_bounds__(256) k_grad_march(Geo<T> G, const T* __restrict__ p, MV<T> U, int chunk,
+                                                     T* __restrict__ pe) {
+  const int k = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = 1 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (k > G.n[2] || j > G.n[1]) return;
+  const int ib = 1 + blockIdx.z * chunk;
+  const int ie = min(ib + chunk, G.n[0] + 1);
+  const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
+  const long long s0 = G.s[0], s1 = G.s[1];
+  const long long os = (long long)n1 * n2;
+  T* __restrict__ u0 = U.c[0];
+  T* __restrict__ u1 = U.c[1];
+  T* __restrict__ u2 = U.c[2];
+  const bool per1 = G.per[1] && !G.halo[1], per2 = G.per[2] && !G.halo[2];
+  const bool dof1 = !(!G.per[1] && j == n1), dof2 = !(!G.per[2] && k == n2);
+  const long long oj = (j == n1 && per1) ? -(long long)(n1 - 1) * n2 : n2;
+  const long long ok = (k == n2 && per2) ? -(long long)(n2 - 1) : 1;
+  const T r1 = tab(G, 1, T_RDU, j), r2 = tab(G, 2, T_RDU, k);
+  const bool per0 = G.per[0] && !G.halo[0], wall0 = !G.per[0];
+  long long x = (long long)ib * s0 + (long long)j * s1 + k;
+  long long o = ((long long)(ib - 1) * n1 + (j - 1)) * n2 + (k - 1);
+  T pc = p[o];
+#pragma unroll 4
+  for (int i = ib; i < ie; ++i, x += s0, o += os) {
+    // next plane (periodic wrap at i = n0; a halo axis reads the stored halo plane)
+    const long long on = (i == n0 && per0) ? o - (long long)(n0 - 1) * os : o + os;
+    const bool has_next = !(wall0 && i == n0);
+    const T pn = (has_next || i < n0) ? p[on] : pc;
+    const T pj = dof1 ? p[o + oj] : pc;
+    const T pk = dof2 ? p[o + ok] : pc;
+    if (pe) pe[x] = pc;
+    if (has_next) u0[x] -= (pn - pc) * tab(G, 0, T_RDU, i);
+    if (dof1) u1[x] -= (pj - pc) * r1;
+    if (dof2) u2[x] -= (pk - pc) * r2;
+    pc = pn;
+  }
+}
+
+template <typename T>
+static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t st);
+
 // extended, ghost-filled pressure from the interior solution (fields.py:81-93)
 template <typename T, int D>
 __global__ void k_p_ext(Geo<T> G, const T* __restrict__ p, T* __restrict__ pe, Box B) {
@@ -101,6 +196,46 @@ __global__ void k_p_ext(Geo<T> G, const T* __restrict__ p, T* __restrict__ pe, B
   long long o = (long long)J[0] * G.n[1] + J[1];
   if (D == 3) o = o * G.n[2] + J[2];
   pe[lin<T, D>(G, I)] = p[o];
+}
+
+template <typename T>
+static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t st) {
+  if (G.dim == 3 && !getenv("SFB_GRAD_GENERIC")) {
+    dim3 blk(64, 4);
+    const int bx = (G.n[2] + 63) / 64, by = (G.n[1] + 3) / 4;
+    const long long bps = (long long)bx * by;
+    long long want = (4LL * 148 * 8 + bps - 1) / bps;
+    int chunk = (int)((G.n[0] + want - 1) / want);
+    if (chunk < 8) chunk = 8;
+    const int bz = (G.n[0] + chunk - 1) / chunk;
+    k_grad_march<T><<<dim3(bx, by, bz), blk, 0, st>>>(G, p, U, chunk, pe);
+    SFB_LAUNCH_CHECK("gradient subtract (march)");
+    return SFB_OK;
+  }
+  Box B = int_box(G);
+  SFB_DISPATCH_DIM(G.dim, D, (k_grad_sub<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, p, U, B, pe)));
+  SFB_LAUNCH_CHECK("gradient subtract");
+  return SFB_OK;
+}
+
+template <typename T>
+static int launch_div(const Geo<T>& G, CV<T> C, T* out, cudaStream_t st) {
+  if (G.dim == 3 && !getenv("SFB_DIV_GENERIC")) {
+    dim3 blk(64, 4);
+    const int bx = (G.n[2] + 63) / 64, by = (G.n[1] + 3) / 4;
+    const long long bps = (long long)bx * by;
+    long long want = (4LL * 148 * 8 + bps - 1) / bps;
+    int chunk = (int)((G.n[0] + want - 1) / want);
+    if (chunk < 8) chunk = 8;
+    const int bz = (G.n[0] + chunk - 1) / chunk;
+    k_div_march<T><<<dim3(bx, by, bz), blk, 0, st>>>(G, C, out, chunk);
+    SFB_LAUNCH_CHECK("divergence (march)");
+    return SFB_OK;
+  }
+  Box B = int_box(G);
+  SFB_DISPATCH_DIM(G.dim, D, (k_div_int<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, C, out, B)));
+  SFB_LAUNCH_CHECK("projection divergence");
+  return SFB_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -323,13 +458,10 @@ static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) 
     // divergence fused into the first FFT pass
     if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, (const void* const*)u))) return rc;
   } else {
-    SFB_DISPATCH_DIM(G.dim, D, (k_div_int<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, C, rb, B)));
-    SFB_LAUNCH_CHECK("projection divergence");
+    if ((rc = launch_div<T>(G, C, rb, st))) return rc;
     if ((rc = solve_inplace<T>(s, rb, st))) return rc;
   }
-  SFB_DISPATCH_DIM(G.dim, D,
-                   (k_grad_sub<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, rb, U, B, (T*)p_ext)));
-  SFB_LAUNCH_CHECK("gradient subtract");
+  if ((rc = launch_grad<T>(G, rb, U, (T*)p_ext, st))) return rc;
   if ((rc = launch_planes<T>(G, U, p->dim, 0, st))) return rc;
   if (p_ext) {
     // pressure ghosts (fields.py:81-93) from the interior just written
@@ -592,9 +724,8 @@ static int slab_forward(sfb_solver* s, void* const* u, cudaStream_t st) {
   const Geo<T>& G = geo<T>(p);
   CV<T> C;
   for (int a = 0; a < 3; ++a) C.c[a] = (const T*)u[a];
-  Box B = int_box(G);
-  k_div_int<T, 3><<<box_grid(3, B), box_block(3), 0, st>>>(G, C, (T*)s->rbuf, B);
-  SFB_LAUNCH_CHECK("slab divergence");
+  int rc = launch_div<T>(G, C, (T*)s->rbuf, st);
+  if (rc) return rc;
   return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st);
 }
 
@@ -605,9 +736,9 @@ static int slab_correct(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t
   MV<T> U;
   for (int a = 0; a < 3; ++a) U.c[a] = (T*)u[a];
   Box B = int_box(G);
-  k_grad_sub<T, 3><<<box_grid(3, B), box_block(3), 0, st>>>(G, (const T*)s->rbuf, U, B, (T*)p_ext);
-  SFB_LAUNCH_CHECK("slab gradient subtract");
-  int rc = launch_planes<T>(G, U, 3, 0, st);
+  int rc = launch_grad<T>(G, (const T*)s->rbuf, U, (T*)p_ext, st);
+  if (rc) return rc;
+  rc = launch_planes<T>(G, U, 3, 0, st);
   if (rc) return rc;
   if (p_ext && (rc = launch_planes<T>(G, MV<T>{{(T*)p_ext, nullptr, nullptr}}, 1, 1, st))) return rc;
   return SFB_OK;
