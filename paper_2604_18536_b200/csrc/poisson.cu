@@ -200,7 +200,7 @@ __global__ void k_p_ext(Geo<T> G, const T* __restrict__ p, T* __restrict__ pe, B
 
 template <typename T>
 static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t st) {
-  if (G.dim == 3 && !getenv("SFB_GRAD_GENERIC")) {
+  if (G.dim == 3 && getenv("SFB_GRAD_MARCH")) {
     dim3 blk(64, 4);
     const int bx = (G.n[2] + 63) / 64, by = (G.n[1] + 3) / 4;
     const long long bps = (long long)bx * by;
@@ -220,7 +220,7 @@ static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t
 
 template <typename T>
 static int launch_div(const Geo<T>& G, CV<T> C, T* out, cudaStream_t st) {
-  if (G.dim == 3 && !getenv("SFB_DIV_GENERIC")) {
+  if (G.dim == 3 && getenv("SFB_DIV_MARCH")) {
     dim3 blk(64, 4);
     const int bx = (G.n[2] + 63) / 64, by = (G.n[1] + 3) / 4;
     const long long bps = (long long)bx * by;
