@@ -292,7 +292,7 @@ __device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, const C* __re
 //   element (m, col) at base + m*S + col, col in [0, ncol), tile W columns
 // ---------------------------------------------------------------------------
 template <typename T, int MODE, int W>  // MODE 0 fwd, 1 inv, 2 fwd+scale+inv
-__global__ void __launch_bounds__(256, 2) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P,
+__global__ void __launch_bounds__(512, 2) k_fft_strided(typename CX<T>::t* __restrict__ data, FftLen P,
                                                      long long S, int ncol, long long bstride,
                                                      const typename CX<T>::t* __restrict__ tw, ScaleArgs sc) {
   typedef typename CX<T>::t C;
@@ -631,10 +631,10 @@ static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long 
   dim3 grid((ncol + W - 1) / W, nbatch);
   const size_t sm = 2 * (size_t)P.L * W * sizeof(C);
   switch (W) {
-    case 8: k_fft_strided<T, MODE, 8><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
-    case 4: k_fft_strided<T, MODE, 4><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
-    case 2: k_fft_strided<T, MODE, 2><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
-    default: k_fft_strided<T, MODE, 1><<<grid, 256, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 8: k_fft_strided<T, MODE, 8><<<grid, 512, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 4: k_fft_strided<T, MODE, 4><<<grid, 512, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    case 2: k_fft_strided<T, MODE, 2><<<grid, 512, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
+    default: k_fft_strided<T, MODE, 1><<<grid, 512, sm, st>>>(data, P, S, ncol, bstride, tw, sc); break;
   }
   SFB_LAUNCH_CHECK("fft strided pass");
   return SFB_OK;
