@@ -506,6 +506,14 @@ static int setup_fft(sfb_solver* s) {
   F.sc.invN = 1.0 / (double)p->int_count;
   F.sc.zero_ok = 1;
   F.enabled = true;
+  if (dim == 3 && !getenv("SFB_NO_TMA")) {
+    const int n0 = p->n[0], n1 = p->n[1];
+    const long long nh = nlast / 2 + 1;
+    // axis-1 pass: box over (nh complex columns, n1 rows, n0 batch); axis-0: (n1*nh, n0)
+    if (fft_tma_fits(n1, f64) && (rc = fft_tma_make(F.tma_ax1, s->cbuf, f64, 3, nh, n1, n0, n1))) return rc;
+    if (fft_tma_fits(n0, f64) && (rc = fft_tma_make(F.tma_ax0, s->cbuf, f64, 2, (long long)n1 * nh, n0, 1, n0)))
+      return rc;
+  }
   return SFB_OK;
 }
 
@@ -697,6 +705,12 @@ int sfb_slab_solver_create(sfb_plan* p, int n0g, int rank, int nranks, sfb_solve
   F.sc.invN = 1.0 / ((double)n0g * n1 * n2);
   F.sc.zero_ok = rank == 0;
   F.enabled = true;
+  if (!getenv("SFB_NO_TMA")) {
+    if (fft_tma_fits(n1, f64) && (rc = fft_tma_make(F.tma_ax1, s->cbuf, f64, 3, nh, n1, m, n1))) goto bad;
+    if (fft_tma_fits(n0g, f64) &&
+        (rc = fft_tma_make(F.tma_ax0, s->tbuf, f64, 2, (long long)(n1 / nranks) * nh, n0g, 1, n0g)))
+      goto bad;
+  }
   *out = s;
   return SFB_OK;
 bad:

@@ -1,6 +1,8 @@
 // Hand-written FFT engine (fft.cu) declarations.
 #pragma once
 
+#include <cuda.h>
+
 #include "sfb_common.cuh"
 
 namespace sfb {
@@ -20,6 +22,14 @@ struct ScaleArgs {
   int zero_ok;                // this chunk holds the k = 0 mode (zeroed)
 };
 
+// TMA description of one strided pass: a (2W x Lb [x batch]) box over the
+// complex buffer viewed as reals; nbox boxes cover the transform length.
+struct FftTma {
+  CUtensorMap map;
+  int rank = 0, nbox = 0, lb = 0, ncol = 0, nbatch = 0;
+  bool ok = false;
+};
+
 struct FftSolve {
   bool enabled = false;
   int dim = 0;
@@ -31,6 +41,7 @@ struct FftSolve {
   void* tw_full = nullptr;  // exp(-2 pi i k / n_last), k < n_last
   void* tw_ax[3] = {nullptr, nullptr, nullptr};
   ScaleArgs sc{};
+  FftTma tma_ax1, tma_ax0;  // TMA maps of the axis-1 and axis-0 passes (3D)
 };
 
 bool fft_factor(int L, FftLen& P);
@@ -43,6 +54,11 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const G
                       const void* const* u = nullptr);
 template <typename T>
 int fft_set_smem_limits();
+bool fft_tma_fits(int L, bool f64);
+int fft_tma_make(FftTma& M, void* base, bool f64, int rank, long long inner_complex, long long rows, long long batch,
+                 int L);
+template <typename T, int MODE>
+int fft_tma_pass(const FftTma& M, const FftLen& P, const void* tw, const ScaleArgs& sc, cudaStream_t st);
 template <typename T>
 int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st);
 template <typename T>
