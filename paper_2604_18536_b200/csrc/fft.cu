@@ -349,6 +349,7 @@ int fft_upload_pass_twiddles(FftLen& P, bool f64, void** dev) {
         for (int r = 1; r < R; ++r) push_root(t, (long long)k * r * step, L);
     Ns *= R;
   }
+  P.twn = (int)(t.size() / 2);
   return upload(t, f64, dev);
 }
 

@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_tma(const __grid_constant__ CUten
   C* buf[3] = {reinterpret_cast<C*>(smem_raw), reinterpret_cast<C*>(smem_raw) + bufc,
                reinterpret_cast<C*>(smem_raw) + 2 * bufc};
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw + 3 * bufc * sizeof(C));
+  C* stw = reinterpret_cast<C*>(smem_raw + 3 * bufc * sizeof(C) + 64);  // twiddle tables staged once per CTA
+  for (int e = threadIdx.x; e < P.twn; e += NT) stw[e] = tw[e];
   const unsigned tile_bytes = (unsigned)(bufc * sizeof(C));
   const int ntx = (tt.ncol + W - 1) / W;
   const int ntiles = ntx * tt.nbatch;
@@ -110,8 +112,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_tma(const __grid_constant__ CUten
     mbar_wait(&bars[cur], phase[cur]);
     phase[cur] ^= 1;
     C* res;
-    if (MODE == 1) res = run_fft<C, true, W>(buf[cur], buf[tmp], P, tw);
-    else res = run_fft<C, false, W>(buf[cur], buf[tmp], P, tw);
+    if (MODE == 1) res = run_fft<C, true, W, true>(buf[cur], buf[tmp], P, stw);
+    else res = run_fft<C, false, W, true>(buf[cur], buf[tmp], P, stw);
     const int bx = t % ntx, by = t / ntx;
     const int c0 = bx * W;
     if (MODE == 2) {
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_tma(const __grid_constant__ CUten
         }
       }
       C* other = (res == buf[cur]) ? buf[tmp] : buf[cur];
-      res = run_fft<C, true, W>(res, other, P, tw);
+      res = run_fft<C, true, W, true>(res, other, P, stw);
     }
     // results of this tile -> HBM by TMA; smem writes must be visible to the async proxy
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -198,10 +200,14 @@ int fft_tma_make(FftTma& M, void* base, bool f64, int rank, long long inner_comp
   cuuint64_t strides[2] = {(cuuint64_t)(2 * inner_complex * esz), (cuuint64_t)(2 * inner_complex * esz * rows)};
   cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)lb, 1};
   cuuint32_t estr[3] = {1, 1, 1};
+  M.ok = false;
+  // TMA needs 16-byte multiples for the global strides; otherwise keep the
+  // cp.async path for this pass
+  if ((strides[0] % 16) != 0 || (rank == 3 && (strides[1] % 16) != 0) || ((uintptr_t)base % 16) != 0) return SFB_OK;
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(&M.map), f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    (cuuint32_t)rank, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(SFB_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  if (r != CUDA_SUCCESS) return SFB_OK;  // unsupported geometry: cp.async path
   M.rank = rank;
   M.nbox = nbox;
   M.lb = lb;
@@ -217,7 +223,7 @@ int fft_tma_pass(const FftTma& M, const FftLen& P, const void* tw, const ScaleAr
   constexpr int W = sizeof(T) == 8 ? 4 : 8;
   static int nsm = 0;
   static bool attr = false;
-  const size_t smem = 3 * (size_t)M.nbox * M.lb * W * sizeof(C) + 64;
+  const size_t smem = 3 * (size_t)M.nbox * M.lb * W * sizeof(C) + 64 + (size_t)P.twn * sizeof(C);
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   if (!attr) {
     cudaFuncSetAttribute(k_fft_tma<T, MODE, W, kTmaNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -242,7 +248,7 @@ bool fft_tma_fits(int L, bool f64) {
   const int W = tma_w(f64);
   const int nbox = (L + 255) / 256;
   const int lb = (((L + nbox - 1) / nbox) + 1) & ~1;
-  const size_t bytes = 3 * (size_t)nbox * lb * W * (f64 ? 16 : 8) + 64;
+  const size_t bytes = 3 * (size_t)nbox * lb * W * (f64 ? 16 : 8) + 64 + 2 * (size_t)L * (f64 ? 16 : 8);
   return bytes <= 227 * 1024;
 }
 

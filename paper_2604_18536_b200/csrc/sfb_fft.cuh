@@ -12,6 +12,7 @@ struct FftLen {
   int np;         // number of Stockham passes
   int radix[12];  // radices in pass order
   int twoff[12];  // offset of each pass's twiddle table (after the plain table)
+  int twn;        // total twiddle entries (plain + per-pass)
 };
 
 struct ScaleArgs {

@@ -214,7 +214,7 @@ __device__ __forceinline__ void divmod_ns(int j, int Ns, float inv, int& q, int&
 // One Stockham pass over a tile stored [m][w] (m < L, w < W): src -> dst.
 // Thread t owns column t % W and butterflies j = t / W + s * (NT / W).
 // twp: this pass's twiddles laid out [k][r-1] (contiguous per butterfly).
-template <typename C, int R, bool INV, int W>
+template <typename C, int R, bool INV, int W, bool TWS = false>
 __device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restrict__ dst, int L, int Ns,
                                          const C* __restrict__ twp) {
   const int nb = L / R;
@@ -235,7 +235,7 @@ __device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restric
       const C* tp = twp + k * (R - 1);
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        C w = __ldg(tp + (r - 1));
+        C w = TWS ? tp[r - 1] : __ldg(tp + (r - 1));
         if (INV) w.y = -w.y;
         v[r] = cmul(v[r], w);
       }
@@ -249,19 +249,19 @@ __device__ __forceinline__ void stockham(const C* __restrict__ src, C* __restric
 
 // Run all passes of a length-L plan; returns the buffer holding the result.
 // tw: plain table exp(-2 pi i m / L) followed by the per-pass tables.
-template <typename C, bool INV, int W>
+template <typename C, bool INV, int W, bool TWS = false>
 __device__ __forceinline__ C* run_fft(C* a, C* b, const FftLen& P, const C* __restrict__ tw) {
   int Ns = 1;
   for (int p = 0; p < P.np; ++p) {
     __syncthreads();
     const C* twp = tw + P.twoff[p];
     switch (P.radix[p]) {
-      case 8: stockham<C, 8, INV, W>(a, b, P.L, Ns, twp); break;
-      case 4: stockham<C, 4, INV, W>(a, b, P.L, Ns, twp); break;
-      case 2: stockham<C, 2, INV, W>(a, b, P.L, Ns, twp); break;
-      case 7: stockham<C, 7, INV, W>(a, b, P.L, Ns, twp); break;
-      case 5: stockham<C, 5, INV, W>(a, b, P.L, Ns, twp); break;
-      default: stockham<C, 3, INV, W>(a, b, P.L, Ns, twp); break;
+      case 8: stockham<C, 8, INV, W, TWS>(a, b, P.L, Ns, twp); break;
+      case 4: stockham<C, 4, INV, W, TWS>(a, b, P.L, Ns, twp); break;
+      case 2: stockham<C, 2, INV, W, TWS>(a, b, P.L, Ns, twp); break;
+      case 7: stockham<C, 7, INV, W, TWS>(a, b, P.L, Ns, twp); break;
+      case 5: stockham<C, 5, INV, W, TWS>(a, b, P.L, Ns, twp); break;
+      default: stockham<C, 3, INV, W, TWS>(a, b, P.L, Ns, twp); break;
     }
     Ns *= P.radix[p];
     C* t = a;
