@@ -1,0 +1,56 @@
+// Shared pieces of the RK-stage kernels (stage.cu, stage_pair.cu).
+#pragma once
+
+#include "sfb_kernels.cuh"
+
+namespace sfb {
+
+template <typename T>
+struct StageArgs {
+  CV<T> y, u0, s_in;
+  MV<T> s_out, y_next, k_out;
+  T cb, ca, nu;
+  Force<T> F;
+  int has_s, has_next, has_k, s_from_u0, diff;
+};
+
+template <typename T>
+__device__ __forceinline__ void cp_async_val(T* smem, const T* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? (int)sizeof(T) : 0;
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Coefficients of one axis at one index (operators.py:47-84 tables).
+template <typename T>
+struct Coef {
+  T rdu, wlo, whi, ohi, olo, rdx, thi, tlo;
+};
+template <typename T>
+__device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
+  Coef<T> c;
+  c.rdu = tab(G, axis, T_RDU, i);
+  c.wlo = tab(G, axis, T_WLO, i);
+  c.whi = tab(G, axis, T_WHI, i);
+  c.ohi = tab(G, axis, T_OHI, i);
+  c.olo = tab(G, axis, T_OLO, i);
+  c.rdx = tab(G, axis, T_RDX, i);
+  c.thi = tab(G, axis, T_THI, i);
+  c.tlo = tab(G, axis, T_TLO, i);
+  return c;
+}
+
+// epilogue variants (compile-time): bit 1 k_out, bit 2 s_out, bit 4 s from
+// u0 (else s_in), bit 8 y_next
+enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8 };
+
+template <typename T>
+int stage_pair(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st);
+
+}  // namespace sfb

@@ -11,18 +11,9 @@
 // (u0, s, y, y_next), which is what lets 840^3 fp64 fit on one B200.
 #include <cstdlib>
 
-#include "sfb_kernels.cuh"
+#include "sfb_stage.cuh"
 
 namespace sfb {
-
-template <typename T>
-struct StageArgs {
-  CV<T> y, u0, s_in;
-  MV<T> s_out, y_next, k_out;
-  T cb, ca, nu;
-  Force<T> F;
-  int has_s, has_next, has_k, s_from_u0, diff;
-};
 
 template <typename T, int D>
 __global__ void __launch_bounds__(256) k_stage_generic(Geo<T> G, StageArgs<T> A, Box B) {
@@ -51,42 +42,10 @@ __global__ void __launch_bounds__(256) k_stage_generic(Geo<T> G, StageArgs<T> A,
 // the stencil's 27 reads per cell come from shared memory.  u0 / s are read
 // and s / y_next written once, coalesced, at the centre.
 // ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ void cp_async_val(T* smem, const T* gmem, bool pred) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = pred ? (int)sizeof(T) : 0;
-  if constexpr (sizeof(T) == 8)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 template <int TJ, int TK>
 struct RingGeom {
   static constexpr int PW = TK + 2, PH = TJ + 2, PS = PW * PH, NT = TJ * TK;
 };
-
-// Coefficients of one axis at one index (operators.py:47-84 tables).
-template <typename T>
-struct Coef {
-  T rdu, wlo, whi, ohi, olo, rdx, thi, tlo;
-};
-template <typename T>
-__device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
-  Coef<T> c;
-  c.rdu = tab(G, axis, T_RDU, i);
-  c.wlo = tab(G, axis, T_WLO, i);
-  c.whi = tab(G, axis, T_WHI, i);
-  c.ohi = tab(G, axis, T_OHI, i);
-  c.olo = tab(G, axis, T_OLO, i);
-  c.rdx = tab(G, axis, T_RDX, i);
-  c.thi = tab(G, axis, T_THI, i);
-  c.tlo = tab(G, axis, T_TLO, i);
-  return c;
-}
 
 // Momentum RHS of component A at the thread's cell from the smem ring, same
 // arithmetic and order as rhs_comp (sfb_kernels.cuh).  P[d] points at the
@@ -134,10 +93,6 @@ __device__ __forceinline__ T rhs_ring(const T* const (&P)[3], const Coef<T> (&C)
 }
 
 constexpr int kRing = 5;  // planes i-1, i, i+1 in use, i+2 landing, i+3 issued
-
-// epilogue variants (compile-time): bit 1 k_out, bit 2 s_out, bit 4 s from
-// u0 (else s_in), bit 8 y_next
-enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8 };
 
 template <typename T, int TJ, int TK, int CPT, int FL, int MINB>
 __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
@@ -315,6 +270,10 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
   if (G.dim == 3 && !getenv("SFB_STAGE_GENERIC")) {
+    if (!getenv("SFB_NO_PAIR")) {
+      const int rcp = stage_pair<T>(G, A, st);
+      if (rcp >= 0) return rcp;
+    }
     const int rc = stage_march<T>(G, A, st);
     if (rc >= 0) return rc;
   }
