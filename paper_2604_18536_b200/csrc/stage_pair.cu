@@ -41,11 +41,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
 template <int FL>
-__global__ void __launch_bounds__(PNT, 3) k_stage_pair(Geo<double> G, StageArgs<double> A, int chunk) {
+__global__ void __launch_bounds__(PNT, 4) k_stage_pair(Geo<double> G, StageArgs<double> A, int chunk) {
   typedef double T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);                      // [PRING][3][PPH][PPW]
   Coef<T>* cj = reinterpret_cast<Coef<T>*>(ring + PRING * PNE);  // axis-1 coefficients of the tile rows
+  Coef<T>* ck = cj + PTJ;                                        // axis-2 coefficients of the tile cells
   const int tp = threadIdx.x, tq = threadIdx.y, tid = tq * (PTK / 2) + tp;
   const int kb = blockIdx.x * PTK;  // even extended k of the tile start
   const int j0 = 1 + blockIdx.y * PTJ;
@@ -86,9 +87,7 @@ __global__ void __launch_bounds__(PNT, 3) k_stage_pair(Geo<double> G, StageArgs<
   const bool jin = j <= G.n[1];
   const bool v0 = jin && k >= 1 && k <= G.n[2];
   const bool v1 = jin && k + 1 >= 1 && k + 1 <= G.n[2];
-  Coef<T> C2[2];
-  C2[0] = coef_at(G, 2, min(max(k, 1), G.n[2]));
-  C2[1] = coef_at(G, 2, min(max(k + 1, 1), G.n[2]));
+  if (tid < PTK) ck[tid] = coef_at(G, 2, min(max(kb + tid, 1), G.n[2]));
 
   int sl_m = (ib - 1) % PRING;
   load_plane(ib - 1, sl_m);
@@ -161,7 +160,7 @@ __global__ void __launch_bounds__(PNT, 3) k_stage_pair(Geo<double> G, StageArgs<
     T kv[2][3];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const Coef<T>& Ck = C2[q];
+      const Coef<T> Ck = ck[2 * tp + q];
       // neighbours of component a at cell q along axis b: up/um
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -241,7 +240,7 @@ __global__ void __launch_bounds__(PNT, 3) k_stage_pair(Geo<double> G, StageArgs<
 
 template <int FL>
 static int pair_launch(const Geo<double>& G, const StageArgs<double>& A, cudaStream_t st) {
-  const size_t smem = (size_t)PRING * PNE * sizeof(double) + PTJ * sizeof(Coef<double>);
+  const size_t smem = (size_t)PRING * PNE * sizeof(double) + (PTJ + PTK) * sizeof(Coef<double>);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_stage_pair<FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
