@@ -100,8 +100,8 @@ int sfb_momentum_rhs(sfb_plan* plan, const void* const* u, double nu, const doub
 
 /* RK building blocks (timestep.py:166-214). */
 int sfb_rk_stage(sfb_plan* plan, const sfb_stage_args* args, void* stream);
-/* dst = base + sum_l k[l]*coef[l] on DOFs (acc.copy_from + _axpy chain).
- * k: flat array of nk*3 component pointers, k[3*l + a]. */
+/* dst = base + sum_l k[l]*coef[l] on DOFs (acc.copy_from + _axpy chain);
+ * base == NULL means zero.  k: flat array of nk*3 component pointers, k[3*l + a]. */
 int sfb_combine(sfb_plan* plan, void* const* dst, const void* const* base, int nk,
                 const void* const* k, const double* coef, void* stream);
 /* Wray3 register update (timestep.py:231-246): fnew *= g; u += fnew; if fold: fold *= z; u += fold. */
@@ -160,6 +160,9 @@ int sfb_rhs_pullback(sfb_plan* plan, void* const* vbar, const void* const* u, do
                      void* const* out, double scale, int accumulate, void* stream);
 /* project_pullback (adjoint.py:335-349): out = vbar + D^T S^T G^T(-vbar). */
 int sfb_project_pullback(sfb_solver* s, void* const* vbar, void* const* out, void* stream);
+/* Same, with out optional (NULL) and, if acc != NULL, acc += result on DOFs
+ * (the g0 accumulation of step_backward, adjoint.py:412-415, fused). */
+int sfb_project_pullback_ex(sfb_solver* s, void* const* vbar, void* const* out, void* const* acc, void* stream);
 
 #ifdef __cplusplus
 }

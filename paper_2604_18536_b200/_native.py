@@ -87,6 +87,7 @@ _SIGS = {
     "sfb_convection_pullback": [vp, VP3, VP3, VP3, vp],
     "sfb_rhs_pullback": [vp, VP3, VP3, ctypes.c_double, VP3, ctypes.c_double, ctypes.c_int, vp],
     "sfb_project_pullback": [vp, VP3, VP3, vp],
+    "sfb_project_pullback_ex": [vp, VP3, ctypes.POINTER(VP3), ctypes.POINTER(VP3), vp],
 }
 
 EXPORTED = sorted(list(_SIGS) + ["sfb_abi_version", "sfb_last_error"])
@@ -136,7 +137,7 @@ KERNELS_PER_CALL = {
     "sfb_diffusion": 1, "sfb_momentum_rhs": 1, "sfb_weighted_scale": 1, "sfb_kinetic_energy": 2,
     "sfb_weighted_inner": 2, "sfb_cfl_conv": 2, "sfb_solver_solve": 1, "sfb_project": 4,
     "sfb_divergence_pullback": 2, "sfb_pressure_gradient_pullback": 2, "sfb_diffusion_pullback": 2,
-    "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4,
+    "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4, "sfb_project_pullback_ex": 4,
     "sfb_slab_forward": 3, "sfb_slab_axis0": 1, "sfb_slab_inverse": 2, "sfb_slab_correct": 2,
 }
 launches = 0
@@ -146,7 +147,7 @@ def call(name, *args):
     global launches
     check(getattr(lib, name)(*args))
     k = KERNELS_PER_CALL.get(name, 0)
-    if name in ("sfb_project", "sfb_project_pullback", "sfb_solver_solve"):
+    if name in ("sfb_project", "sfb_project_pullback", "sfb_project_pullback_ex", "sfb_solver_solve"):
         own = lib.sfb_solver_uses_own_fft(args[0])
         k += 4 if own else 0
     if name == "sfb_project" and args[2] is not None and args[2] != 0:

@@ -187,7 +187,7 @@ def project_pullback(vbar, solver, bcs):
     (gradient pullback -> weighted solve -> divergence pullback)."""
     _require_periodic(bcs)
     s = _native_solver(solver, bcs)
-    out = VelocityField(vbar.grid)
+    out = VelocityField(vbar.grid, empty=True)
     N.call("sfb_project_pullback", s.handle, N.ptr3(vbar.u), N.ptr3(out.u), stream_ptr())
     return out
 
@@ -202,8 +202,7 @@ def _axpy_into(grid, dst, src, coef):
 
 def step_forward_tape(u0, dt, tableau, solver, setup):
     """adjoint.py:352-384: one projected RK step recording the stage states.
-    Uses the same fused stage kernels as rk_step, so the primal trajectory is
-    bitwise the in-place one."""
+    Uses the same stage kernels as rk_step."""
     from .timestep import _combine, _stage
     from .poisson import project_into
 
@@ -217,29 +216,81 @@ def step_forward_tape(u0, dt, tableau, solver, setup):
         if j == 0:
             yj = u0
         else:
-            yj = VelocityField(grid)
+            yj = VelocityField(grid, empty=True)
             terms = [(ks[l], dt * tableau.a[j][l]) for l in range(j) if tableau.a[j][l] != 0.0]
             _combine(grid, yj, u0, [k for k, _ in terms], [c for _, c in terms])
             project_into(yj, solver, bcs)
         stages.append(yj)
-        kj = VelocityField(grid)
+        kj = VelocityField(grid, empty=True)
         _stage(setup, yj, k_out=kj)
         ks.append(kj)
-    u1 = VelocityField(grid)
+    u1 = VelocityField(grid, empty=True)
     terms = [(ks[l], dt * tableau.b[l]) for l in range(s) if tableau.b[l] != 0.0]
     _combine(grid, u1, u0, [k for k, _ in terms], [c for _, c in terms])
     project_into(u1, solver, bcs)
     return u1, (stages, dt, tableau)
 
 
+def _combine_into(grid, dst, terms):
+    """dst = sum coef*field on DOFs (no base): one kernel."""
+    from .timestep import _combine
+
+    N.call("sfb_combine", _plan(grid), N.ptr3(dst.u), None, len(terms),
+           _ks(terms), (N.ctypes.c_double * max(len(terms), 1))(*[c for _, c in terms]), stream_ptr())
+    _ = _combine
+
+
+def _ks(terms):
+    karr = (N.VP3 * max(len(terms), 1))()
+    for i, (f, _) in enumerate(terms):
+        karr[i] = N.ptr3(f.u)
+    return karr
+
+
+def _project_pullback_into(vbar, solver, bcs, out=None, acc=None):
+    s = _native_solver(solver, bcs)
+    N.call("sfb_project_pullback_ex", s.handle, N.ptr3(vbar.u),
+           N.ctypes.byref(N.ptr3(out.u)) if out is not None else None,
+           N.ctypes.byref(N.ptr3(acc.u)) if acc is not None else None, stream_ptr())
+
+
 def step_backward(tape, ubar, solver, setup):
-    """adjoint.py:387-422"""
+    """adjoint.py:387-422.
+
+    For sub-diagonal tableaus (RK4) the stage cotangents are formed on the fly,
+    kbar_j = dt*b_j*ybar + dt*a_{j+1,j}*ybar_{j+1} (one combine kernel, no
+    zero-initialised accumulators), and ``g0 += ybar_j`` is fused into the
+    projection pullback; the generic path follows the reference loop."""
     stages, dt, tableau = tape
     bcs = setup.bcs
     grid = stages[0].grid
     s = tableau.stages
     ybar = project_pullback(ubar, solver, bcs)
     g0 = ybar.copy()
+    if tableau.subdiagonal:
+        kb = VelocityField(grid, empty=True)
+        fb = VelocityField(grid, empty=True)
+        ynext = None
+        spare = VelocityField(grid, empty=True)
+        for j in reversed(range(s)):
+            terms = []
+            if tableau.b[j] != 0.0:
+                terms.append((ybar, dt * tableau.b[j]))
+            if ynext is not None and j + 1 < s and tableau.a[j + 1][j] != 0.0:
+                terms.append((ynext, dt * tableau.a[j + 1][j]))
+            if not terms:
+                ynext = None
+                continue
+            _combine_into(grid, kb, terms)
+            if j == 0:
+                rhs_pullback(kb, stages[0], setup.nu, bcs, out=g0, accumulate=True)
+                continue
+            rhs_pullback(kb, stages[j], setup.nu, bcs, out=fb)
+            yj = spare
+            _project_pullback_into(fb, solver, bcs, out=yj, acc=g0)
+            spare = ynext if ynext is not None else VelocityField(grid, empty=True)
+            ynext = yj
+        return g0
     kbars = [None] * s
     for l in range(s):
         if tableau.b[l] != 0.0:

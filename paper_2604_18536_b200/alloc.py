@@ -25,5 +25,14 @@ def zeros(shape, dtype, device=None):
     return torch.zeros(tuple(shape), dtype=torch_dtype(dtype), device=device)
 
 
+def empty(shape, dtype, device=None):
+    """Uninitialised buffer for outputs a kernel writes completely."""
+    global _count
+    _count += 1
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return torch.empty(tuple(shape), dtype=torch_dtype(dtype), device=device)
+
+
 def allocation_count():
     return _count

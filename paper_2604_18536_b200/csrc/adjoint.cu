@@ -205,13 +205,15 @@ __global__ void __launch_bounds__(256) k_rhs_pb(Geo<T> G, CV<T> Vb, CV<T> U, MV<
 
 // projection pullback tail: out_a = vbar_a + D^T(w * s)  (adjoint.py:335-349)
 template <typename T, int D>
-__global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T> O, Box B) {
+__global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T> O, Box B, MV<T> Acc) {
   int J[3];
   if (!box_coords<D>(B, J)) return;
   const long long x = lin<T, D>(G, J);
   if (!is_pdof<T, D>(G, J)) {
+    if (O.c[0]) {
 #pragma unroll
-    for (int a = 0; a < D; ++a) O.c[a][x] = T(0);
+      for (int a = 0; a < D; ++a) O.c[a][x] = T(0);
+    }
     return;
   }
   auto sbar = [&](const int K[3]) -> T {
@@ -228,7 +230,9 @@ __global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T
     int K[3] = {J[0], J[1], J[2]};
     K[a] = wr(J[a] + 1, G.n[a]);
     const T d = s0 * tab(G, a, T_RDX, J[a]) - sbar(K) * tab(G, a, T_RDX, K[a]);
-    O.c[a][x] = Vb.c[a][x] + d;
+    const T r = Vb.c[a][x] + d;
+    if (O.c[0]) O.c[a][x] = r;
+    if (Acc.c[0]) Acc.c[a][x] += r;  // g0 += ybar_j (adjoint.py:414-415)
   }
 }
 
@@ -251,7 +255,7 @@ static int need_periodic(const sfb_plan* p) {
 }
 
 template <typename T>
-static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, cudaStream_t st) {
+static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, void* const* acc, cudaStream_t st) {
   sfb_plan* p = s->plan;
   const Geo<T>& G = geo<T>(p);
   int rc;
@@ -262,7 +266,9 @@ static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, cudaSt
   SFB_LAUNCH_CHECK("project pullback: gradient pullback");
   if ((rc = solve_inplace<T>(s, rb, st))) return rc;
   Box E = ext_box(G);
-  SFB_DISPATCH_DIM(G.dim, D, (k_proj_pb_tail<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, cvp<T>(p, vbar), mvp<T>(p, out), E)));
+  MV<T> O = out ? mvp<T>(p, out) : MV<T>{{nullptr, nullptr, nullptr}};
+  MV<T> Acc = acc ? mvp<T>(p, acc) : MV<T>{{nullptr, nullptr, nullptr}};
+  SFB_DISPATCH_DIM(G.dim, D, (k_proj_pb_tail<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, cvp<T>(p, vbar), O, E, Acc)));
   SFB_LAUNCH_CHECK("project pullback: divergence pullback");
   return SFB_OK;
 }
@@ -359,10 +365,17 @@ int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, doubl
 }
 
 int sfb_project_pullback(sfb_solver* s, void* const* vbar, void* const* out, void* stream) {
-  if (!s || !okp(s->plan, vbar) || !okp(s->plan, out)) return fail(SFB_EINVAL, "null argument");
+  return sfb_project_pullback_ex(s, vbar, out, nullptr, stream);
+}
+
+int sfb_project_pullback_ex(sfb_solver* s, void* const* vbar, void* const* out, void* const* acc, void* stream) {
+  if (!s || !okp(s->plan, vbar)) return fail(SFB_EINVAL, "null argument");
+  if (out && !okp(s->plan, out)) return fail(SFB_EINVAL, "bad out");
+  if (acc && !okp(s->plan, acc)) return fail(SFB_EINVAL, "bad acc");
+  if (!out && !acc) return fail(SFB_EINVAL, "project pullback needs out or acc");
   if (int rc = need_periodic(s->plan)) return rc;
-  return s->plan->dtype == SFB_F64 ? project_pb<double>(s, vbar, out, (cudaStream_t)stream)
-                                   : project_pb<float>(s, vbar, out, (cudaStream_t)stream);
+  return s->plan->dtype == SFB_F64 ? project_pb<double>(s, vbar, out, acc, (cudaStream_t)stream)
+                                   : project_pb<float>(s, vbar, out, acc, (cudaStream_t)stream);
 }
 
 }  // extern "C"

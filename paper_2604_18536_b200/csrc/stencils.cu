@@ -218,7 +218,7 @@ __global__ void k_combine(Geo<T> G, MV<T> Dst, CV<T> Base, KList<T> K, int nk, B
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     if (!is_udof<T, D>(G, I, a)) continue;
-    T v = Base.c[a][x];
+    T v = Base.c[a] ? Base.c[a][x] : T(0);
     for (int l = 0; l < nk; ++l) v += K.k[l][a][x] * K.coef[l];
     Dst.c[a][x] = v;
   }
@@ -454,7 +454,8 @@ int sfb_momentum_rhs(sfb_plan* p, const void* const* u, double nu, const double*
 
 int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, const void* const* k,
                 const double* coef, void* stream) {
-  if (!p || !ptrs_ok(p, dst) || !ptrs_ok(p, base) || nk < 0 || nk > SFB_MAX_K) return fail(SFB_EINVAL, "bad combine args");
+  if (!p || !ptrs_ok(p, dst) || nk < 0 || nk > SFB_MAX_K) return fail(SFB_EINVAL, "bad combine args");
+  if (base && !ptrs_ok(p, base)) return fail(SFB_EINVAL, "bad combine base");
   cudaStream_t st = (cudaStream_t)stream;
   return SFB_TYPED(p, ([&]() {
     const Geo<T>& G = geo<T>(p);
@@ -464,7 +465,8 @@ int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, 
       K.coef[l] = (T)coef[l];
     }
     Box B = int_box(G);
-    SFB_DISPATCH_DIM(G.dim, D, (k_combine<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, mv<T>(p, dst), cv<T>(p, base), K, nk, B)));
+    CV<T> bb = base ? cv<T>(p, base) : CV<T>{{nullptr, nullptr, nullptr}};
+    SFB_DISPATCH_DIM(G.dim, D, (k_combine<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, mv<T>(p, dst), bb, K, nk, B)));
     SFB_LAUNCH_CHECK("combine");
     return (int)SFB_OK;
   })());

@@ -52,10 +52,11 @@ class ScalarField:
 class VelocityField:
     """d staggered components on the GPU (fields.py:33-53)."""
 
-    def __init__(self, grid, components=None):
+    def __init__(self, grid, components=None, empty=False):
         self.grid = grid
         if components is None:
-            self.u = [alloc.zeros(grid.ext_shape, grid.dtype) for _ in range(grid.dim)]
+            mk = alloc.empty if empty else alloc.zeros
+            self.u = [mk(grid.ext_shape, grid.dtype) for _ in range(grid.dim)]
         else:
             self.u = [_as_device(grid, c) for c in components]
 
