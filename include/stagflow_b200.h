@@ -101,7 +101,7 @@ int sfb_momentum_rhs(sfb_plan* plan, const void* const* u, double nu, const doub
 /* RK building blocks (timestep.py:166-214). */
 int sfb_rk_stage(sfb_plan* plan, const sfb_stage_args* args, void* stream);
 /* dst = base + sum_l k[l]*coef[l] on DOFs (acc.copy_from + _axpy chain);
- * base == NULL means zero.  k: flat array of nk*3 component pointers, k[3*l + a]. */
+ * base == NULL (or base[0] == NULL) means zero.  k: flat array of nk*3 component pointers, k[3*l + a]. */
 int sfb_combine(sfb_plan* plan, void* const* dst, const void* const* base, int nk,
                 const void* const* k, const double* coef, void* stream);
 /* Wray3 register update (timestep.py:231-246): fnew *= g; u += fnew; if fold: fold *= z; u += fold. */

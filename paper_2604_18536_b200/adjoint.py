@@ -235,7 +235,7 @@ def _combine_into(grid, dst, terms):
     """dst = sum coef*field on DOFs (no base): one kernel."""
     from .timestep import _combine
 
-    N.call("sfb_combine", _plan(grid), N.ptr3(dst.u), None, len(terms),
+    N.call("sfb_combine", _plan(grid), N.ptr3(dst.u), N.ptr3([None] * 3), len(terms),
            _ks(terms), (N.ctypes.c_double * max(len(terms), 1))(*[c for _, c in terms]), stream_ptr())
     _ = _combine
 

@@ -455,6 +455,7 @@ int sfb_momentum_rhs(sfb_plan* p, const void* const* u, double nu, const double*
 int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, const void* const* k,
                 const double* coef, void* stream) {
   if (!p || !ptrs_ok(p, dst) || nk < 0 || nk > SFB_MAX_K) return fail(SFB_EINVAL, "bad combine args");
+  if (base && !base[0]) base = nullptr;  // all-NULL base: zero
   if (base && !ptrs_ok(p, base)) return fail(SFB_EINVAL, "bad combine base");
   cudaStream_t st = (cudaStream_t)stream;
   return SFB_TYPED(p, ([&]() {
