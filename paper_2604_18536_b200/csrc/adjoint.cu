@@ -8,8 +8,10 @@
 // cotangent / primal values it depends on (reach +-1 per axis, including the
 // (-e_a+e_c) diagonals of the convective pullback) and writes once.  No
 // atomics, so results are deterministic run to run.
-#include "sfb_kernels.cuh"
+#include <cstdlib>
+
 #include "sfb_solver.cuh"
+#include "sfb_stage.cuh"
 
 namespace sfb {
 
@@ -203,6 +205,176 @@ __global__ void __launch_bounds__(256) k_rhs_pb(Geo<T> G, CV<T> Vb, CV<T> U, MV<
   }
 }
 
+// ---------------------------------------------------------------------------
+// rhs pullback, 3D marching form: a CTA owns an 8 x 32 (j, k) tile and walks a
+// chunk of planes; vbar and the primal u (6 components) stream through a
+// 5-slot shared-memory ring whose halo rows / planes are loaded from the
+// periodically wrapped source indices (so no ghost values are read).  Same
+// arithmetic as conv_pb + diff_pb above.
+// ---------------------------------------------------------------------------
+constexpr int kPbTJ = 8, kPbTK = 32, kPbRing = 5;
+constexpr int kPbPW = kPbTK + 2, kPbPH = kPbTJ + 2, kPbPS = kPbPW * kPbPH, kPbNE = 6 * kPbPS;
+constexpr int kPbNT = kPbTJ * kPbTK, kPbNQ = (kPbNE + kPbNT - 1) / kPbNT;
+
+template <typename T, int ACC>
+__global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, CV<T> U, MV<T> O, T nu, int diff,
+                                                            int chunk) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);  // [slot][6][PS]: vbar0..2, u0..2
+  const int tk = threadIdx.x, tj = threadIdx.y, tid = tj * kPbTK + tk;
+  const int k0 = 1 + blockIdx.x * kPbTK, j0 = 1 + blockIdx.y * kPbTJ;
+  const int ib = 1 + blockIdx.z * chunk;
+  const int ie = min(ib + chunk, G.n[0] + 1);
+  const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
+  const long long s0 = G.s[0], s1 = G.s[1];
+  const T* fsrc[kPbNQ];
+  bool fok[kPbNQ];
+#pragma unroll
+  for (int q = 0; q < kPbNQ; ++q) {
+    const int e = tid + q * kPbNT;
+    const int f = e / kPbPS;
+    const int r = e - f * kPbPS;
+    const int jj = r / kPbPW, kk = r - jj * kPbPW;
+    const int gj = wr(j0 - 1 + jj, n1), gk = wr(k0 - 1 + kk, n2);  // periodic wrap of the halo
+    fok[q] = e < kPbNE;
+    const T* base = f < 3 ? Vb.c[f] : U.c[f < 6 ? f - 3 : 0];
+    fsrc[q] = base + (fok[q] ? (long long)gj * s1 + gk : 0);
+  }
+  auto load_plane = [&](int ip, int slot) {
+    if (ip < 0 || ip > n0 + 1) return;
+    const long long base = (long long)wr(ip, n0) * s0;
+    T* dst = ring + slot * kPbNE + tid;
+#pragma unroll
+    for (int q = 0; q < kPbNQ; ++q)
+      if (q < kPbNQ - 1 || tid + q * kPbNT < kPbNE) cp_async_val(dst + q * kPbNT, fsrc[q] + (fok[q] ? base : 0), fok[q]);
+  };
+  const int j = j0 + tj, k = k0 + tk;
+  const bool inside = j <= n1 && k <= n2;
+  // wrapped neighbour indices for the per-axis tables (own_lo at n+1 is not
+  // a periodic image in the reference tables, so always index wrapped)
+  const int jm = wr(j - 1, n1), jp = wr(j + 1, n1), km = wr(k - 1, n2), kp = wr(k + 1, n2);
+
+  int sl_m = (ib - 1) % kPbRing;
+  load_plane(ib - 1, sl_m);
+  load_plane(ib, (sl_m + 1) % kPbRing);
+  load_plane(ib + 1, (sl_m + 2) % kPbRing);
+  cp_commit();
+  load_plane(ib + 2, (sl_m + 3) % kPbRing);
+  cp_commit();
+  const int c0 = (tj + 1) * kPbPW + (tk + 1);
+  long long x = (long long)ib * s0 + (long long)j * s1 + k;
+  for (int i = ib; i < ie; ++i, x += s0) {
+    T accin[3] = {T(0), T(0), T(0)};
+    if (ACC && inside) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) accin[c] = O.c[c][x];
+    }
+    cp_wait<1>();
+    __syncthreads();
+    int sl_l = sl_m + 4;
+    if (sl_l >= kPbRing) sl_l -= kPbRing;
+    load_plane(i + 3, sl_l);
+    cp_commit();
+    int s1i = sl_m + 1, s2i = sl_m + 2;
+    if (s1i >= kPbRing) s1i -= kPbRing;
+    if (s2i >= kPbRing) s2i -= kPbRing;
+    if (inside) {
+      const T* P[3] = {ring + sl_m * kPbNE + c0, ring + s1i * kPbNE + c0, ring + s2i * kPbNE + c0};
+      // field f at offset (d0, d1, d2), f in 0..2 vbar, 3..5 u
+      auto R = [&](int f, int d0, int d1, int d2) -> T { return P[1 + d0][f * kPbPS + d1 * kPbPW + d2]; };
+      const int im = wr(i - 1, n0), ipn = wr(i + 1, n0);
+      const int Jc[3] = {i, j, k}, Jm[3] = {im, jm, km}, Jp[3] = {ipn, jp, kp};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        int ec[3] = {0, 0, 0};
+        ec[c] = 1;
+        T acc = T(0);
+        {  // (i) a = b = c
+          const T l_m = R(c, -ec[0], -ec[1], -ec[2]) * tab(G, c, T_RDU, Jm[c]);
+          const T l_0 = R(c, 0, 0, 0) * tab(G, c, T_RDU, Jc[c]);
+          const T l_p = R(c, ec[0], ec[1], ec[2]) * tab(G, c, T_RDU, Jp[c]);
+          const T u_m = R(3 + c, -ec[0], -ec[1], -ec[2]);
+          const T u_0 = R(3 + c, 0, 0, 0);
+          const T u_p = R(3 + c, ec[0], ec[1], ec[2]);
+          acc += (l_p - l_0) * ((u_0 + u_p) * T(0.5)) + (l_0 - l_m) * ((u_m + u_0) * T(0.5));
+        }
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          if (b == c) continue;
+          int eb[3] = {0, 0, 0};
+          eb[b] = 1;
+          {  // (ii) a = c, b != c
+            const T l_m = R(c, -eb[0], -eb[1], -eb[2]) * tab(G, b, T_RDX, Jm[b]);
+            const T l_0 = R(c, 0, 0, 0) * tab(G, b, T_RDX, Jc[b]);
+            const T l_p = R(c, eb[0], eb[1], eb[2]) * tab(G, b, T_RDX, Jp[b]);
+            const T wl = tab(G, c, T_WLO, Jc[c]), wh = tab(G, c, T_WHI, Jc[c]);
+            const T V0 = wl * R(3 + b, 0, 0, 0) + wh * R(3 + b, ec[0], ec[1], ec[2]);
+            const T Vm = wl * R(3 + b, -eb[0], -eb[1], -eb[2]) + wh * R(3 + b, ec[0] - eb[0], ec[1] - eb[1], ec[2] - eb[2]);
+            acc += T(0.5) * ((l_p - l_0) * V0 + (l_0 - l_m) * Vm);
+          }
+          {  // (iii) transporting component c inside F_ac, a = b
+            const int a = b;
+            const T rc0 = tab(G, c, T_RDX, Jc[c]);
+            const T rcp = tab(G, c, T_RDX, Jp[c]);
+            {
+              const T fb = R(a, ec[0], ec[1], ec[2]) * rcp - R(a, 0, 0, 0) * rc0;
+              const T tt = (R(3 + a, 0, 0, 0) + R(3 + a, ec[0], ec[1], ec[2])) * T(0.5);
+              acc += fb * tt * tab(G, a, T_WLO, Jc[a]);
+            }
+            {
+              const T fb = R(a, ec[0] - eb[0], ec[1] - eb[1], ec[2] - eb[2]) * rcp - R(a, -eb[0], -eb[1], -eb[2]) * rc0;
+              const T tt = (R(3 + a, -eb[0], -eb[1], -eb[2]) + R(3 + a, ec[0] - eb[0], ec[1] - eb[1], ec[2] - eb[2])) * T(0.5);
+              acc += fb * tt * tab(G, a, T_WHI, Jm[a]);
+            }
+          }
+        }
+        if (diff) {
+          T ad = T(0);
+          const T vc = R(c, 0, 0, 0);
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            int eb[3] = {0, 0, 0};
+            eb[b] = 1;
+            const int shi = (b == c) ? T_OHI : T_THI, slo = (b == c) ? T_OLO : T_TLO;
+            const T vm = R(c, -eb[0], -eb[1], -eb[2]);
+            const T vp = R(c, eb[0], eb[1], eb[2]);
+            ad += vm * tab(G, b, shi, Jm[b]) - vc * (tab(G, b, shi, Jc[b]) + tab(G, b, slo, Jc[b])) +
+                  vp * tab(G, b, slo, Jp[b]);
+          }
+          acc += nu * ad;
+        }
+        if (ACC) acc += accin[c];
+        O.c[c][x] = acc;
+      }
+    }
+    sl_m = s1i;
+  }
+  cp_wait<0>();
+}
+
+template <typename T>
+static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int diff, int accumulate, cudaStream_t st) {
+  const size_t smem = (size_t)kPbRing * kPbNE * sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rhs_pb_march<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_rhs_pb_march<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int bx = (G.n[2] + kPbTK - 1) / kPbTK, by = (G.n[1] + kPbTJ - 1) / kPbTJ;
+  const long long bps = (long long)bx * by;
+  long long want = (4LL * 148 * 2 + bps - 1) / bps;
+  int chunk = (int)((G.n[0] + want - 1) / want);
+  if (chunk < 16) chunk = 16;
+  const int bz = (G.n[0] + chunk - 1) / chunk;
+  dim3 grid(bx, by, bz), blk(kPbTK, kPbTJ);
+  if (accumulate) k_rhs_pb_march<T, 1><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk);
+  else k_rhs_pb_march<T, 0><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk);
+  SFB_LAUNCH_CHECK("rhs pullback (march)");
+  if (!accumulate) return launch_planes<T>(G, O, 3, 2, st);  // non-DOF entries of the output are zero
+  return SFB_OK;
+}
+
 // projection pullback tail: out_a = vbar_a + D^T(w * s)  (adjoint.py:335-349)
 template <typename T, int D>
 __global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T> O, Box B, MV<T> Acc) {
@@ -357,6 +529,9 @@ int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, doubl
     const Geo<T>& G = geo<T>(p);
     int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);
     if (rc) return rc;
+    if (G.dim == 3 && !getenv("SFB_PB_GENERIC"))
+      return rhs_pb_march<T>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), mvp<T>(p, out), (T)nu, nu != 0.0,
+                             accumulate, st);
     Box E = ext_box(G);
     SFB_DISPATCH_DIM(G.dim, D, (k_rhs_pb<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), mvp<T>(p, out), E, (T)nu, 1, nu != 0.0, accumulate)));
     SFB_LAUNCH_CHECK("rhs pullback");
