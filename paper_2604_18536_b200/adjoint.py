@@ -211,6 +211,27 @@ def step_forward_tape(u0, dt, tableau, solver, setup):
     s = tableau.stages
     fill_ghosts_velocity(u0, bcs)
     stages = []
+    if tableau.subdiagonal:
+        # the fused stage kernels of rk_step (bitwise the same primal), each
+        # projected stage state kept in its own buffer for the tape
+        from .timestep import _project_quiet
+
+        acc = VelocityField(grid, empty=True)
+        started = False
+        cur = u0
+        for j in range(s):
+            stages.append(cur)
+            nxt = j + 1 < s
+            yn = VelocityField(grid, empty=True) if nxt else None
+            b = tableau.b[j]
+            _stage(setup, cur, u0=u0, s_in=acc if started else None, s_out=acc if b != 0.0 else None,
+                   y_next=yn, cb=dt * b, ca=dt * (tableau.a[j + 1][j] if nxt else 0.0))
+            started = started or b != 0.0
+            if nxt:
+                _project_quiet(yn, solver, bcs)
+                cur = yn
+        project_into(acc, solver, bcs)
+        return acc, (stages, dt, tableau)
     ks = []
     for j in range(s):
         if j == 0:
