@@ -76,6 +76,33 @@ def case_channel(nx=512, ny=256, nz=256):
             "cell_updates_per_s": nx * ny * nz / (ms * 1e-3)}
 
 
+def case_solve(n, dtype):
+    """Spectral Poisson solve alone (5 FFT passes, in place on the solver's
+    contiguous buffer; no copies)."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200 import _native as N
+    from paper_2604_18536_b200 import cases
+
+    g = cases.periodic_box(n, dtype=np.float64 if dtype == "f64" else np.float32)
+    s = P.make_solver("spectral", g, P.BoundarySpec.all_periodic(3))
+    buf = torch.randn(g.shape, dtype=torch.float64 if dtype == "f64" else torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        N.call("sfb_solver_solve", s.handle, buf.data_ptr(), buf.data_ptr(), ctypes.c_void_p(st))
+
+    ms = _time(run, 10, 3)
+    esz = 8 if dtype == "f64" else 4
+    half = n * n * (n // 2 + 1) * 2 * esz
+    gbytes = (2 * (n**3 * esz + half) + 6 * half) / 1e9  # R2C + C2R + 3 strided passes (r+w)
+    return {"case": f"spectral solve {n}^3 {dtype}", "ms": ms, "gb_moved_min": gbytes, "gbs": gbytes / (ms * 1e-3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default="step512,step512f32,step840f32,vjp512,channel")
@@ -87,6 +114,10 @@ def main():
             r = case_step(n, "f32" if f32 else "f64")
         elif c.startswith("vjp"):
             r = case_vjp(int(c[3:]))
+        elif c.startswith("solve"):
+            f32 = c.endswith("f32")
+            n = int(c[5:-3] if f32 else c[5:])
+            r = case_solve(n, "f32" if f32 else "f64")
         elif c == "channel":
             r = case_channel()
         else:

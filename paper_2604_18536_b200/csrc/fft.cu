@@ -18,6 +18,7 @@
 
 #include "sfb_fft.cuh"
 #include "sfb_fft_dev.cuh"
+#include "sfb_fft_reg.cuh"
 #include "sfb_kernels.cuh"
 
 namespace sfb {
@@ -305,6 +306,24 @@ bool fft_factor(int L, FftLen& P) {
   return true;
 }
 
+void fft_reg_assign(FftSolve& F) {
+  RegLen R;
+  F.reg_half = 0;
+  if (reg_factor(F.half.L, R)) {
+    F.reg_half = R.L;
+    F.reg_a_half = R.A;
+    F.reg_b_half = R.B;
+  }
+  for (int a = 0; a < 3; ++a) {
+    F.reg_ax[a] = 0;
+    if (a < F.dim - 1 && reg_factor(F.ax[a].L, R)) {
+      F.reg_ax[a] = R.L;
+      F.reg_a[a] = R.A;
+      F.reg_b[a] = R.B;
+    }
+  }
+}
+
 static int upload(const std::vector<double>& t, bool f64, void** dev) {
   size_t bytes;
   std::vector<float> tf;
@@ -360,11 +379,32 @@ static int pick_w(int L, size_t csz) {
   return W;
 }
 
+static RegLen reg_of(int L, int A, int B) {
+  RegLen R;
+  R.L = L;
+  R.A = A;
+  R.B = B;
+  R.ok = L > 0;
+  return R;
+}
+
 template <typename T, int MODE>
 static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long long S, int ncol, long long bstride,
                           int nbatch, const typename CX<T>::t* tw, const ScaleArgs& sc, cudaStream_t st,
-                          const FftTma* tma = nullptr) {
+                          const FftTma* tma = nullptr, RegLen reg = RegLen{}) {
   typedef typename CX<T>::t C;
+  if (reg.ok) {
+    RegCall c{};
+    c.kind = MODE;
+    c.out = data;
+    c.S = S;
+    c.ncol = ncol;
+    c.bstride = bstride;
+    c.nbatch = nbatch;
+    c.twL = tw;
+    c.sc = sc;
+    return reg_run<T>(reg, c, st);
+  }
   if (tma && tma->ok && !getenv("SFB_NO_TMA")) return fft_tma_pass<T, MODE>(*tma, P, tw, sc, st);
   dim3 grid((ncol + W - 1) / W, nbatch);
   const size_t sm = 2 * (size_t)P.L * W * sizeof(C);
@@ -377,6 +417,52 @@ static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long 
   SFB_LAUNCH_CHECK("fft strided pass");
   return SFB_OK;
 }
+
+template <typename T>
+static int launch_r2c(FftSolve& F, const T* rbuf, typename CX<T>::t* cbuf, long long rows, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  const int nlast = F.n[F.dim - 1], M = nlast / 2, nh = M + 1;
+  if (F.reg_half) {
+    RegCall c{};
+    c.kind = 3;
+    c.in = rbuf;
+    c.out = cbuf;
+    c.rows = rows;
+    c.in_row = nlast;
+    c.out_row = nh;
+    c.twL = F.tw_half;
+    c.twN = F.tw_full;
+    return reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
+  }
+  k_fft_r2c<T><<<(unsigned)rows, 128, 2 * (size_t)M * sizeof(C), st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half,
+                                                                       (const C*)F.tw_full, nlast, nh);
+  SFB_LAUNCH_CHECK("fft r2c");
+  return SFB_OK;
+}
+
+template <typename T>
+static int launch_c2r(FftSolve& F, const typename CX<T>::t* cbuf, T* rbuf, long long rows, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  const int nlast = F.n[F.dim - 1], M = nlast / 2, nh = M + 1;
+  if (F.reg_half) {
+    RegCall c{};
+    c.kind = 4;
+    c.in = cbuf;
+    c.out = rbuf;
+    c.rows = rows;
+    c.in_row = nh;
+    c.out_row = nlast;
+    c.twL = F.tw_half;
+    c.twN = F.tw_full;
+    return reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
+  }
+  k_fft_c2r<T><<<(unsigned)rows, 128, (2 * (size_t)M + 2) * sizeof(C), st>>>(cbuf, rbuf, F.half, (const C*)F.tw_half,
+                                                                             (const C*)F.tw_full, nh, nlast);
+  SFB_LAUNCH_CHECK("fft c2r");
+  return SFB_OK;
+}
+
+#define SFB_REG(F, a) reg_of((F).reg_ax[a], (F).reg_a[a], (F).reg_b[a])
 
 template <typename T>
 int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u) {
@@ -400,9 +486,9 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
                                                                               (const C*)F.tw_full, nh)));
       SFB_LAUNCH_CHECK("fft r2c (fused divergence)");
     } else {
-      k_fft_r2c<T><<<(unsigned)rows, 128, sm, st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nlast,
-                                                    nh);
-      SFB_LAUNCH_CHECK("fft r2c");
+      (void)sm;
+      int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
+      if (rc) return rc;
     }
   }
   ScaleArgs none{};
@@ -411,29 +497,25 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
     // 2. axis 1 forward: S = nh, columns k2 < nh, batch over k0
     int rc;
     if ((rc = launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, csz), nh, nh, (long long)n1 * nh, n0,
-                                   (const C*)F.tw_ax[1], none, st, &F.tma_ax1)))
+                                   (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1))))
       return rc;
     // 3. axis 0 forward + scale + inverse: S = n1*nh, columns (k1,k2)
     if ((rc = launch_strided<T, 2>(cbuf, F.ax[0], pick_w(n0, csz), (long long)n1 * nh, n1 * nh, 0, 1,
-                                   (const C*)F.tw_ax[0], F.sc, st, &F.tma_ax0)))
+                                   (const C*)F.tw_ax[0], F.sc, st, &F.tma_ax0, SFB_REG(F, 0))))
       return rc;
     // 4. axis 1 inverse
     if ((rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, csz), nh, nh, (long long)n1 * nh, n0,
-                                   (const C*)F.tw_ax[1], none, st, &F.tma_ax1)))
+                                   (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1))))
       return rc;
   } else {
     const int n0 = F.n[0];
     int rc;
-    if ((rc = launch_strided<T, 2>(cbuf, F.ax[0], pick_w(n0, csz), nh, nh, 0, 1, (const C*)F.tw_ax[0], F.sc, st)))
+    if ((rc = launch_strided<T, 2>(cbuf, F.ax[0], pick_w(n0, csz), nh, nh, 0, 1, (const C*)F.tw_ax[0], F.sc, st,
+                                   nullptr, SFB_REG(F, 0))))
       return rc;
   }
   // 5. C2R along the contiguous axis
-  {
-    size_t sm = (2 * (size_t)M + 2) * csz;
-    k_fft_c2r<T><<<(unsigned)rows, 128, sm, st>>>(cbuf, rbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nh, nlast);
-    SFB_LAUNCH_CHECK("fft c2r");
-  }
-  return SFB_OK;
+  return launch_c2r<T>(F, cbuf, rbuf, rows, st);
 }
 template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*);
 template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*);
@@ -446,12 +528,12 @@ int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
   C* cbuf = (C*)cbuf_v;
   const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], M = nlast / 2, nh = M + 1;
   const long long rows = (long long)m * n1;
-  k_fft_r2c<T><<<(unsigned)rows, 128, 2 * (size_t)M * sizeof(C), st>>>(rbuf, cbuf, F.half, (const C*)F.tw_half,
-                                                                       (const C*)F.tw_full, nlast, nh);
-  SFB_LAUNCH_CHECK("slab r2c");
+  (void)M;
+  int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
+  if (rc) return rc;
   ScaleArgs none{};
   return launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
-                              (const C*)F.tw_ax[1], none, st, &F.tma_ax1);
+                              (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
 }
 template <typename T>
 int fft_slab_axis0(FftSolve& F, void* tbuf_v, int n1_chunk, cudaStream_t st) {
@@ -459,7 +541,7 @@ int fft_slab_axis0(FftSolve& F, void* tbuf_v, int n1_chunk, cudaStream_t st) {
   const int nh = F.n[2] / 2 + 1;
   const int ncol = n1_chunk * nh;
   return launch_strided<T, 2>((C*)tbuf_v, F.ax[0], pick_w(F.ax[0].L, sizeof(C)), ncol, ncol, 0, 1,
-                              (const C*)F.tw_ax[0], F.sc, st, &F.tma_ax0);
+                              (const C*)F.tw_ax[0], F.sc, st, &F.tma_ax0, SFB_REG(F, 0));
 }
 template <typename T>
 int fft_slab_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st) {
@@ -468,12 +550,10 @@ int fft_slab_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st) {
   const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], M = nlast / 2, nh = M + 1;
   ScaleArgs none{};
   int rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
-                                (const C*)F.tw_ax[1], none, st, &F.tma_ax1);
+                                (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
   if (rc) return rc;
-  k_fft_c2r<T><<<(unsigned)((long long)m * n1), 128, (2 * (size_t)M + 2) * sizeof(C), st>>>(
-      cbuf, rbuf, F.half, (const C*)F.tw_half, (const C*)F.tw_full, nh, nlast);
-  SFB_LAUNCH_CHECK("slab c2r");
-  return SFB_OK;
+  (void)M;
+  return launch_c2r<T>(F, cbuf, rbuf, (long long)m * n1, st);
 }
 template int fft_slab_forward<double>(FftSolve&, double*, void*, cudaStream_t);
 template int fft_slab_forward<float>(FftSolve&, float*, void*, cudaStream_t);
@@ -484,6 +564,7 @@ template int fft_slab_inverse<float>(FftSolve&, void*, float*, cudaStream_t);
 
 template <typename T>
 int fft_set_smem_limits() {
+  if (int rc = fft_reg_init()) return rc;
   const int big = 200 * 1024;
   cudaError_t e = cudaSuccess;
 #define SFB_SMEM(K) \

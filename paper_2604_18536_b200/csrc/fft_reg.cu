@@ -1,0 +1,55 @@
+// Host dispatch of the register-resident FFT engine (sfb_fft_reg.cuh).
+#include <cstdlib>
+
+#include "sfb_fft_reg.cuh"
+
+namespace sfb {
+
+// lengths with an instantiated (A, B) engine (fft_reg_{d,f}{1,2}.cu)
+bool reg_factor(int L, RegLen& R) {
+  static const int tab[][3] = {{840, 28, 30}, {420, 20, 21}, {512, 16, 32}, {256, 16, 16}, {1024, 32, 32},
+                               {16, 4, 4},    {20, 4, 5},    {24, 4, 6},    {32, 4, 8},    {40, 5, 8},
+                               {48, 6, 8},    {64, 8, 8},    {96, 8, 12},   {128, 8, 16},  {192, 12, 16},
+                               {384, 16, 24}};
+  R = RegLen{};
+  if (getenv("SFB_FFT_STOCKHAM")) return false;
+  for (const auto& e : tab)
+    if (e[0] == L) {
+      R.L = L;
+      R.A = e[1];
+      R.B = e[2];
+      R.ok = true;
+      return true;
+    }
+  return false;
+}
+
+int fft_reg_init() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SFB_ECUDA, "cudaGetDevice");
+  static bool done[64] = {};
+  if (dev < 64 && done[dev]) return SFB_OK;
+  if (reg_tu_d1_init() || reg_tu_d2_init() || reg_tu_f1_init() || reg_tu_f2_init())
+    return fail(SFB_ECUDA, "upload of the register-FFT twiddle tables failed");
+  if (dev < 64) done[dev] = true;
+  return SFB_OK;
+}
+
+template <>
+int reg_run<double>(const RegLen& R, const RegCall& c, cudaStream_t st) {
+  int rc = reg_tu_d1(R.L, c, st);
+  if (rc == -1) rc = reg_tu_d2(R.L, c, st);
+  if (rc == -1) return fail(SFB_EINVAL, "register FFT: length not instantiated");
+  if (rc) return cuda_check(cudaGetLastError(), "register FFT launch");
+  return SFB_OK;
+}
+template <>
+int reg_run<float>(const RegLen& R, const RegCall& c, cudaStream_t st) {
+  int rc = reg_tu_f1(R.L, c, st);
+  if (rc == -1) rc = reg_tu_f2(R.L, c, st);
+  if (rc == -1) return fail(SFB_EINVAL, "register FFT: length not instantiated");
+  if (rc) return cuda_check(cudaGetLastError(), "register FFT launch");
+  return SFB_OK;
+}
+
+}  // namespace sfb

@@ -505,6 +505,7 @@ static int setup_fft(sfb_solver* s) {
   F.sc.l2 = s->lam[2];
   F.sc.invN = 1.0 / (double)p->int_count;
   F.sc.zero_ok = 1;
+  fft_reg_assign(F);
   F.enabled = true;
   if (dim == 3 && !getenv("SFB_NO_TMA")) {
     const int n0 = p->n[0], n1 = p->n[1];
@@ -704,6 +705,7 @@ int sfb_slab_solver_create(sfb_plan* p, int n0g, int rank, int nranks, sfb_solve
   F.sc.l2 = s->lam[2];
   F.sc.invN = 1.0 / ((double)n0g * n1 * n2);
   F.sc.zero_ok = rank == 0;
+  fft_reg_assign(F);
   F.enabled = true;
   if (!getenv("SFB_NO_TMA")) {
     if (fft_tma_fits(n1, f64) && (rc = fft_tma_make(F.tma_ax1, s->cbuf, f64, 3, nh, n1, m, n1))) goto bad;

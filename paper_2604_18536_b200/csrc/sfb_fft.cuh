@@ -43,9 +43,14 @@ struct FftSolve {
   void* tw_ax[3] = {nullptr, nullptr, nullptr};
   ScaleArgs sc{};
   FftTma tma_ax1, tma_ax0;  // TMA maps of the axis-1 and axis-0 passes (3D)
+  // register-resident engine (sfb_fft_reg.cuh) per pass, when instantiated
+  int reg_half = 0, reg_ax[3] = {0, 0, 0};  // 0 = Stockham engine, else L
+  int reg_a_half = 0, reg_b_half = 0, reg_a[3] = {0, 0, 0}, reg_b[3] = {0, 0, 0};
 };
 
 bool fft_factor(int L, FftLen& P);
+// choose the register engine for every pass whose length is instantiated
+void fft_reg_assign(FftSolve& F);
 int fft_upload_twiddles(int L, bool f64, void** dev);
 int fft_upload_pass_twiddles(FftLen& P, bool f64, void** dev);
 // Spectral solve in place on rbuf.  When G/u are given, the right-hand side

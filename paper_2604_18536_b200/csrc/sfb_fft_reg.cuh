@@ -1,0 +1,459 @@
+// Register-resident two-level FFT engine (sm_100a) for the spectral solve.
+//
+// A length-L transform with L = A*B (A, B <= 32) is done as one "four-step":
+//   n = B*n1 + n2, k = k1 + A*k2
+//   phase 1: B threads, thread n2 holds x[B*n1 + n2] (n1 < A) in registers,
+//            A-point DFT, twiddle W_L^(n2*k1)
+//   exchange through shared memory (the only one)
+//   phase 2: A threads, thread k1 holds the B values of its k1, B-point DFT,
+//            result X[k1 + A*k2] (natural order) in registers
+// The A- and B-point DFTs are themselves four-steps over the radices
+// 8/7/5/4/3/2 with compile-time indices, so the data never leaves registers
+// inside a phase; twiddles of the sub-DFTs come from the constant bank.
+//
+// Compared with the shared-memory Stockham engine (fft.cu: one smem round trip
+// and one __syncthreads per radix pass) this does one exchange per transform,
+// loads straight from HBM into registers and stores straight back, which is
+// what lets the strided passes run at HBM speed.  The fused
+// forward -> eigenvalue scaling -> inverse pass (axis 0) keeps the spectrum of
+// a column in registers between the forward phase 2 and the inverse phase 1.
+#pragma once
+
+#include "sfb_fft.cuh"
+#include "sfb_fft_dev.cuh"
+
+namespace sfb {
+
+// W_N^j = exp(-2 pi i j / N) for sub-DFT sizes N <= 32 (index N*32 + j).
+// Internal linkage: every translation unit that instantiates kernels owns a
+// copy and uploads it through its reg_tu_*_init() (fft_reg.cu calls them all).
+static __constant__ double2 c_twd[33 * 32];
+static __constant__ float2 c_twf[33 * 32];
+
+template <typename C>
+__device__ __forceinline__ C ctw(int N, int j);
+template <>
+__device__ __forceinline__ double2 ctw<double2>(int N, int j) { return c_twd[N * 32 + j]; }
+template <>
+__device__ __forceinline__ float2 ctw<float2>(int N, int j) { return c_twf[N * 32 + j]; }
+
+__host__ __device__ constexpr bool rdft_base(int N) { return N == 2 || N == 3 || N == 4 || N == 5 || N == 7 || N == 8; }
+
+// factor p of a composite N (base radix closest to sqrt(N), N/p > 1)
+__host__ __device__ constexpr int rdft_pick(int N) {
+  int best = 0, bd = 1 << 30;
+  const int cand[6] = {8, 7, 5, 4, 3, 2};
+  for (int i = 0; i < 6; ++i) {
+    const int p = cand[i];
+    if (N % p == 0 && N / p > 1) {
+      const int q = N / p;
+      const int d = p > q ? p - q : q - p;
+      if (d < bd) {
+        bd = d;
+        best = p;
+      }
+    }
+  }
+  return best;
+}
+
+// x * W_N^j (forward) or x * conj(W_N^j) (INV); j a compile-time constant
+// after unrolling; multiples of N/4 are done exactly.
+template <typename C, int N, bool INV>
+__device__ __forceinline__ C twmul_c(C x, int j) {
+  j %= N;
+  if (j == 0) return x;
+  if ((4 * j) % N == 0) {
+    const int q = 4 * j / N;  // W^(q N/4) = (-i)^q
+    if (q == 2) {
+      x.x = -x.x;
+      x.y = -x.y;
+      return x;
+    }
+    const bool mi = (q == 1) != INV;  // multiply by -i ?
+    C r;
+    if (mi) {
+      r.x = x.y;
+      r.y = -x.x;
+    } else {
+      r.x = -x.y;
+      r.y = x.x;
+    }
+    return r;
+  }
+  C w = ctw<C>(N, j);
+  if (INV) w.y = -w.y;
+  return cmul(x, w);
+}
+
+// In-register DFT of N points (natural order in, natural order out).
+template <typename C, int N, bool INV>
+__device__ __forceinline__ void rdft(C* v) {
+  if constexpr (N == 1) {
+  } else if constexpr (rdft_base(N)) {
+    dft<C, N, INV>(v);
+  } else {
+    constexpr int p = rdft_pick(N), q = N / p;
+    static_assert(p > 1 && p * q == N, "rdft: unsupported length");
+    C t[N];
+#pragma unroll
+    for (int n2 = 0; n2 < q; ++n2) {
+      C a[p];
+#pragma unroll
+      for (int n1 = 0; n1 < p; ++n1) a[n1] = v[q * n1 + n2];
+      rdft<C, p, INV>(a);
+#pragma unroll
+      for (int k1 = 0; k1 < p; ++k1) t[n2 * p + k1] = twmul_c<C, N, INV>(a[k1], n2 * k1);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < p; ++k1) {
+      C b[q];
+#pragma unroll
+      for (int n2 = 0; n2 < q; ++n2) b[n2] = t[n2 * p + k1];
+      rdft<C, q, INV>(b);
+#pragma unroll
+      for (int k2 = 0; k2 < q; ++k2) v[k1 + p * k2] = b[k2];
+    }
+  }
+}
+
+// compile-time tile geometry of an (A, B) engine for element type C
+template <typename C, int A, int B>
+struct RegGeo {
+  static constexpr int L = A * B;
+  static constexpr int TT = A > B ? A : B;  // threads per transform
+  // strided passes: W contiguous columns per CTA (128-B segments), tile <= 112 KB
+#ifndef SFB_REG_SEG
+#define SFB_REG_SEG 64
+#endif
+#ifndef SFB_REG_MINB
+#define SFB_REG_MINB 3
+#endif
+  static constexpr int W0 = (int)(SFB_REG_SEG / sizeof(C));
+  static constexpr int W = (size_t)L * W0 * sizeof(C) <= 112 * 1024 ? W0 : W0 / 2;
+  static constexpr int NT_S = W * TT;
+  static constexpr size_t SMEM_S = (size_t)L * W * sizeof(C);
+  static constexpr int MINB_S = SMEM_S * SFB_REG_MINB <= 220 * 1024 ? SFB_REG_MINB : 1;
+  // row passes: RP rows per CTA; exchange rows padded to an odd stride
+  static constexpr int AP = (A % 2 == 0) ? A + 1 : A;
+  static constexpr int ROWBUF = (B * AP > L + 1 ? B * AP : L + 1);
+  static constexpr int RP = (192 / TT) > 0 ? 192 / TT : 1;
+  static constexpr int NT_R = RP * TT;
+  static constexpr size_t SMEM_R = (size_t)RP * ROWBUF * sizeof(C);
+};
+
+template <typename C>
+__device__ __forceinline__ C czero() {
+  C z;
+  z.x = 0;
+  z.y = 0;
+  return z;
+}
+
+// ---------------------------------------------------------------------------
+// strided C2C pass over columns: element (m, col) at data + b*bstride + m*S + col
+// MODE 0 forward, 1 inverse, 2 forward -> 1/(Lambda N) -> inverse (axis 0)
+// ---------------------------------------------------------------------------
+template <typename T, int A, int B, int MODE>
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<typename CX<T>::t, A, B>::MINB_S)
+    k_rfft_strided(typename CX<T>::t* __restrict__ data, long long S, int ncol, long long bstride,
+                   const typename CX<T>::t* __restrict__ twL, ScaleArgs sc) {
+  typedef typename CX<T>::t C;
+  typedef RegGeo<C, A, B> RG;
+  constexpr int W = RG::W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* buf = reinterpret_cast<C*>(smem_raw);  // [(n2*A + k1)][W]
+  const int w = threadIdx.x % W, t = threadIdx.x / W;
+  const int col = blockIdx.x * W + w;
+  const bool ok = col < ncol;
+  C* base = data + (long long)blockIdx.y * bstride + (ok ? col : 0);
+  constexpr bool INV1 = MODE == 1;
+  // phase 1: thread n2 = t
+  if (t < B) {
+    const int n2 = t;
+    C v[A];
+    const C* g = base + (long long)n2 * S;
+    const long long gs = (long long)B * S;
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(g + n1 * gs) : czero<C>();
+    rdft<C, A, INV1>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) {
+      C x = v[k1];
+      if (k1 > 0) {
+        C tw = __ldg(twL + n2 * k1);
+        if (INV1) tw.y = -tw.y;
+        x = cmul(x, tw);
+      }
+      buf[(n2 * A + k1) * W + w] = x;
+    }
+  }
+  __syncthreads();
+  if (t < A) {
+    const int k1 = t;
+    C v[B];
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) v[n2] = buf[(n2 * A + k1) * W + w];
+    rdft<C, B, INV1>(v);
+    if constexpr (MODE == 2) {
+      // eigenvalue scaling (poisson.py:179-199): lam in fp64, cast to T
+      double lc = 0.0, l2v = 0.0;
+      if (sc.dim == 3) {
+        const int c1 = col / sc.nh, c2 = col - c1 * sc.nh;
+        lc = ok ? sc.l1[c1] : 0.0;
+        l2v = ok ? sc.l2[c2] : 0.0;
+      } else {
+        lc = ok ? sc.l1[col] : 0.0;
+      }
+      const bool zmode = col == 0 && blockIdx.y == 0 && sc.zero_ok;
+#pragma unroll
+      for (int k2 = 0; k2 < B; ++k2) {
+        const int m = k1 + A * k2;
+        const double lam = sc.dim == 3 ? (sc.l0[m] + lc) + l2v : sc.l0[m] + lc;
+        if (m == 0 && zmode) {
+          v[k2] = czero<C>();
+        } else {
+          const T f = T(1) / (T)lam * (T)sc.invN;
+          v[k2].x *= f;
+          v[k2].y *= f;
+        }
+      }
+      // inverse: B-point inverse DFT over k2 in registers, conj twiddle,
+      // back into the same smem slots this thread read
+      rdft<C, B, true>(v);
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) {
+        C x = v[n2];
+        if (k1 > 0) {
+          C tw = __ldg(twL + n2 * k1);
+          tw.y = -tw.y;
+          x = cmul(x, tw);
+        }
+        buf[(n2 * A + k1) * W + w] = x;
+      }
+    } else {
+      if (ok) {
+#pragma unroll
+        for (int k2 = 0; k2 < B; ++k2) __stcs(base + (long long)(k1 + A * k2) * S, v[k2]);
+      }
+    }
+  }
+  if constexpr (MODE == 2) {
+    __syncthreads();
+    if (t < B) {
+      const int n2 = t;
+      C v[A];
+#pragma unroll
+      for (int k1 = 0; k1 < A; ++k1) v[k1] = buf[(n2 * A + k1) * W + w];
+      rdft<C, A, true>(v);
+      if (ok) {
+        C* g = base + (long long)n2 * S;
+        const long long gs = (long long)B * S;
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) __stcs(g + n1 * gs, v[n1]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// contiguous-axis real transforms, M = A*B complex points per row (N = 2M reals)
+// ---------------------------------------------------------------------------
+template <typename T, int A, int B>
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
+    k_rfft_r2c(const T* __restrict__ in, typename CX<T>::t* __restrict__ out, long long rows, long long in_row,
+               long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
+  typedef typename CX<T>::t C;
+  typedef RegGeo<C, A, B> RG;
+  constexpr int M = A * B, TT = RG::TT, AP = RG::AP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int r = threadIdx.x / TT, t = threadIdx.x % TT;
+  const long long row = (long long)blockIdx.x * RG::RP + r;
+  const bool okr = row < rows;
+  C* buf = reinterpret_cast<C*>(smem_raw) + r * RG::ROWBUF;
+  if (t < B) {
+    const int n2 = t;
+    const C* x = reinterpret_cast<const C*>(in + (okr ? row : 0) * in_row);
+    C v[A];
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) v[n1] = okr ? __ldcs(x + B * n1 + n2) : czero<C>();
+    rdft<C, A, false>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) {
+      C y = v[k1];
+      if (k1 > 0) y = cmul(y, __ldg(twM + n2 * k1));
+      buf[n2 * AP + k1] = y;
+    }
+  }
+  __syncthreads();
+  C v[B];
+  if (t < A) {
+    const int k1 = t;
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) v[n2] = buf[n2 * AP + k1];
+    rdft<C, B, false>(v);
+  }
+  __syncthreads();
+  if (t < A) {
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) buf[t + A * k2] = v[k2];
+  }
+  __syncthreads();
+  if (!okr) return;
+  C* o = out + row * out_row;
+  // X[k] = E[k] + w^k O[k],  E = (Z[k] + conj Z[M-k]) / 2,  O = (Z[k] - conj Z[M-k]) / (2i)
+  for (int k = t; k <= M; k += TT) {
+    const C zk = buf[k == M ? 0 : k];
+    const C zc = buf[k == 0 ? 0 : M - k];
+    C e, od;
+    e.x = T(0.5) * (zk.x + zc.x);
+    e.y = T(0.5) * (zk.y - zc.y);
+    od.x = T(0.5) * (zk.y + zc.y);
+    od.y = -T(0.5) * (zk.x - zc.x);
+    const C w = __ldg(twN + k);
+    __stcs(o + k, cadd(e, cmul(w, od)));
+  }
+}
+
+template <typename T, int A, int B>
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
+    k_rfft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, long long rows, long long in_row,
+               long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
+  typedef typename CX<T>::t C;
+  typedef RegGeo<C, A, B> RG;
+  constexpr int M = A * B, TT = RG::TT, AP = RG::AP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int r = threadIdx.x / TT, t = threadIdx.x % TT;
+  const long long row = (long long)blockIdx.x * RG::RP + r;
+  const bool okr = row < rows;
+  C* buf = reinterpret_cast<C*>(smem_raw) + r * RG::ROWBUF;
+  if (t < B) {
+    const int n2 = t;
+    const C* X = in + (okr ? row : 0) * in_row;
+    C v[A];
+    // Z[k] = (X[k] + conj X[M-k]) + i (X[k] - conj X[M-k]) exp(+2 pi i k / N)
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) {
+      const int k = B * n1 + n2;
+      C z = czero<C>();
+      if (okr) {
+        const C xk = X[k];
+        const C xc = X[M - k];
+        C fe, d, w;
+        fe.x = xk.x + xc.x;
+        fe.y = xk.y - xc.y;
+        d.x = xk.x - xc.x;
+        d.y = xk.y + xc.y;
+        w = __ldg(twN + k);
+        w.y = -w.y;
+        const C fo = cmul(d, w);
+        z.x = fe.x - fo.y;
+        z.y = fe.y + fo.x;
+      }
+      v[n1] = z;
+    }
+    rdft<C, A, true>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) {
+      C y = v[k1];
+      if (k1 > 0) {
+        C tw = __ldg(twM + n2 * k1);
+        tw.y = -tw.y;
+        y = cmul(y, tw);
+      }
+      buf[n2 * AP + k1] = y;
+    }
+  }
+  __syncthreads();
+  if (t < A && okr) {
+    const int k1 = t;
+    C v[B];
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) v[n2] = buf[n2 * AP + k1];
+    rdft<C, B, true>(v);
+    C* o = reinterpret_cast<C*>(out + row * out_row);
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) __stcs(o + k1 + A * k2, v[k2]);
+  }
+}
+
+// ---- host side ----
+struct RegLen {
+  int L = 0, A = 0, B = 0;
+  bool ok = false;
+};
+// one launch request: kind 0/1/2 strided MODE, 3 R2C, 4 C2R
+struct RegCall {
+  int kind;
+  const void* in;
+  void* out;  // strided: in == out (in place)
+  long long S, bstride, rows, in_row, out_row;
+  int ncol, nbatch;
+  const void* twL;  // plain table exp(-2 pi i m / L), m < L
+  const void* twN;  // real trick: exp(-2 pi i k / 2L), k <= L
+  ScaleArgs sc;
+};
+
+static int reg_upload_tables() {
+  static double2 hd[33 * 32];
+  static float2 hf[33 * 32];
+  for (int N = 1; N <= 32; ++N)
+    for (int j = 0; j < 32; ++j) {
+      const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)(j % N) / (long double)N;
+      hd[N * 32 + j] = make_double2((double)cosl(a), (double)sinl(a));
+      hf[N * 32 + j] = make_float2((float)cosl(a), (float)sinl(a));
+    }
+  if (cudaMemcpyToSymbol(c_twd, hd, sizeof(hd)) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(c_twf, hf, sizeof(hf)) != cudaSuccess) return -1;
+  return 0;
+}
+
+template <typename T, int A, int B>
+static int reg_launch(const RegCall& c, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  typedef RegGeo<C, A, B> RG;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
+    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
+    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
+    cudaFuncSetAttribute(k_rfft_r2c<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
+    cudaFuncSetAttribute(k_rfft_c2r<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
+    attr = true;
+  }
+  if (c.kind <= 2) {
+    dim3 grid((c.ncol + RG::W - 1) / RG::W, c.nbatch);
+    C* d = (C*)c.out;
+    const C* tw = (const C*)c.twL;
+    if (c.kind == 0) k_rfft_strided<T, A, B, 0><<<grid, RG::NT_S, RG::SMEM_S, st>>>(d, c.S, c.ncol, c.bstride, tw, c.sc);
+    else if (c.kind == 1)
+      k_rfft_strided<T, A, B, 1><<<grid, RG::NT_S, RG::SMEM_S, st>>>(d, c.S, c.ncol, c.bstride, tw, c.sc);
+    else k_rfft_strided<T, A, B, 2><<<grid, RG::NT_S, RG::SMEM_S, st>>>(d, c.S, c.ncol, c.bstride, tw, c.sc);
+  } else {
+    const unsigned nb = (unsigned)((c.rows + RG::RP - 1) / RG::RP);
+    if (c.kind == 3)
+      k_rfft_r2c<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>((const T*)c.in, (C*)c.out, c.rows, c.in_row, c.out_row,
+                                                          (const C*)c.twL, (const C*)c.twN);
+    else
+      k_rfft_c2r<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>((const C*)c.in, (T*)c.out, c.rows, c.in_row, c.out_row,
+                                                          (const C*)c.twL, (const C*)c.twN);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// dispatch (fft_reg.cu); the per-unit entry points return -1 when the length
+// is not instantiated in that unit
+bool reg_factor(int L, RegLen& R);
+int fft_reg_init();
+template <typename T>
+int reg_run(const RegLen& R, const RegCall& c, cudaStream_t st);
+int reg_tu_d1(int L, const RegCall& c, cudaStream_t st);
+int reg_tu_d2(int L, const RegCall& c, cudaStream_t st);
+int reg_tu_f1(int L, const RegCall& c, cudaStream_t st);
+int reg_tu_f2(int L, const RegCall& c, cudaStream_t st);
+int reg_tu_d1_init();
+int reg_tu_d2_init();
+int reg_tu_f1_init();
+int reg_tu_f2_init();
+
+}  // namespace sfb
