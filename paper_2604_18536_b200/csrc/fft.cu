@@ -462,6 +462,15 @@ static int launch_c2r(FftSolve& F, const typename CX<T>::t* cbuf, T* rbuf, long 
   return SFB_OK;
 }
 
+template <typename T>
+bool fft_divfuse_ok(const FftSolve& F, const Geo<T>& G) {
+  if (getenv("SFB_NO_DIVFUSE")) return false;
+  return F.reg_half && G.dim == 3 && F.dim == 3 && G.per[1] && !G.halo[1] && G.per[2] && !G.halo[2] &&
+         (G.per[0] || G.halo[0]) && F.n[0] == G.n[0] && F.n[1] == G.n[1] && F.n[2] == G.n[2];
+}
+template bool fft_divfuse_ok<double>(const FftSolve&, const Geo<double>&);
+template bool fft_divfuse_ok<float>(const FftSolve&, const Geo<float>&);
+
 #define SFB_REG(F, a) reg_of((F).reg_ax[a], (F).reg_a[a], (F).reg_b[a])
 
 template <typename T>
@@ -474,22 +483,31 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
   const int M = nlast / 2;
   const int nh = M + 1;
   const long long rows = F.total / nlast;
-  // 1. R2C along the contiguous axis
-  {
+  // 1. R2C along the contiguous axis (optionally of the divergence of u)
+  if (G && fft_divfuse_ok(F, *G)) {
+    RegCall c{};
+    c.kind = 5;
+    c.out = cbuf;
+    c.rows = rows;
+    c.out_row = nh;
+    c.twL = F.tw_half;
+    c.twN = F.tw_full;
+    c.geo = G;
+    for (int a = 0; a < 3; ++a) c.u[a] = u[a];
+    int rc = reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
+    if (rc) return rc;
+  } else if (G) {
     size_t sm = 2 * (size_t)M * csz;
-    if (G) {
-      CV<T> U;
-      for (int a = 0; a < 3; ++a) U.c[a] = a < dim ? (const T*)u[a] : nullptr;
-      const size_t smd = sm + (size_t)(2 * dim - 1) * nlast * sizeof(T);
-      SFB_DISPATCH_DIM(dim, D,
-                       (k_fft_r2c_div<T, D><<<(unsigned)rows, 128, smd, st>>>(*G, U, cbuf, F.half, (const C*)F.tw_half,
-                                                                              (const C*)F.tw_full, nh)));
-      SFB_LAUNCH_CHECK("fft r2c (fused divergence)");
-    } else {
-      (void)sm;
-      int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
-      if (rc) return rc;
-    }
+    CV<T> U;
+    for (int a = 0; a < 3; ++a) U.c[a] = a < dim ? (const T*)u[a] : nullptr;
+    const size_t smd = sm + (size_t)(2 * dim - 1) * nlast * sizeof(T);
+    SFB_DISPATCH_DIM(dim, D,
+                     (k_fft_r2c_div<T, D><<<(unsigned)rows, 128, smd, st>>>(*G, U, cbuf, F.half, (const C*)F.tw_half,
+                                                                            (const C*)F.tw_full, nh)));
+    SFB_LAUNCH_CHECK("fft r2c (fused divergence)");
+  } else {
+    int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
+    if (rc) return rc;
   }
   ScaleArgs none{};
   if (dim == 3) {

@@ -112,8 +112,12 @@ __global__ void __launch_bounds__(NT, 1) k_fft_tma(const __grid_constant__ CUten
     mbar_wait(&bars[cur], phase[cur]);
     phase[cur] ^= 1;
     C* res;
+#ifdef SFB_TMA_NOCOMPUTE
+    res = buf[cur];
+#else
     if (MODE == 1) res = run_fft<C, true, W, true>(buf[cur], buf[tmp], P, stw);
     else res = run_fft<C, false, W, true>(buf[cur], buf[tmp], P, stw);
+#endif
     const int bx = t % ntx, by = t / ntx;
     const int c0 = bx * W;
     if (MODE == 2) {
@@ -143,8 +147,10 @@ __global__ void __launch_bounds__(NT, 1) k_fft_tma(const __grid_constant__ CUten
           res[m * W + w] = v;
         }
       }
+#ifndef SFB_TMA_NOCOMPUTE
       C* other = (res == buf[cur]) ? buf[tmp] : buf[cur];
       res = run_fft<C, true, W, true>(res, other, P, stw);
+#endif
     }
     // results of this tile -> HBM by TMA; smem writes must be visible to the async proxy
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -454,7 +454,7 @@ static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) 
   T* rb = (T*)s->rbuf;
   Box B = int_box(G);
   int rc;
-  if (s->fft.enabled && getenv("SFB_DIVFUSE")) {
+  if (s->fft.enabled && (fft_divfuse_ok<T>(s->fft, G) || getenv("SFB_DIVFUSE"))) {
     // divergence fused into the first FFT pass
     if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, (const void* const*)u))) return rc;
   } else {

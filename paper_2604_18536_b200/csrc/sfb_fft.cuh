@@ -60,6 +60,9 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const G
                       const void* const* u = nullptr);
 template <typename T>
 int fft_set_smem_limits();
+// the register engine can fuse the divergence of u into the R2C pass
+template <typename T>
+bool fft_divfuse_ok(const FftSolve& F, const Geo<T>& G);
 bool fft_tma_fits(int L, bool f64);
 int fft_tma_make(FftTma& M, void* base, bool f64, int rank, long long inner_complex, long long rows, long long batch,
                  int L);

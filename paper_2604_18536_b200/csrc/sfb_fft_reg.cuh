@@ -21,6 +21,9 @@
 
 #include "sfb_fft.cuh"
 #include "sfb_fft_dev.cuh"
+#include "sfb_kernels.cuh"
+
+#include <cstdlib>
 
 namespace sfb {
 
@@ -89,6 +92,9 @@ __device__ __forceinline__ C twmul_c(C x, int j) {
 // In-register DFT of N points (natural order in, natural order out).
 template <typename C, int N, bool INV>
 __device__ __forceinline__ void rdft(C* v) {
+#ifdef SFB_REG_NOCOMPUTE
+  if (true) return;
+#endif
   if constexpr (N == 1) {
   } else if constexpr (rdft_base(N)) {
     dft<C, N, INV>(v);
@@ -122,17 +128,19 @@ template <typename C, int A, int B>
 struct RegGeo {
   static constexpr int L = A * B;
   static constexpr int TT = A > B ? A : B;  // threads per transform
-  // strided passes: W contiguous columns per CTA (128-B segments), tile <= 112 KB
+  // strided passes: W contiguous columns per CTA (SFB_REG_SEG-byte segments)
 #ifndef SFB_REG_SEG
 #define SFB_REG_SEG 64
 #endif
 #ifndef SFB_REG_MINB
 #define SFB_REG_MINB 3
 #endif
+  static constexpr int E = (int)(128 / sizeof(C));  // elements per 128-byte wavefront
   static constexpr int W0 = (int)(SFB_REG_SEG / sizeof(C));
   static constexpr int W = (size_t)L * W0 * sizeof(C) <= 112 * 1024 ? W0 : W0 / 2;
+  static constexpr int XS = A * W + (W < E ? ((W - (A * W) % E) % E + E) % E : 0);
   static constexpr int NT_S = W * TT;
-  static constexpr size_t SMEM_S = (size_t)L * W * sizeof(C);
+  static constexpr size_t SMEM_S = ((size_t)B * XS + 32 + (L + 31) / 32) * sizeof(C);
   static constexpr int MINB_S = SMEM_S * SFB_REG_MINB <= 220 * 1024 ? SFB_REG_MINB : 1;
   // row passes: RP rows per CTA; exchange rows padded to an odd stride
   static constexpr int AP = (A % 2 == 0) ? A + 1 : A;
@@ -150,9 +158,28 @@ __device__ __forceinline__ C czero() {
   return z;
 }
 
+// Two-level twiddle W_L^m = hi[m >> 5] * lo[m & 31] from shared memory (m < L):
+// 1 KB instead of an L-entry table, so the tile keeps the SM's smem.
+template <typename C>
+__device__ __forceinline__ void tw_fill(C* lo, C* hi, const C* __restrict__ twL, int L) {
+  const int nhi = (L + 31) / 32;
+  for (int j = threadIdx.x; j < 32 + nhi; j += blockDim.x) {
+    if (j < 32) lo[j] = __ldg(twL + (j < L ? j : 0));
+    else hi[j - 32] = __ldg(twL + 32 * (j - 32));
+  }
+}
+template <typename C, bool INV>
+__device__ __forceinline__ C tw_mul(C x, const C* lo, const C* hi, int m) {
+  C w = cmul(hi[m >> 5], lo[m & 31]);
+  if (INV) w.y = -w.y;
+  return cmul(x, w);
+}
+
 // ---------------------------------------------------------------------------
 // strided C2C pass over columns: element (m, col) at data + b*bstride + m*S + col
 // MODE 0 forward, 1 inverse, 2 forward -> 1/(Lambda N) -> inverse (axis 0)
+// Exchange layout: slot (n2, k1, w) at n2*XS + k1*W + w, XS padded so the
+// rows of one 128-byte shared-memory wavefront fall in distinct banks.
 // ---------------------------------------------------------------------------
 template <typename T, int A, int B, int MODE>
 __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<typename CX<T>::t, A, B>::MINB_S)
@@ -160,40 +187,46 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<
                    const typename CX<T>::t* __restrict__ twL, ScaleArgs sc) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
-  constexpr int W = RG::W;
+  constexpr int W = RG::W, XS = RG::XS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* buf = reinterpret_cast<C*>(smem_raw);  // [(n2*A + k1)][W]
+  C* buf = reinterpret_cast<C*>(smem_raw);
+  C* twlo = buf + B * XS;
+  C* twhi = twlo + 32;
   const int w = threadIdx.x % W, t = threadIdx.x / W;
   const int col = blockIdx.x * W + w;
   const bool ok = col < ncol;
   C* base = data + (long long)blockIdx.y * bstride + (ok ? col : 0);
   constexpr bool INV1 = MODE == 1;
-  // phase 1: thread n2 = t
+  const long long gs = (long long)B * S;
+  C v[A > B ? A : B];
+  // phase 1: thread n2 = t loads its column straight into registers
   if (t < B) {
-    const int n2 = t;
-    C v[A];
-    const C* g = base + (long long)n2 * S;
-    const long long gs = (long long)B * S;
+    const C* g = base + (long long)t * S;
 #pragma unroll
     for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(g + n1 * gs) : czero<C>();
+  }
+  tw_fill(twlo, twhi, twL, A * B);
+  __syncthreads();
+  if (t < B) {
+    const int n2 = t;
     rdft<C, A, INV1>(v);
 #pragma unroll
     for (int k1 = 0; k1 < A; ++k1) {
       C x = v[k1];
-      if (k1 > 0) {
-        C tw = __ldg(twL + n2 * k1);
-        if (INV1) tw.y = -tw.y;
-        x = cmul(x, tw);
-      }
-      buf[(n2 * A + k1) * W + w] = x;
+      if (k1 > 0) x = tw_mul<C, INV1>(x, twlo, twhi, n2 * k1);
+      buf[n2 * XS + k1 * W + w] = x;
     }
   }
   __syncthreads();
   if (t < A) {
     const int k1 = t;
-    C v[B];
+    double l0v[MODE == 2 ? B : 1];
+    if constexpr (MODE == 2) {
 #pragma unroll
-    for (int n2 = 0; n2 < B; ++n2) v[n2] = buf[(n2 * A + k1) * W + w];
+      for (int k2 = 0; k2 < B; ++k2) l0v[k2] = __ldg(sc.l0 + k1 + A * k2);
+    }
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) v[n2] = buf[n2 * XS + k1 * W + w];
     rdft<C, B, INV1>(v);
     if constexpr (MODE == 2) {
       // eigenvalue scaling (poisson.py:179-199): lam in fp64, cast to T
@@ -209,7 +242,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<
 #pragma unroll
       for (int k2 = 0; k2 < B; ++k2) {
         const int m = k1 + A * k2;
-        const double lam = sc.dim == 3 ? (sc.l0[m] + lc) + l2v : sc.l0[m] + lc;
+        const double lam = sc.dim == 3 ? (l0v[k2] + lc) + l2v : l0v[k2] + lc;
         if (m == 0 && zmode) {
           v[k2] = czero<C>();
         } else {
@@ -224,31 +257,23 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<
 #pragma unroll
       for (int n2 = 0; n2 < B; ++n2) {
         C x = v[n2];
-        if (k1 > 0) {
-          C tw = __ldg(twL + n2 * k1);
-          tw.y = -tw.y;
-          x = cmul(x, tw);
-        }
-        buf[(n2 * A + k1) * W + w] = x;
+        if (k1 > 0) x = tw_mul<C, true>(x, twlo, twhi, n2 * k1);
+        buf[n2 * XS + k1 * W + w] = x;
       }
-    } else {
-      if (ok) {
+    } else if (ok) {
 #pragma unroll
-        for (int k2 = 0; k2 < B; ++k2) __stcs(base + (long long)(k1 + A * k2) * S, v[k2]);
-      }
+      for (int k2 = 0; k2 < B; ++k2) __stcs(base + (long long)(k1 + A * k2) * S, v[k2]);
     }
   }
   if constexpr (MODE == 2) {
     __syncthreads();
     if (t < B) {
       const int n2 = t;
-      C v[A];
 #pragma unroll
-      for (int k1 = 0; k1 < A; ++k1) v[k1] = buf[(n2 * A + k1) * W + w];
+      for (int k1 = 0; k1 < A; ++k1) v[k1] = buf[n2 * XS + k1 * W + w];
       rdft<C, A, true>(v);
       if (ok) {
         C* g = base + (long long)n2 * S;
-        const long long gs = (long long)B * S;
 #pragma unroll
         for (int n1 = 0; n1 < A; ++n1) __stcs(g + n1 * gs, v[n1]);
       }
@@ -302,6 +327,91 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
   if (!okr) return;
   C* o = out + row * out_row;
   // X[k] = E[k] + w^k O[k],  E = (Z[k] + conj Z[M-k]) / 2,  O = (Z[k] - conj Z[M-k]) / (2i)
+  for (int k = t; k <= M; k += TT) {
+    const C zk = buf[k == M ? 0 : k];
+    const C zc = buf[k == 0 ? 0 : M - k];
+    C e, od;
+    e.x = T(0.5) * (zk.x + zc.x);
+    e.y = T(0.5) * (zk.y - zc.y);
+    od.x = T(0.5) * (zk.y + zc.y);
+    od.y = -T(0.5) * (zk.x - zc.x);
+    const C w = __ldg(twN + k);
+    __stcs(o + k, cadd(e, cmul(w, od)));
+  }
+}
+
+// R2C of the projection right-hand side computed on the fly: the real input
+// at interior cell (i, j, k) is the divergence of the velocity
+// (operators.py:108-122, same operation order as k_div_int), read from the
+// extended velocity arrays; the divergence field never touches HBM.
+// Axes 1 and 2 periodic, axis 0 periodic or a halo axis (slab).
+template <typename T>
+__device__ __forceinline__ T div_at(const Geo<T>& G, const T* __restrict__ u0, const T* __restrict__ u1,
+                                    const T* __restrict__ u2, long long x, long long o0m, long long o1m, T r0, T r1,
+                                    int kk) {
+  const long long xk = x + kk;
+  const long long o2m = kk == 1 ? (long long)(G.n[2] - 1) : -1;
+  T acc = (__ldg(u0 + xk) - __ldg(u0 + xk + o0m)) * r0;
+  acc += (__ldg(u1 + xk) - __ldg(u1 + xk + o1m)) * r1;
+  acc += (__ldg(u2 + xk) - __ldg(u2 + xk + o2m)) * tab(G, 2, T_RDX, kk);
+  return acc;
+}
+
+template <typename T, int A, int B>
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
+    k_rfft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, long long rows, long long out_row,
+                   const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
+  typedef typename CX<T>::t C;
+  typedef RegGeo<C, A, B> RG;
+  constexpr int M = A * B, TT = RG::TT, AP = RG::AP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int r = threadIdx.x / TT, t = threadIdx.x % TT;
+  const long long row = (long long)blockIdx.x * RG::RP + r;
+  const bool okr = row < rows;
+  C* buf = reinterpret_cast<C*>(smem_raw) + r * RG::ROWBUF;
+  if (t < B) {
+    const int n2 = t;
+    C v[A];
+    if (okr) {
+      const int i = 1 + (int)(row / G.n[1]), j = 1 + (int)(row % G.n[1]);
+      const long long x = (long long)i * G.s[0] + (long long)j * G.s[1];
+      const long long o0m = (i == 1 && !G.halo[0]) ? (long long)(G.n[0] - 1) * G.s[0] : -G.s[0];
+      const long long o1m = j == 1 ? (long long)(G.n[1] - 1) * G.s[1] : -G.s[1];
+      const T r0 = tab(G, 0, T_RDX, i), r1 = tab(G, 1, T_RDX, j);
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) {
+        const int m = B * n1 + n2;
+        v[n1].x = div_at(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 1);
+        v[n1].y = div_at(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 2);
+      }
+    } else {
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) v[n1] = czero<C>();
+    }
+    rdft<C, A, false>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) {
+      C y = v[k1];
+      if (k1 > 0) y = cmul(y, __ldg(twM + n2 * k1));
+      buf[n2 * AP + k1] = y;
+    }
+  }
+  __syncthreads();
+  C v[B];
+  if (t < A) {
+    const int k1 = t;
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) v[n2] = buf[n2 * AP + k1];
+    rdft<C, B, false>(v);
+  }
+  __syncthreads();
+  if (t < A) {
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) buf[t + A * k2] = v[k2];
+  }
+  __syncthreads();
+  if (!okr) return;
+  C* o = out + row * out_row;
   for (int k = t; k <= M; k += TT) {
     const C zk = buf[k == M ? 0 : k];
     const C zc = buf[k == 0 ? 0 : M - k];
@@ -382,7 +492,7 @@ struct RegLen {
   int L = 0, A = 0, B = 0;
   bool ok = false;
 };
-// one launch request: kind 0/1/2 strided MODE, 3 R2C, 4 C2R
+// one launch request: kind 0/1/2 strided MODE, 3 R2C, 4 C2R, 5 R2C of the divergence
 struct RegCall {
   int kind;
   const void* in;
@@ -392,6 +502,8 @@ struct RegCall {
   const void* twL;  // plain table exp(-2 pi i m / L), m < L
   const void* twN;  // real trick: exp(-2 pi i k / 2L), k <= L
   ScaleArgs sc;
+  const void* geo;     // kind 5: host Geo<T> of the velocity plan
+  const void* u[3];    // kind 5: extended velocity components
 };
 
 static int reg_upload_tables() {
@@ -419,6 +531,7 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
     cudaFuncSetAttribute(k_rfft_r2c<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
     cudaFuncSetAttribute(k_rfft_c2r<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
+    cudaFuncSetAttribute(k_rfft_r2c_div<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
     attr = true;
   }
   if (c.kind <= 2) {
@@ -434,9 +547,15 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     if (c.kind == 3)
       k_rfft_r2c<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>((const T*)c.in, (C*)c.out, c.rows, c.in_row, c.out_row,
                                                           (const C*)c.twL, (const C*)c.twN);
-    else
+    else if (c.kind == 4)
       k_rfft_c2r<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>((const C*)c.in, (T*)c.out, c.rows, c.in_row, c.out_row,
                                                           (const C*)c.twL, (const C*)c.twN);
+    else {
+      CV<T> U;
+      for (int a = 0; a < 3; ++a) U.c[a] = (const T*)c.u[a];
+      k_rfft_r2c_div<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>(*(const Geo<T>*)c.geo, U, (C*)c.out, c.rows, c.out_row,
+                                                              (const C*)c.twL, (const C*)c.twN);
+    }
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
