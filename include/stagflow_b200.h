@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SFB_ABI_VERSION 1
+#define SFB_ABI_VERSION 2
 
 enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4 };
 enum { SFB_F64 = 0, SFB_F32 = 1 };
@@ -77,6 +77,11 @@ typedef struct sfb_stage_args {
   void* k_out[3];
   double cb, ca, nu;
   double force[3];
+  /* Optional (NULL = off): contiguous interior pressure (n0*n1*n2) of the
+   * projection of y (poisson.py:333-339 fused into the stage): the kernel
+   * forms y - G p on the fly, so the gradient-subtract pass and the ghost fill
+   * of y are skipped.  All-periodic 3D plans only. */
+  const void* p_int;
 } sfb_stage_args;
 
 int sfb_abi_version(void);
@@ -129,6 +134,13 @@ int sfb_solver_uses_own_fft(const sfb_solver* s);
 int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream);
 /* Full projection of u in place; p_ext (extended, ghosts filled) optional. */
 int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream);
+/* First half of the projection (poisson.py:321-333: divergence -> solve) without
+ * the gradient subtract: *p_int receives the solver-owned contiguous interior
+ * pressure, valid until the solver's next use.  Feed it to the next
+ * sfb_rk_stage (sfb_stage_args.p_int), which applies u - G p on the fly. */
+int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, void* stream);
+/* Number of kernels (ours) one sfb_project launches (bench bookkeeping). */
+int sfb_project_launches(const sfb_solver* s, int with_pressure);
 
 /* Slab-decomposed spectral solve (multi-GPU, axis 0 split over nranks; the
  * plan's axis 0 is SFB_BC_HALO).  One projection =

@@ -17,7 +17,7 @@ SFB_F64, SFB_F32 = 0, 1
 SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC, SFB_BC_HALO = 0, 1, 2, 3
 SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL = 0, 1
 SFB_NTAB = 10
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 vp = ctypes.c_void_p
 VP3 = vp * 3
@@ -49,6 +49,7 @@ class StageArgs(ctypes.Structure):
         ("ca", ctypes.c_double),
         ("nu", ctypes.c_double),
         ("force", ctypes.c_double * 3),
+        ("p_int", vp),
     ]
 
 
@@ -75,6 +76,8 @@ _SIGS = {
     "sfb_solver_uses_own_fft": [vp],
     "sfb_solver_solve": [vp, vp, vp, vp],
     "sfb_project": [vp, VP3, vp, vp],
+    "sfb_project_solve": [vp, VP3, ctypes.POINTER(vp), vp],
+    "sfb_project_launches": [vp, ctypes.c_int],
     "sfb_slab_solver_create": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
     "sfb_slab_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
     "sfb_slab_forward": [vp, VP3, vp],
@@ -146,12 +149,16 @@ launches = 0
 def call(name, *args):
     global launches
     check(getattr(lib, name)(*args))
+    if name in ("sfb_project", "sfb_project_solve"):
+        global launches
+        with_p = name == "sfb_project" and args[2] is not None and args[2] != 0
+        k = lib.sfb_project_launches(args[0], 2 if name == "sfb_project_solve" else int(with_p))
+        launches += k
+        return
     k = KERNELS_PER_CALL.get(name, 0)
-    if name in ("sfb_project", "sfb_project_pullback", "sfb_project_pullback_ex", "sfb_solver_solve"):
+    if name in ("sfb_project_pullback", "sfb_project_pullback_ex", "sfb_solver_solve"):
         own = lib.sfb_solver_uses_own_fft(args[0])
         k += 4 if own else 0
-    if name == "sfb_project" and args[2] is not None and args[2] != 0:
-        k += 1  # extended pressure written
     launches += k
 
 

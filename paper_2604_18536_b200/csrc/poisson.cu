@@ -442,26 +442,38 @@ template int solve_inplace<double>(sfb_solver*, double*, cudaStream_t);
 template int solve_inplace<float>(sfb_solver*, float*, cudaStream_t);
 
 template <typename T>
-static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) {
+static bool divfused(const sfb_solver* s) {
+  return s->fft.enabled && (fft_divfuse_ok<T>(s->fft, geo<T>(s->plan)) || getenv("SFB_DIVFUSE"));
+}
+
+// divergence -> solve; the pressure interior is left in s->rbuf
+template <typename T>
+static int project_solve(sfb_solver* s, const void* const* u, cudaStream_t st) {
   sfb_plan* p = s->plan;
   const Geo<T>& G = geo<T>(p);
-  MV<T> U;
   CV<T> C;
-  for (int a = 0; a < 3; ++a) {
-    U.c[a] = a < p->dim ? (T*)u[a] : nullptr;
-    C.c[a] = U.c[a];
-  }
+  for (int a = 0; a < 3; ++a) C.c[a] = a < p->dim ? (const T*)u[a] : nullptr;
   T* rb = (T*)s->rbuf;
-  Box B = int_box(G);
   int rc;
-  if (s->fft.enabled && (fft_divfuse_ok<T>(s->fft, G) || getenv("SFB_DIVFUSE"))) {
+  if (divfused<T>(s)) {
     // divergence fused into the first FFT pass
-    if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, (const void* const*)u))) return rc;
+    if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, u))) return rc;
   } else {
     if ((rc = launch_div<T>(G, C, rb, st))) return rc;
     if ((rc = solve_inplace<T>(s, rb, st))) return rc;
   }
-  if ((rc = launch_grad<T>(G, rb, U, (T*)p_ext, st))) return rc;
+  return SFB_OK;
+}
+
+template <typename T>
+static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) {
+  sfb_plan* p = s->plan;
+  const Geo<T>& G = geo<T>(p);
+  MV<T> U;
+  for (int a = 0; a < 3; ++a) U.c[a] = a < p->dim ? (T*)u[a] : nullptr;
+  int rc;
+  if ((rc = project_solve<T>(s, (const void* const*)u, st))) return rc;
+  if ((rc = launch_grad<T>(G, (T*)s->rbuf, U, (T*)p_ext, st))) return rc;
   if ((rc = launch_planes<T>(G, U, p->dim, 0, st))) return rc;
   if (p_ext) {
     // pressure ghosts (fields.py:81-93) from the interior just written
@@ -632,6 +644,27 @@ int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream) {
   rc = p->dtype == SFB_F64 ? solve_inplace<double>(s, (double*)s->rbuf, st) : solve_inplace<float>(s, (float*)s->rbuf, st);
   if (rc) return rc;
   return cuda_check(cudaMemcpyAsync(out, s->rbuf, bytes, cudaMemcpyDeviceToDevice, st), "copy out");
+}
+
+int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, void* stream) {
+  if (!s || !u || !p_int) return fail(SFB_EINVAL, "null argument");
+  if (s->slab) return fail(SFB_ECONFIG, "sfb_project_solve: slab solvers use the sfb_slab_* sequence");
+  for (int a = 0; a < s->plan->dim; ++a)
+    if (!u[a]) return fail(SFB_EINVAL, "null velocity component");
+  const int rc = s->plan->dtype == SFB_F64 ? project_solve<double>(s, u, (cudaStream_t)stream)
+                                           : project_solve<float>(s, u, (cudaStream_t)stream);
+  *p_int = rc ? nullptr : s->rbuf;
+  return rc;
+}
+
+int sfb_project_launches(const sfb_solver* s, int mode) {
+  if (!s) return 0;
+  const bool fused = s->plan->dtype == SFB_F64 ? divfused<double>(s) : divfused<float>(s);
+  int n;
+  if (s->fft.enabled) n = (s->plan->dim == 3 ? 5 : 3) + (fused ? 0 : 1);
+  else n = 2;  // divergence + eigenvalue scaling / tridiagonal (cuFFT transforms not counted)
+  if (mode == 2) return n;
+  return n + 2 + (mode == 1 ? 1 : 0);  // gradient subtract, velocity ghosts (+ pressure ghosts)
 }
 
 int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream) {

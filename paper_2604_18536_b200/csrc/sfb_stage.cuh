@@ -11,6 +11,7 @@ struct StageArgs {
   MV<T> s_out, y_next, k_out;
   T cb, ca, nu;
   Force<T> F;
+  const T* p_int;  // FL_PROJ: contiguous interior pressure; y is projected on the fly
   int has_s, has_next, has_k, s_from_u0, diff;
 };
 
@@ -48,7 +49,8 @@ __device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
 
 // epilogue variants (compile-time): bit 1 k_out, bit 2 s_out, bit 4 s from
 // u0 (else s_in), bit 8 y_next
-enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8 };
+// bit 16: y is unprojected, y - G p is formed in shared memory (all-periodic 3D)
+enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16 };
 
 template <typename T>
 int stage_pair(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st);

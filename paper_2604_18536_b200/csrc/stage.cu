@@ -92,24 +92,30 @@ __device__ __forceinline__ T rhs_ring(const T* const (&P)[3], const Coef<T> (&C)
   return v;
 }
 
-constexpr int kRing = 5;  // planes i-1, i, i+1 in use, i+2 landing, i+3 issued
+constexpr int kRing = 5;   // planes i-1, i, i+1 in use, i+2 landing, i+3 issued
+constexpr int kPRing = 4;  // FL_PROJ: pressure planes, slot = plane & 3
 
 template <typename T, int TJ, int TK, int CPT, int FL, int MINB>
 __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
   typedef RingGeom<TJ, TK> RG;
+  constexpr bool PROJ = (FL & FL_PROJ) != 0;
   constexpr int NTH = TJ / CPT * TK;                // threads per CTA
   constexpr int NE = 3 * RG::PS;                    // values per plane slot
   constexpr int NQ = (NE + NTH - 1) / NTH;          // fill copies per thread
   constexpr int RS = TJ / CPT;                      // row stride between a thread's cells
+  constexpr int PPW = TK + 3, PPS = (TJ + 3) * PPW; // FL_PROJ pressure slot (j0-1 .. j0+TJ+1)
+  constexpr int NQP = PROJ ? (PPS + NTH - 1) / NTH : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);         // [kRing][3][PS]
   Coef<T>* cj = reinterpret_cast<Coef<T>*>(ring + kRing * NE);  // axis-1 coefficients of the tile rows
+  T* pring = reinterpret_cast<T*>(cj + TJ);         // FL_PROJ: [kPRing][PPS]
   const int tk = threadIdx.x, tq = threadIdx.y, tid = tq * TK + tk;
   const int k0 = 1 + blockIdx.x * TK, j0 = 1 + blockIdx.y * TJ;
   const int ib = 1 + blockIdx.z * chunk;
   const int ie = min(ib + chunk, G.n[0] + 1);
   const int k = k0 + tk;
   const long long s0 = G.s[0];
+  const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
 
   const T* fsrc[NQ];
   bool fok[NQ];
@@ -120,28 +126,96 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
     const int r = e - c * RG::PS;
     const int jj = r / RG::PW;
     const int kk = r - jj * RG::PW;
-    const int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
+    int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
     fok[q] = e < NE && gj < G.E[1] && gk < G.E[2];
+    if (PROJ) {
+      gj = wrap1(gj, n1);
+      gk = wrap1(gk, n2);
+    }
     fsrc[q] = A.y.c[c < 3 ? c : 0] + (fok[q] ? (long long)gj * G.s[1] + gk : 0);
   }
-  auto load_plane = [&](int ip, int slot) {
+  const T* psrc[NQP];
+  bool pok[NQP];
+  if constexpr (PROJ) {
+#pragma unroll
+    for (int q = 0; q < NQP; ++q) {
+      const int e = tid + q * NTH;
+      const int jj = e / PPW, kk = e - (e / PPW) * PPW;
+      const int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
+      pok[q] = e < PPS && gj <= n1 + 2 && gk <= n2 + 2;
+      psrc[q] = A.p_int + (pok[q] ? (long long)(wrap1(gj, n1) - 1) * n2 + (wrap1(gk, n2) - 1) : 0);
+    }
+  }
+  const long long ps0 = (long long)n1 * n2;
+  auto load_p = [&](int ip) {
+    if constexpr (PROJ) {
+      T* dst = pring + (ip & (kPRing - 1)) * PPS + tid;
+      const long long base = (long long)(wrap1(ip, n0) - 1) * ps0;
+#pragma unroll
+      for (int q = 0; q < NQP; ++q)
+        if (q < NQP - 1 || tid + q * NTH < PPS) cp_async_val(dst + q * NTH, psrc[q] + (pok[q] ? base : 0), pok[q]);
+    }
+  };
+  auto load_plane = [&](int ip, int slot, bool with_p = true) {
     if (ip < 0 || ip >= G.E[0]) return;
     T* dst = ring + slot * NE + tid;
-    const long long base = (long long)ip * s0;
+    const long long base = (long long)(PROJ ? wrap1(ip, n0) : ip) * s0;
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
       if (q < NQ - 1 || tid + q * NTH < NE) cp_async_val(dst + q * NTH, fsrc[q] + (fok[q] ? base : 0), fok[q]);
+    if (with_p) load_p(ip + 1);  // the pressure plane this y plane's projection needs besides its own
+  };
+  // y -= G p on one freshly landed plane slot (poisson.py:334-339 arithmetic).
+  // A thread owns the same in-plane positions r = tid + q*NTH of every plane:
+  // their pressure-slot offsets are fixed, the axis-1/2 reciprocal widths
+  // come from two small shared tables filled once.
+  constexpr int NR = (RG::PS + NTH - 1) / NTH;
+  T* rdj = pring + kPRing * PPS;  // [TJ+2] 1/du_1 of the slot rows (wrapped)
+  T* rdk = rdj + (TJ + 2);        // [TK+2] 1/du_2 of the slot columns
+  int rpo[NR];
+  if constexpr (PROJ) {
+    for (int e = tid; e < TJ + 2; e += NTH) rdj[e] = tab(G, 1, T_RDU, wrap1(min(j0 - 1 + e, n1 + 1), n1));
+    for (int e = tid; e < TK + 2; e += NTH) rdk[e] = tab(G, 2, T_RDU, wrap1(min(k0 - 1 + e, n2 + 1), n2));
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int r = tid + q * NTH;
+      const int jj = r / RG::PW, kk = r - (r / RG::PW) * RG::PW;
+      rpo[q] = (jj << 16) | kk;
+    }
+  }
+  auto project_plane = [&](int ip, int slot) {
+    if constexpr (PROJ) {
+      T* ys = ring + slot * NE;
+      const T* pc = pring + (ip & (kPRing - 1)) * PPS;
+      const T* pn = pring + ((ip + 1) & (kPRing - 1)) * PPS;
+      const T r0 = tab(G, 0, T_RDU, wrap1(ip, n0));
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int r = tid + q * NTH;
+        if (q < NR - 1 || r < RG::PS) {
+          const int jj = rpo[q] >> 16, kk = rpo[q] & 0xffff;
+          const int po = jj * PPW + kk;
+          const T p0 = pc[po];
+          ys[r] -= (pn[po] - p0) * r0;
+          ys[RG::PS + r] -= (pc[po + PPW] - p0) * rdj[jj];
+          ys[2 * RG::PS + r] -= (pc[po + 1] - p0) * rdk[kk];
+        }
+      }
+    }
   };
   if (tid < TJ) cj[tid] = coef_at(G, 1, min(j0 + tid, G.n[1]));
   Coef<T> C[3];
   C[2] = coef_at(G, 2, min(k, G.n[2]));
 
   int sl_m = (ib - 1) % kRing;
+  if (PROJ) load_p(ib - 1);
   load_plane(ib - 1, sl_m);
   load_plane(ib, (sl_m + 1) % kRing);
   load_plane(ib + 1, (sl_m + 2) % kRing);
   cp_commit();
-  load_plane(ib + 2, (sl_m + 3) % kRing);
+  // FL_PROJ: pressure plane ib+3 would land in the slot of ib-1, still needed
+  // by the first projection; it is loaded in the first iteration instead
+  load_plane(ib + 2, (sl_m + 3) % kRing, !PROJ);
   cp_commit();
 
   bool inside[CPT];
@@ -174,15 +248,25 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
       }
     }
     C[0] = coef_at(G, 0, i);
-    cp_wait<1>();
+    if (PROJ && i == ib + 1) cp_wait<0>();
+    else cp_wait<1>();
     __syncthreads();
     int sl_l = sl_m + 4;
     if (sl_l >= kRing) sl_l -= kRing;
-    load_plane(i + 3, sl_l);
-    cp_commit();
     int s1i = sl_m + 1, s2i = sl_m + 2;
     if (s1i >= kRing) s1i -= kRing;
     if (s2i >= kRing) s2i -= kRing;
+    if constexpr (PROJ) {
+      if (i == ib) {
+        project_plane(i - 1, sl_m);
+        project_plane(i, s1i);
+      }
+      project_plane(i + 1, s2i);
+      __syncthreads();
+      if (i == ib) load_p(ib + 3);
+    }
+    load_plane(i + 3, sl_l);
+    cp_commit();
 #pragma unroll
     for (int r = 0; r < CPT; ++r) {
       const int c0 = (tq + r * RS + 1) * RG::PW + (tk + 1);
@@ -211,8 +295,15 @@ constexpr int kTJ = 8, kTK = 32, kCPT = 2;
 template <typename T, int FL>
 static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
   typedef RingGeom<kTJ, kTK> RG;
-  constexpr int MINB = 4;
-  const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T) + kTJ * sizeof(Coef<T>);
+#ifndef SFB_STAGE_MINB
+#define SFB_STAGE_MINB 3
+#endif
+#ifndef SFB_STAGE_MINB_PROJ
+#define SFB_STAGE_MINB_PROJ 3
+#endif
+  constexpr int MINB = (FL & FL_PROJ) ? SFB_STAGE_MINB_PROJ : SFB_STAGE_MINB;
+  const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T) + kTJ * sizeof(Coef<T>) +
+                      ((FL & FL_PROJ) ? ((size_t)kPRing * (kTJ + 3) * (kTK + 3) + kTJ + kTK + 4) * sizeof(T) : 0);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_stage_march<T, kTJ, kTK, kCPT, FL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -233,8 +324,10 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
 template <typename T>
 static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
   const int fl = (A.has_k ? FL_K : 0) | (A.has_s ? FL_S : 0) | (A.has_s && A.s_from_u0 ? FL_SU0 : 0) |
-                 (A.has_next ? FL_NEXT : 0);
+                 (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0);
   switch (fl) {
+    case FL_S | FL_NEXT | FL_PROJ: return stage_march_launch<T, FL_S | FL_NEXT | FL_PROJ>(G, A, st);
+    case FL_S | FL_PROJ: return stage_march_launch<T, FL_S | FL_PROJ>(G, A, st);
     case FL_S | FL_SU0 | FL_NEXT: return stage_march_launch<T, FL_S | FL_SU0 | FL_NEXT>(G, A, st);
     case FL_S | FL_NEXT: return stage_march_launch<T, FL_S | FL_NEXT>(G, A, st);
     case FL_S: return stage_march_launch<T, FL_S>(G, A, st);
@@ -267,15 +360,19 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
   A.has_s = a->s_out[0] != nullptr;
   A.has_next = a->y_next[0] != nullptr;
   A.s_from_u0 = a->s_in[0] == nullptr;
+  A.p_int = (const T*)a->p_int;
+  if (A.p_int && !(G.dim == 3 && p->all_periodic && !G.halo[0]))
+    return fail(SFB_ECONFIG, "on-the-fly projection needs an all-periodic 3D plan");
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
-  if (G.dim == 3 && !getenv("SFB_STAGE_GENERIC")) {
-    if (getenv("SFB_PAIR")) {
+  if (G.dim == 3 && (!getenv("SFB_STAGE_GENERIC") || A.p_int)) {
+    if (getenv("SFB_PAIR") && !A.p_int) {
       const int rcp = stage_pair<T>(G, A, st);
       if (rcp >= 0) return rcp;
     }
     const int rc = stage_march<T>(G, A, st);
     if (rc >= 0) return rc;
+    if (A.p_int) return fail(SFB_ECONFIG, "on-the-fly projection: unsupported stage variant");
   }
   Box B = int_box(G);
   SFB_DISPATCH_DIM(G.dim, D, (k_stage_generic<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, A, B)));
