@@ -50,7 +50,9 @@ __device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
 // epilogue variants (compile-time): bit 1 k_out, bit 2 s_out, bit 4 s from
 // u0 (else s_in), bit 8 y_next
 // bit 16: y is unprojected, y - G p is formed in shared memory (all-periodic 3D)
-enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16 };
+// bit 32: every axis periodic (every interior cell is a DOF of every component):
+// branch-free stencil evaluation, stores predicated on the tile bounds only
+enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16, FL_PER = 32 };
 
 template <typename T>
 int stage_pair(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st);

@@ -99,6 +99,7 @@ template <typename T, int TJ, int TK, int CPT, int FL, int MINB>
 __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
   typedef RingGeom<TJ, TK> RG;
   constexpr bool PROJ = (FL & FL_PROJ) != 0;
+  constexpr bool PER = (FL & FL_PER) != 0;
   constexpr int NTH = TJ / CPT * TK;                // threads per CTA
   constexpr int NE = 3 * RG::PS;                    // values per plane slot
   constexpr int NQ = (NE + NTH - 1) / NTH;          // fill copies per thread
@@ -234,9 +235,9 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
 #pragma unroll
     for (int r = 0; r < CPT; ++r) {
       const long long x = x0 + r * rstep;
-      dof[r][0] = inside[r] && !(wall0 && i == G.n[0]);
-      dof[r][1] = inside[r] && !(wall1 && jr[r] == G.n[1]);
-      dof[r][2] = inside[r] && !(wall2 && k == G.n[2]);
+      dof[r][0] = inside[r] && (PER || !(wall0 && i == G.n[0]));
+      dof[r][1] = inside[r] && (PER || !(wall1 && jr[r] == G.n[1]));
+      dof[r][2] = inside[r] && (PER || !(wall2 && k == G.n[2]));
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         b0[r][a] = T(0);
@@ -273,9 +274,15 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
       const T* const P[3] = {ring + sl_m * NE + c0, ring + s1i * NE + c0, ring + s2i * NE + c0};
       C[1] = cj[tq + r * RS];
       T kv[3];
-      kv[0] = dof[r][0] ? rhs_ring<T, 0, TJ, TK>(P, C, A.diff, A.nu, A.F.f[0]) : T(0);
-      kv[1] = dof[r][1] ? rhs_ring<T, 1, TJ, TK>(P, C, A.diff, A.nu, A.F.f[1]) : T(0);
-      kv[2] = dof[r][2] ? rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]) : T(0);
+      if constexpr (PER) {
+        kv[0] = rhs_ring<T, 0, TJ, TK>(P, C, A.diff, A.nu, A.F.f[0]);
+        kv[1] = rhs_ring<T, 1, TJ, TK>(P, C, A.diff, A.nu, A.F.f[1]);
+        kv[2] = rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]);
+      } else {
+        kv[0] = dof[r][0] ? rhs_ring<T, 0, TJ, TK>(P, C, A.diff, A.nu, A.F.f[0]) : T(0);
+        kv[1] = dof[r][1] ? rhs_ring<T, 1, TJ, TK>(P, C, A.diff, A.nu, A.F.f[1]) : T(0);
+        kv[2] = dof[r][2] ? rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]) : T(0);
+      }
       const long long x = x0 + r * rstep;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -322,10 +329,17 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
 }
 
 template <typename T>
-static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
+static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st, bool allow_per = true) {
+  const bool per = allow_per && G.per[0] && G.per[1] && G.per[2] && !G.halo[0] && !G.halo[1] && !G.halo[2] &&
+                   !getenv("SFB_STAGE_NOPER");
   const int fl = (A.has_k ? FL_K : 0) | (A.has_s ? FL_S : 0) | (A.has_s && A.s_from_u0 ? FL_SU0 : 0) |
-                 (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0);
+                 (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0) | (per ? FL_PER : 0);
   switch (fl) {
+    case FL_PER | FL_S | FL_NEXT | FL_PROJ: return stage_march_launch<T, FL_PER | FL_S | FL_NEXT | FL_PROJ>(G, A, st);
+    case FL_PER | FL_S | FL_PROJ: return stage_march_launch<T, FL_PER | FL_S | FL_PROJ>(G, A, st);
+    case FL_PER | FL_S | FL_SU0 | FL_NEXT: return stage_march_launch<T, FL_PER | FL_S | FL_SU0 | FL_NEXT>(G, A, st);
+    case FL_PER | FL_S | FL_NEXT: return stage_march_launch<T, FL_PER | FL_S | FL_NEXT>(G, A, st);
+    case FL_PER | FL_S: return stage_march_launch<T, FL_PER | FL_S>(G, A, st);
     case FL_S | FL_NEXT | FL_PROJ: return stage_march_launch<T, FL_S | FL_NEXT | FL_PROJ>(G, A, st);
     case FL_S | FL_PROJ: return stage_march_launch<T, FL_S | FL_PROJ>(G, A, st);
     case FL_S | FL_SU0 | FL_NEXT: return stage_march_launch<T, FL_S | FL_SU0 | FL_NEXT>(G, A, st);
@@ -334,7 +348,9 @@ static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) 
     case FL_S | FL_SU0: return stage_march_launch<T, FL_S | FL_SU0>(G, A, st);
     case FL_K: return stage_march_launch<T, FL_K>(G, A, st);
     case FL_NEXT: return stage_march_launch<T, FL_NEXT>(G, A, st);
-    default: return -1;  // uncommon combination: generic kernel
+    default:
+      if (fl & FL_PER) return stage_march<T>(G, A, st, false);  // rarer variants: general-BC kernels
+      return -1;  // uncommon combination: generic kernel
   }
 }
 
