@@ -350,7 +350,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "k_stage_march (fused RHS + RK stage combine)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind, "traffic": traffic,
-                         "bytes_per_cell": "72/120/120/72 per stage launch (avg 96 B fp64)",
+                         "bytes_per_cell": ("72/128/128/80 B fp64 per stage launch: y, u0, s, y_next fields "
+                                            "+ the pressure on the stages that apply the previous projection"),
                          "stage_share_of_step": st_ms / (ms * args.steps)},
             "step_roofline": {"algorithmic_bytes_per_cell": bpc, "achieved": step_gbs, "peak": peak,
                               "frac": step_gbs / peak},

@@ -1,0 +1,98 @@
+"""GPU tests of the fast paths behind the reference API, each against the CPU
+oracle and against the slower path it replaces:
+
+* the register-resident FFT engine (sfb_fft_reg.cuh) on every transform
+  length class it instantiates, fp64 and fp32, including the 28 x 30 strided
+  engine (840) and the 20 x 21 real-trick rows (840 reals);
+* the divergence fused into the first FFT pass (poisson.py:321-333);
+* the gradient subtract of the intermediate RK projections fused into the next
+  stage kernel (timestep.py:198-199 + poisson.py:333-339), which never
+  materialises the projected stage state.
+"""
+
+import numpy as np
+import pytest
+
+from _dev import grids, random_vel, rel, tol, vel
+from oracle import stagflow_np as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2604_18536_b200 as P
+
+    return P
+
+
+def _solve(P, shape, dtype, monkeypatch, stockham):
+    if stockham:
+        monkeypatch.setenv("SFB_FFT_STOCKHAM", "1")
+    else:
+        monkeypatch.delenv("SFB_FFT_STOCKHAM", raising=False)
+    rng = np.random.default_rng(sum(shape))
+    bounds = [O.uniform_bounds(0, 1.0 + 0.2 * a, n) for a, n in enumerate(shape)]
+    pg, og = grids(P, bounds, (True,) * len(shape), dtype)
+    solver = P.make_solver("spectral", pg, P.BoundarySpec.all_periodic(len(shape)))
+    rhs = og.zeros()
+    rhs[og.pdof()] = rng.standard_normal(og.shape)
+    rhs[og.pdof()] -= rhs[og.pdof()].mean()
+    got = solver.solve(P.ScalarField(pg, rhs)).numpy()[pg.p_slices()]
+    og64 = O.OGrid(bounds, (True,) * len(shape), np.float64)
+    ref = O.SpectralSolve(og64)(rhs[og.pdof()].astype(np.float64))
+    return got, ref
+
+
+# strided lengths 840 (28x30), 512 (16x32), 420 (20x21), 256, 96, 64, 48, 40;
+# real-trick half lengths 420, 256, 128, 48, 24, 20, 16
+@pytest.mark.parametrize("shape", [(840, 6, 8), (6, 840, 40), (512, 4, 16), (4, 420, 48), (256, 8, 840),
+                                   (96, 64, 512), (48, 40, 32), (840, 32)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_register_fft_solve_vs_oracle_and_stockham(P, shape, dtype, monkeypatch):
+    got, ref = _solve(P, shape, dtype, monkeypatch, stockham=False)
+    assert rel(got, ref) <= (1e-12 if dtype == np.float64 else 2e-5)
+    old, _ = _solve(P, shape, dtype, monkeypatch, stockham=True)
+    assert rel(got, old) <= (1e-13 if dtype == np.float64 else 2e-5)
+
+
+def _rk4(P, n, dtype, monkeypatch, env):
+    for k in ("SFB_NO_PROJFUSE", "SFB_NO_DIVFUSE"):
+        monkeypatch.delenv(k, raising=False)
+    for k in env:
+        monkeypatch.setenv(k, "1")
+    bounds = [O.uniform_bounds(0.0, 1.0 + 0.3 * a, m) for a, m in enumerate(n)]
+    pg, og = grids(P, bounds, (True,) * 3, dtype)
+    rng = np.random.default_rng(7)
+    u0 = random_vel(og, rng)
+    O.fill_velocity(og, O.periodic_bcs(3), u0)
+    solve = O.SpectralSolve(og)
+    O.project_into(og, O.periodic_bcs(3), solve, u0)
+    setup = P.Setup(pg, P.BoundarySpec.all_periodic(3), nu=0.02, force=(0.3, 0.0, -0.1), solver="spectral",
+                    method="rk4")
+    st = setup.new_state(u0=vel(P, pg, u0))
+    P.rk_step(st, 2e-3, P.RK4, setup.solver, setup)
+    ref_u, ref_p = O.rk_step(og, O.periodic_bcs(3), solve, [x.copy() for x in u0], 2e-3, O.RK4, 0.02,
+                             (0.3, 0.0, -0.1))
+    return st.u.numpy(), st.pressure.numpy(), ref_u, ref_p
+
+
+@pytest.mark.parametrize("n", [(24, 20, 40), (40, 33, 48), (16, 16, 840)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_fused_projection_paths(P, n, dtype, monkeypatch):
+    """RK4 step with (a) divergence fused into R2C + gradient subtract fused
+    into the next stage (default), (b) no stage fusion, (c) no fusion at all:
+    all equal the oracle within the north-star tolerance and each other."""
+    t = tol(dtype)
+    runs = [_rk4(P, n, dtype, monkeypatch, env) for env in ((), ("SFB_NO_PROJFUSE",),
+                                                          ("SFB_NO_PROJFUSE", "SFB_NO_DIVFUSE"))]
+    for u, p, ref_u, ref_p in runs:
+        for a in range(3):
+            assert rel(u[a], ref_u[a]) <= t, a
+        assert rel(p, ref_p) <= 10 * t
+    for a in range(3):
+        assert rel(runs[0][0][a], runs[2][0][a]) <= t
