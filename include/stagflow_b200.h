@@ -139,7 +139,8 @@ int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream);
  * pressure, valid until the solver's next use.  Feed it to the next
  * sfb_rk_stage (sfb_stage_args.p_int), which applies u - G p on the fly. */
 int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, void* stream);
-/* Number of kernels (ours) one sfb_project launches (bench bookkeeping). */
+/* Number of kernels (ours) launched by sfb_project (mode 0: without, 1: with
+ * the extended pressure), sfb_project_solve (2) or sfb_slab_forward (3). */
 int sfb_project_launches(const sfb_solver* s, int with_pressure);
 
 /* Slab-decomposed spectral solve (multi-GPU, axis 0 split over nranks; the

@@ -138,10 +138,10 @@ KERNELS_PER_CALL = {
     "sfb_rk_stage": 1, "sfb_combine": 1, "sfb_wray_update": 1, "sfb_fill_ghosts_velocity": 1,
     "sfb_fill_ghosts_scalar": 1, "sfb_divergence": 1, "sfb_pressure_gradient": 1, "sfb_convection": 1,
     "sfb_diffusion": 1, "sfb_momentum_rhs": 1, "sfb_weighted_scale": 1, "sfb_kinetic_energy": 2,
-    "sfb_weighted_inner": 2, "sfb_cfl_conv": 2, "sfb_solver_solve": 1, "sfb_project": 4,
+    "sfb_weighted_inner": 2, "sfb_cfl_conv": 2, "sfb_solver_solve": 1,
     "sfb_divergence_pullback": 2, "sfb_pressure_gradient_pullback": 2, "sfb_diffusion_pullback": 2,
     "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4, "sfb_project_pullback_ex": 4,
-    "sfb_slab_forward": 3, "sfb_slab_axis0": 1, "sfb_slab_inverse": 2, "sfb_slab_correct": 2,
+    "sfb_slab_axis0": 1, "sfb_slab_inverse": 2, "sfb_slab_correct": 2,
 }
 launches = 0
 
@@ -149,10 +149,10 @@ launches = 0
 def call(name, *args):
     global launches
     check(getattr(lib, name)(*args))
-    if name in ("sfb_project", "sfb_project_solve"):
-        global launches
+    if name in ("sfb_project", "sfb_project_solve", "sfb_slab_forward"):
         with_p = name == "sfb_project" and args[2] is not None and args[2] != 0
-        k = lib.sfb_project_launches(args[0], 2 if name == "sfb_project_solve" else int(with_p))
+        mode = {"sfb_project_solve": 2, "sfb_slab_forward": 3}.get(name, int(with_p))
+        k = lib.sfb_project_launches(args[0], mode)
         launches += k
         return
     k = KERNELS_PER_CALL.get(name, 0)

@@ -541,13 +541,26 @@ template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, co
 // ---- slab-decomposed pieces (multi-GPU): F.n = {m local planes, n1, n2},
 // F.ax[0] is the global axis-0 length, F.sc.l1 offset to this rank's k1 chunk.
 template <typename T>
-int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st) {
+int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u) {
   typedef typename CX<T>::t C;
   C* cbuf = (C*)cbuf_v;
-  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], M = nlast / 2, nh = M + 1;
+  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], nh = nlast / 2 + 1;
   const long long rows = (long long)m * n1;
-  (void)M;
-  int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
+  int rc;
+  if (G && fft_divfuse_ok(F, *G)) {
+    RegCall c{};
+    c.kind = 5;
+    c.out = cbuf;
+    c.rows = rows;
+    c.out_row = nh;
+    c.twL = F.tw_half;
+    c.twN = F.tw_full;
+    c.geo = G;
+    for (int a = 0; a < 3; ++a) c.u[a] = u[a];
+    rc = reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
+  } else {
+    rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
+  }
   if (rc) return rc;
   ScaleArgs none{};
   return launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
@@ -573,8 +586,9 @@ int fft_slab_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st) {
   (void)M;
   return launch_c2r<T>(F, cbuf, rbuf, (long long)m * n1, st);
 }
-template int fft_slab_forward<double>(FftSolve&, double*, void*, cudaStream_t);
-template int fft_slab_forward<float>(FftSolve&, float*, void*, cudaStream_t);
+template int fft_slab_forward<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*,
+                                      const void* const*);
+template int fft_slab_forward<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*);
 template int fft_slab_axis0<double>(FftSolve&, void*, int, cudaStream_t);
 template int fft_slab_axis0<float>(FftSolve&, void*, int, cudaStream_t);
 template int fft_slab_inverse<double>(FftSolve&, void*, double*, cudaStream_t);

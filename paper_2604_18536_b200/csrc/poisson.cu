@@ -660,6 +660,7 @@ int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, v
 int sfb_project_launches(const sfb_solver* s, int mode) {
   if (!s) return 0;
   const bool fused = s->plan->dtype == SFB_F64 ? divfused<double>(s) : divfused<float>(s);
+  if (mode == 3) return fused ? 2 : 3;  // sfb_slab_forward
   int n;
   if (s->fft.enabled) n = (s->plan->dim == 3 ? 5 : 3) + (fused ? 0 : 1);
   else n = 2;  // divergence + eigenvalue scaling / tridiagonal (cuFFT transforms not counted)
@@ -771,6 +772,8 @@ template <typename T>
 static int slab_forward(sfb_solver* s, void* const* u, cudaStream_t st) {
   sfb_plan* p = s->plan;
   const Geo<T>& G = geo<T>(p);
+  if (fft_divfuse_ok<T>(s->fft, G))
+    return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st, &G, (const void* const*)u);
   CV<T> C;
   for (int a = 0; a < 3; ++a) C.c[a] = (const T*)u[a];
   int rc = launch_div<T>(G, C, (T*)s->rbuf, st);

@@ -68,8 +68,10 @@ int fft_tma_make(FftTma& M, void* base, bool f64, int rank, long long inner_comp
                  int L);
 template <typename T, int MODE>
 int fft_tma_pass(const FftTma& M, const FftLen& P, const void* tw, const ScaleArgs& sc, cudaStream_t st);
+// divergence of u fused into the R2C pass when G/u are given and supported
 template <typename T>
-int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st);
+int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const Geo<T>* G = nullptr,
+                     const void* const* u = nullptr);
 template <typename T>
 int fft_slab_axis0(FftSolve& F, void* tbuf, int n1_chunk, cudaStream_t st);
 template <typename T>
