@@ -22,6 +22,8 @@
  *      SFB_EINVAL   -> ValueError            (e.g. operators.py:142-143)
  *      SFB_ECONFIG  -> ConfigurationError    (errors.py:4-5)
  *      SFB_ENUMERIC -> NumericalError        (errors.py:17-18)
+ *      SFB_ECONVERGE -> ConvergenceError     (errors.py:8-14; sfb_cg_info gives
+ *                       the iterations and the residual history)
  *      SFB_ECUDA    -> RuntimeError (CUDA / cuFFT failure)
  */
 #ifndef STAGFLOW_B200_H
@@ -35,12 +37,12 @@ extern "C" {
 
 #define SFB_ABI_VERSION 2
 
-enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4 };
+enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4, SFB_ECONVERGE = 5 };
 enum { SFB_F64 = 0, SFB_F32 = 1 };
 /* SFB_BC_HALO: ghost planes of this axis are supplied by the caller (the
  * neighbouring z-slab of a multi-GPU decomposition); DOFs as periodic. */
 enum { SFB_BC_PERIODIC = 0, SFB_BC_DIRICHLET = 1, SFB_BC_SYMMETRIC = 2, SFB_BC_HALO = 3 };
-enum { SFB_SOLVER_SPECTRAL = 0, SFB_SOLVER_CHANNEL = 1 };
+enum { SFB_SOLVER_SPECTRAL = 0, SFB_SOLVER_CHANNEL = 1, SFB_SOLVER_CG = 2 };
 
 /* Per-axis host tables, packed axis by axis, each of length n[a]+2, in this
  * order (values already rounded to the plan dtype, as grid.py:168-171 and
@@ -127,6 +129,13 @@ int sfb_cfl_conv(sfb_plan* plan, const void* const* u, double* out, void* stream
  *           DirectPoissonSolver (poisson.py:203-229) by FFT(x,z) x batched
  *           tridiagonal(y) with the weighted zero-mean gauge. */
 int sfb_solver_create(sfb_plan* plan, int kind, sfb_solver** out);
+/* CG: matrix-free conjugate gradient on -W L (poisson.py:232-308), any BCs
+ * and stretching.  Defaults follow the reference (tol 1e-10 fp64 / 1e-5 fp32,
+ * max_iter = min(10000, 10 ceil(N^(1/d)) + 10)); sfb_cg_configure overrides. */
+int sfb_cg_configure(sfb_solver* s, double tol, int max_iter);
+/* Iterations of the last solve and its residual history (|r| before the first
+ * iteration, then after each); *count = history length. */
+int sfb_cg_info(const sfb_solver* s, int* iterations, double* history, int cap, int* count);
 int sfb_solver_destroy(sfb_solver* s);
 /* 1 if the solver runs the hand-written FFT engine, 0 if it uses cuFFT. */
 int sfb_solver_uses_own_fft(const sfb_solver* s);

@@ -401,6 +401,85 @@ class SpectralSolve:
         return _irfftn(rh, s=self.g.shape)
 
 
+def homogeneous_bcs(bcs):
+    """poisson.py:31-40: Dirichlet values -> 0, other kinds unchanged."""
+    return [tuple(("D", 0.0) if _kind(c) == "D" else c for c in side) for side in bcs]
+
+
+def laplacian_apply(g, bcs, p_int):
+    """poisson.py:43-68: scalar fill, gradient on the velocity DOFs,
+    homogeneous velocity fill, divergence; interior in, interior out."""
+    pf = g.zeros()
+    pf[g.pdof()] = p_int
+    fill_scalar(g, bcs, pf)
+    vf = g.zeros_vel()
+    for a in range(g.dim):
+        sl = g.udof(a)
+        t = np.subtract(pf[_sh(sl, a, 1)], pf[sl])
+        t /= g.col(g.du[a], a, sl[a])
+        vf[a][sl] = t
+    fill_velocity(g, homogeneous_bcs(bcs), vf)
+    return divergence(g, vf)[g.pdof()]
+
+
+class CGSolve:
+    """poisson.py:232-308: matrix-free CG on -W L, same update order,
+    gauge fixing and stopping test; records iterations and the residual
+    history."""
+
+    def __init__(self, g, bcs, tol=None, max_iter=None):
+        self.g, self.bcs = g, bcs
+        self.w = pressure_weights(g)
+        self.wtot = float(np.sum(self.w))
+        self.tol = (1e-10 if g.dtype == np.float64 else 1e-5) if tol is None else float(tol)
+        n_dof = int(np.prod(g.shape))
+        self.max_iter = min(10000, 10 * int(np.ceil(n_dof ** (1.0 / g.dim))) + 10) if max_iter is None else max_iter
+        self.iterations = 0
+        self.residual_history = []
+
+    def _wmean(self, a):
+        return float(np.dot(self.w.ravel(), a.ravel()) / self.wtot)
+
+    def __call__(self, rhs):
+        w = self.w
+        r = np.array(rhs, dtype=self.g.dtype)
+        r -= self._wmean(r)
+        r *= w
+        np.negative(r, out=r)
+        b_norm = float(np.linalg.norm(r.ravel()))
+        self.residual_history = [b_norm]
+        x = np.zeros(self.g.shape, dtype=self.g.dtype)
+        self.iterations = 0
+        if b_norm == 0.0:
+            return x
+        p = r.copy()
+        rs = float(np.dot(r.ravel(), r.ravel()))
+        for it in range(1, self.max_iter + 1):
+            ap = laplacian_apply(self.g, self.bcs, p)
+            ap *= w
+            np.negative(ap, out=ap)
+            denom = float(np.dot(p.ravel(), ap.ravel()))
+            if denom <= 0.0:
+                raise FloatingPointError("pressure operator lost positive definiteness")
+            alpha = rs / denom
+            x += p * alpha
+            x -= self._wmean(x)
+            ap *= alpha
+            r -= ap
+            r -= np.mean(r)
+            res = float(np.linalg.norm(r.ravel()))
+            self.residual_history.append(res)
+            self.iterations = it
+            if res <= self.tol * b_norm:
+                return x
+            rs_new = float(np.dot(r.ravel(), r.ravel()))
+            beta = rs_new / rs
+            rs = rs_new
+            p *= beta
+            p += r
+        raise RuntimeError(f"pressure CG did not reach tol={self.tol} in {self.max_iter} iterations")
+
+
 def project_into(g, bcs, solve, u):
     """poisson.py:321-341; returns the ghost-filled pressure."""
     fill_velocity(g, bcs, u)

@@ -7,15 +7,15 @@ fails, and every compute call goes through the CUDA library.
 import ctypes
 import os
 
-from .errors import ConfigurationError, NumericalError
+from .errors import ConfigurationError, ConvergenceError, NumericalError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libstagflow_b200.so")
 
-SFB_OK, SFB_EINVAL, SFB_ECONFIG, SFB_ENUMERIC, SFB_ECUDA = range(5)
+SFB_OK, SFB_EINVAL, SFB_ECONFIG, SFB_ENUMERIC, SFB_ECUDA, SFB_ECONVERGE = range(6)
 SFB_F64, SFB_F32 = 0, 1
 SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC, SFB_BC_HALO = 0, 1, 2, 3
-SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL = 0, 1
+SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL, SFB_SOLVER_CG = 0, 1, 2
 SFB_NTAB = 10
 ABI_VERSION = 2
 
@@ -72,6 +72,9 @@ _SIGS = {
     "sfb_weighted_inner": [vp, VP3, VP3, ctypes.POINTER(ctypes.c_double), vp],
     "sfb_cfl_conv": [vp, VP3, ctypes.POINTER(ctypes.c_double), vp],
     "sfb_solver_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
+    "sfb_cg_configure": [vp, ctypes.c_double, ctypes.c_int],
+    "sfb_cg_info": [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                    ctypes.POINTER(ctypes.c_int)],
     "sfb_solver_destroy": [vp],
     "sfb_solver_uses_own_fft": [vp],
     "sfb_solver_solve": [vp, vp, vp, vp],
@@ -127,6 +130,8 @@ def check(rc):
         raise ValueError(msg)
     if rc == SFB_ECONFIG:
         raise ConfigurationError(msg)
+    if rc == SFB_ECONVERGE:
+        raise ConvergenceError(msg)
     if rc == SFB_ENUMERIC:
         raise NumericalError(msg)
     raise RuntimeError(f"stagflow_b200 CUDA failure: {msg}")

@@ -416,6 +416,7 @@ int solve_inplace(sfb_solver* s, T* buf, cudaStream_t st) {
   // buf: contiguous interior rhs in, solution out
   sfb_plan* p = s->plan;
   int rc;
+  if (s->kind == SFB_SOLVER_CG) return cg_solve<T>(s, buf, st);
   if (s->fft.enabled) return fft_solve_inplace<T>(s->fft, buf, s->cbuf, st);
   if ((rc = exec_fwd<T>(s, buf, st))) return rc;
   if (s->kind == SFB_SOLVER_SPECTRAL) {
@@ -557,6 +558,21 @@ int sfb_solver_create(sfb_plan* p, int kind, sfb_solver** out) {
       return fail(SFB_ECONFIG, "channel pressure solver requires periodic x/z and walls on y");
     if (!axis_uniform(p->hdx[0]) || !axis_uniform(p->hdx[2]))
       return fail(SFB_ECONFIG, "channel pressure solver requires uniform x/z");
+  } else if (kind == SFB_SOLVER_CG) {
+    for (int a = 0; a < p->dim; ++a)
+      if (p->bc_lo[a] == SFB_BC_HALO) return fail(SFB_ECONFIG, "the CG solver does not run on slab plans");
+    sfb_solver* s = new sfb_solver();
+    s->plan = p;
+    s->kind = kind;
+    const size_t esz = p->dtype == SFB_F64 ? 8 : 4;
+    int rc = cuda_check(cudaMalloc(&s->rbuf, esz * p->int_count), "cudaMalloc(rbuf)");
+    if (!rc) rc = cg_setup(s);
+    if (rc) {
+      sfb_solver_destroy(s);
+      return rc;
+    }
+    *out = s;
+    return SFB_OK;
   } else {
     return fail(SFB_ECONFIG, "unknown pressure solver kind");
   }
@@ -625,6 +641,7 @@ int sfb_solver_destroy(sfb_solver* s) {
   if (!s) return SFB_OK;
   if (s->has_fwd) cufftDestroy(s->fwd);
   if (s->has_inv) cufftDestroy(s->inv);
+  cg_release(s);
   void* bufs[] = {s->tbuf, s->work, s->rbuf, s->cbuf, s->cprime, s->dscr, s->lam[0], s->lam[1], s->lam[2],
                   s->up, s->lo, s->di, s->dxy, s->tmp, s->fft.tw_half, s->fft.tw_full,
                   s->fft.tw_ax[0], s->fft.tw_ax[1], s->fft.tw_ax[2]};
@@ -663,6 +680,7 @@ int sfb_project_launches(const sfb_solver* s, int mode) {
   if (mode == 3) return fused ? 2 : 3;  // sfb_slab_forward
   int n;
   if (s->fft.enabled) n = (s->plan->dim == 3 ? 5 : 3) + (fused ? 0 : 1);
+  else if (s->kind == SFB_SOLVER_CG) n = 1 + 4 + 7 * s->cg_iters;  // divergence, CG init, CG iterations
   else n = 2;  // divergence + eigenvalue scaling / tridiagonal (cuFFT transforms not counted)
   if (mode == 2) return n;
   return n + 2 + (mode == 1 ? 1 : 0);  // gradient subtract, velocity ghosts (+ pressure ghosts)

@@ -20,6 +20,11 @@ struct CT<float> {
 
 template <typename T>
 int solve_inplace(sfb_solver* s, T* buf, cudaStream_t st);
+// matrix-free CG (cg.cu)
+template <typename T>
+int cg_solve(sfb_solver* s, T* buf, cudaStream_t st);
+int cg_setup(sfb_solver* s);
+void cg_release(sfb_solver* s);
 }  // namespace sfb
 
 struct sfb_solver {
@@ -41,4 +46,10 @@ struct sfb_solver {
   bool slab = false;
   int n0g = 0, rank = 0, nranks = 1;
   void* tbuf = nullptr;      // transposed spectrum (n0 global, n1/P, nh)
+  // matrix-free CG (SFB_SOLVER_CG)
+  double cg_tol = 0.0, cg_wtot = 0.0;
+  int cg_max_iter = 0, cg_iters = 0, cg_nb = 0;
+  void *cg_x = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_ap = nullptr;
+  double *cg_part = nullptr, *cg_dsc = nullptr, *cg_hsc = nullptr;
+  std::vector<double> cg_hist;
 };

@@ -12,8 +12,9 @@ Backends (same duck-typed interface as the reference: ``kind``,
   weighted zero-mean gauge.  It solves exactly the system of the reference's
   ``DirectPoissonSolver`` (poisson.py:203-229), so ``make_solver("direct")``
   returns it on such grids.
-* ``cg``         -- not on the GPU path yet:
-  ``ConfigurationError``.
+* ``cg``         -- matrix-free conjugate gradient on the weighted operator
+  (poisson.py:232-308; csrc/cg.cu): any boundary conditions and stretching,
+  the reference's defaults, ``residual_history`` and ``ConvergenceError``.
 """
 
 import ctypes
@@ -23,7 +24,7 @@ import torch
 
 from . import _native as N
 from .bcs import BoundarySpec, Dirichlet
-from .errors import ConfigurationError
+from .errors import ConfigurationError, ConvergenceError
 from .fields import ScalarField
 from .operators import pressure_weights
 from .plan import get_plan, stream_ptr
@@ -121,9 +122,55 @@ class DirectPoissonSolver(ChannelPoissonSolver):
     kind = "direct"
 
 
-class CGPoissonSolver:
-    def __init__(self, *a, **k):
-        raise ConfigurationError("the CG pressure solver is not on the GPU path yet")
+class CGPoissonSolver(_GpuSolver):
+    """Matrix-free conjugate gradient on the weighted operator
+    (poisson.py:232-308): b = -W (rhs - wmean), CG on -W L with the weighted
+    mean of the iterate and the mean of the residual removed every step,
+    stop at |r| <= tol |b|."""
+
+    kind = "cg"
+    _native_kind = N.SFB_SOLVER_CG
+
+    def __init__(self, grid, bcs, tol=None, max_iter=None):
+        if tol is None:
+            tol = 1e-10 if np.dtype(grid.dtype) == np.float64 else 1e-5
+        if tol <= 0:
+            raise ValueError(f"tolerance must be positive, got {tol}")
+        n_dof = int(np.prod(grid.shape))
+        if max_iter is None:
+            max_iter = min(10000, 10 * int(np.ceil(n_dof ** (1.0 / grid.dim))) + 10)
+        super().__init__(grid, bcs)
+        self.tol = float(tol)
+        self.max_iter = int(max_iter)
+        N.call("sfb_cg_configure", self.handle, self.tol, self.max_iter)
+        self.residual_history = []
+
+    @property
+    def tolerance(self):
+        return self.tol
+
+    def _after_solve(self, failed=None):
+        """Pull the iteration count and residual history of the last solve;
+        attach them to a ConvergenceError."""
+        it = ctypes.c_int()
+        cnt = ctypes.c_int()
+        N.call("sfb_cg_info", self.handle, ctypes.byref(it), None, 0, ctypes.byref(cnt))
+        hist = (ctypes.c_double * max(cnt.value, 1))()
+        N.call("sfb_cg_info", self.handle, ctypes.byref(it), hist, cnt.value, ctypes.byref(cnt))
+        self.residual_history = list(hist[: cnt.value])
+        self.iterations = it.value if failed is None else self.max_iter
+        if failed is not None:
+            b = self.residual_history[0] if self.residual_history else 1.0
+            failed.residual = self.residual_history[-1] / b if b else None
+            failed.iterations = self.max_iter
+
+    def solve_interior(self, rhs, out):
+        try:
+            super().solve_interior(rhs, out)
+        except ConvergenceError as e:
+            self._after_solve(failed=e)
+            raise
+        self._after_solve()
 
 
 def make_solver(kind, grid, bcs, tol=None, max_iter=None):
@@ -156,9 +203,24 @@ def project_into(u, solver, bcs, t=0.0, scratch=None, p_div=None, p_out=None):
     s = _native_solver(solver, bcs)
     if p_out is None:
         p_out = ScalarField(u.grid)
-    N.call("sfb_project", s.handle, N.ptr3(u.u), p_out.data.data_ptr(), stream_ptr())
-    s.iterations = 1
+    call_solver(s, "sfb_project", s.handle, N.ptr3(u.u), p_out.data.data_ptr(), stream_ptr())
     return p_out
+
+
+def call_solver(s, name, *args):
+    """One native call that runs the solver; keeps the solver's iteration
+    bookkeeping (and a ConvergenceError's residual) up to date."""
+    after = getattr(s, "_after_solve", None)
+    try:
+        N.call(name, *args)
+    except ConvergenceError as e:
+        if after is not None:
+            after(failed=e)
+        raise
+    if after is not None:
+        after()
+    else:
+        s.iterations = 1
 
 
 def project(u, solver, bcs, t=0.0):

@@ -28,3 +28,17 @@ def obcs(g):
     """Periodic, or channel walls on the non-periodic axis (the fixtures'
     only two boundary layouts)."""
     return [("P", "P") if p else (("D", 0.0), ("D", 0.0)) for p in g.periodic]
+
+
+def _parse_side(txt):
+    if txt.startswith("Periodic"):
+        return "P"
+    if txt.startswith("Symmetric"):
+        return "S"
+    return ("D", float(txt.split("=")[1].rstrip(")")))
+
+
+def sides_bcs(case):
+    """Oracle BCs from a fixture's ``sides`` (repr strings of the reference's
+    Periodic / Dirichlet(values=v) / Symmetric)."""
+    return [tuple(_parse_side(str(t)) for t in sd) for sd in case["sides"]]

@@ -6,7 +6,7 @@ import math
 import numpy as np
 import pytest
 
-from _golden import load, obcs, ogrid, vel
+from _golden import load, obcs, ogrid, sides_bcs, vel
 from oracle import stagflow_np as O
 from oracle.channel_np import ChannelSolve
 
@@ -171,3 +171,28 @@ def test_known_answer_channel_from_rest():
     u1, _ = O.rk_step(g, bcs, ChannelSolve(g), u0, dt, O.SSP33, 0.0, (1.0, 0.0, 0.0))
     assert np.allclose(u1[0][g.udof(0)], dt, rtol=1e-12)
     assert np.max(np.abs(u1[1][g.udof(1)])) < 1e-14
+
+
+@pytest.mark.parametrize("name", ["cg3d_mixed", "cg2d_stretched"])
+def test_cg_solver_projection_and_step(name):
+    """CGSolve restates poisson.py:232-308 (and laplacian_apply poisson.py:43-68):
+    same iterations and residual history, same solution, projection and SSP33
+    step on a stretched grid with periodic, Dirichlet and symmetric sides."""
+    c = load(name)
+    g = ogrid(c)
+    d = g.dim
+    bcs = sides_bcs(c)
+    cg = O.CGSolve(g, bcs, max_iter=1000)
+    sol = cg(c["rhs"][g.pdof()])
+    assert cg.iterations == int(c["iterations"])
+    assert np.allclose(cg.residual_history, c["residual_history"], rtol=1e-12, atol=0)
+    assert _rel(sol, c["sol"][g.pdof()]) <= 1e-13
+    u = vel(c, "u", d)
+    p = O.project_into(g, bcs, cg, u)
+    for a in range(d):
+        assert _rel(u[a], c[f"uproj{a}"]) <= 1e-12
+    assert _rel(p, c["pproj"]) <= 1e-12
+    u1, p1 = O.rk_step(g, bcs, cg, vel(c, "uproj", d), float(c["dt"]), O.SSP33, float(c["nu"]))
+    for a in range(d):
+        assert _rel(u1[a], c[f"ssp33_u{a}"]) <= 1e-12
+    assert _rel(p1, c["ssp33_p"]) <= 1e-11
