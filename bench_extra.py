@@ -103,6 +103,33 @@ def case_solve(n, dtype):
     return {"case": f"spectral solve {n}^3 {dtype}", "ms": ms, "gb_moved_min": gbytes, "gbs": gbytes / (ms * 1e-3)}
 
 
+def case_cg(n=256):
+    """Matrix-free CG projection + SSP33 step on a tanh-stretched channel-like
+    grid (periodic x, walls y, symmetric/wall z): grids the FFT paths do not
+    cover."""
+    import numpy as np
+
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200.grid import tanh_grid, uniform_grid
+
+    g = P.Grid((uniform_grid(0.0, 2.0, n), tanh_grid(0.0, 1.0, n // 2, 1.6), tanh_grid(0.0, 0.7, n // 2, 1.2)),
+               (True, False, False))
+    bcs = P.BoundarySpec([(P.Periodic(), P.Periodic()), (P.Dirichlet(0.0), P.Dirichlet(0.0)),
+                          (P.Symmetric(), P.Dirichlet(0.0))])
+    solver = P.make_solver("cg", g, bcs, tol=1e-8, max_iter=20000)
+    setup = P.Setup(g, bcs, nu=1e-3, force=(1.0, 0.0, 0.0), solver=solver, method="ssp33")
+    rng = np.random.default_rng(0)
+    u0 = P.VelocityField(g)
+    for a in range(3):
+        u0.u[a].copy_(P.VelocityField(g, [rng.standard_normal(g.ext_shape) * 0.1 for _ in range(3)]).u[a])
+    P.project_into(u0, solver, bcs)
+    st = setup.new_state(u0=u0)
+    ms = _time(lambda: P.rk_step(st, 1e-4, P.SSP33, setup.solver, setup), 3, 1)
+    cells = int(np.prod(g.shape))
+    return {"case": f"SSP33 step, CG pressure (tol 1e-8), stretched {g.shape} periodic/wall/symmetric f64",
+            "ms": ms, "cg_iterations_last_solve": solver.iterations, "cell_updates_per_s": cells / (ms * 1e-3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default="step512,step512f32,step840f32,vjp512,channel")
@@ -118,6 +145,8 @@ def main():
             f32 = c.endswith("f32")
             n = int(c[5:-3] if f32 else c[5:])
             r = case_solve(n, "f32" if f32 else "f64")
+        elif c.startswith("cg"):
+            r = case_cg(int(c[2:]) if len(c) > 2 else 256)
         elif c == "channel":
             r = case_channel()
         else:
