@@ -313,9 +313,11 @@ def convection(g, u, out=None):
     return out
 
 
-def momentum_rhs(g, u, nu, force=None):
-    """operators.py:218-238 (no closure); ``force`` is a d-vector of
-    constants (operators.py:241-259 casts them to the grid dtype)."""
+def momentum_rhs(g, u, nu, force=None, closure=None):
+    """operators.py:218-238; ``force`` is a d-vector of constants
+    (operators.py:241-259 casts them to the grid dtype); ``closure`` is a
+    callable (g, u, out) that accumulates the eddy-stress term
+    (operators.py:236-237, oracle/les_np.py)."""
     out = convection(g, u)
     if nu != 0.0:
         diffusion(g, u, nu, out=out)
@@ -324,6 +326,8 @@ def momentum_rhs(g, u, nu, force=None):
             fa = g.dtype.type(force[a])
             if fa != 0.0:
                 out[a][g.udof(a)] += fa
+    if closure is not None:
+        closure(g, u, out)
     return out
 
 
@@ -538,7 +542,7 @@ def _axpy(g, dst, src, coef):
         dst[a][sl] += np.multiply(src[a][sl], coef)
 
 
-def rk_step(g, bcs, solve, u0, dt, tab, nu, force=None):
+def rk_step(g, bcs, solve, u0, dt, tab, nu, force=None, closure=None):
     """timestep.py:175-214; returns (u1, pressure).  ``u0`` must carry
     filled ghosts (the reference state always does)."""
     if dt <= 0:
@@ -553,7 +557,7 @@ def rk_step(g, bcs, solve, u0, dt, tab, nu, force=None):
                 if tab.a[j][l] != 0.0:
                     _axpy(g, y, ks[l], dt * tab.a[j][l])
             project_into(g, bcs, solve, y)
-        ks.append(momentum_rhs(g, y, nu, force))
+        ks.append(momentum_rhs(g, y, nu, force, closure))
     acc = [x.copy() for x in u0]
     for l in range(tab.stages):
         if tab.b[l] != 0.0:
@@ -834,7 +838,7 @@ def step_forward_tape(g, bcs, solve, u0, dt, tab, nu, force=None):
                         acc[a][sl] += (dt * tab.a[j][l]) * ks[l][a][sl]
             y = project_with_tape(g, bcs, solve, acc)
         stages.append(y)
-        ks.append(momentum_rhs(g, y, nu, force))
+        ks.append(momentum_rhs(g, y, nu, force, closure))
     acc = [x.copy() for x in u0]
     for a in range(g.dim):
         sl = g.udof(a)

@@ -225,6 +225,45 @@ def main():
         out["dt"] = 0.004
         save(name, **out)
 
+    # ---- LES closures (les.py): nu_t of every model, eddy-stress divergence,
+    # closure in the momentum RHS and in RK steps (periodic and channel walls)
+    from stagflow import les
+
+    def les_case(name, g, bcs, solver, u):
+        out = dict(grid_meta(g))
+        out.update(vel("u", u))
+        for kind in les.ClosureModel.KINDS[1:]:
+            out[f"nut_{kind}"] = les.ClosureModel(kind).nu_t(u).data.copy()
+        nut = les.ClosureModel("smagorinsky", c=0.3).nu_t(u)
+        out["nut_in"] = nut.data.copy()
+        out.update(vel("esd", les.eddy_stress_divergence(u, nut)))
+        cl = les.ClosureModel("vreman")
+        out.update(vel("rhs_cl", ops.momentum_rhs(u, 0.01, force=np.array([0.5] + [0.0] * (g.dim - 1)), closure=cl)))
+        for tag, tab, kind in (("ssp33", ts.SSP33, "wale"), ("rk4", rk4, "smagorinsky")):
+            setup = ts.Setup(g, bcs, nu=0.01, solver=solver, closure=les.ClosureModel(kind))
+            st = setup.new_state(u0=u)
+            st.workspace = ts.Workspace(g, tab.stages + 1)
+            ts.rk_step(st, 0.003, tab, setup.solver, setup)
+            out.update(vel(f"{tag}_u", st.u))
+            out[f"{tag}_p"] = st.pressure.data.copy()
+        st = ts.Setup(g, bcs, nu=0.01, solver=solver, closure=les.ClosureModel("qr"), dt_max=1.0).new_state(u0=u)
+        out["adaptive_dt"] = ts._adaptive_dt(st, ts.Setup(g, bcs, nu=0.01, solver=solver,
+                                                         closure=les.ClosureModel("qr"), dt_max=1.0))
+        save(name, **out)
+
+    for name, shape in (("les3d", (7, 6, 5)), ("les2d", (9, 8))):
+        rng = np.random.default_rng(21)
+        g = mkgrid(shape, True)
+        bcs = BoundarySpec.all_periodic(len(shape))
+        u = rvel(g, rng)
+        fill_ghosts_velocity(u, bcs)
+        les_case(name, g, bcs, poisson.make_solver("cg", g, bcs, tol=1e-13, max_iter=5000), u)
+    setup = cases.channel_setup(8, 6, 4, gamma=2.0, solver="direct")
+    g = setup.grid
+    u = setup.new_state().u.copy()
+    poisson.project_into(u, setup.solver, setup.bcs)
+    les_case("les_channel", g, setup.bcs, setup.solver, u)
+
     # ---- adjoint: project pullback and unrolled gradient (RK4, 1 and 2 steps)
     rng = np.random.default_rng(3)
     g = mkgrid((6, 5, 4), False)

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from _golden import load, obcs, ogrid, sides_bcs, vel
+from oracle import les_np as LES
 from oracle import stagflow_np as O
 from oracle.channel_np import ChannelSolve
 
@@ -196,3 +197,54 @@ def test_cg_solver_projection_and_step(name):
     for a in range(d):
         assert _rel(u1[a], c[f"ssp33_u{a}"]) <= 1e-12
     assert _rel(p1, c["ssp33_p"]) <= 1e-11
+
+
+LES_MODELS = ["smagorinsky", "vreman", "qr", "wale", "sigma", "s3pqr"]
+
+
+def _les_closure(kind):
+    def add(g, u, out):
+        LES.eddy_stress_divergence(g, u, _ext(g, LES.nu_t(g, u, kind)), out=out)
+
+    return add
+
+
+def _ext(g, interior):
+    f = g.zeros()
+    f[g.pdof()] = interior
+    return f
+
+
+@pytest.mark.parametrize("name", ["les3d", "les2d", "les_channel"])
+def test_les_closures(name):
+    """oracle/les_np.py restates les.py: every model's nu_t, the eddy-stress
+    divergence, the closure in momentum_rhs and in SSP33 / RK4 steps, the
+    closure-tightened adaptive step (timestep.py:259-270)."""
+    c = load(name)
+    g = ogrid(c)
+    d = g.dim
+    u = vel(c, "u", d)
+    for kind in LES_MODELS:
+        got = LES.nu_t(g, u, kind)
+        assert _rel(got, c[f"nut_{kind}"][g.pdof()]) <= (1e-14 if kind != "sigma" else 1e-12), kind
+    esd = LES.eddy_stress_divergence(g, u, c["nut_in"].copy())
+    for a in range(d):
+        assert _rel(esd[a], c[f"esd{a}"]) <= 1e-14
+    force = [0.5] + [0.0] * (d - 1)
+    rhs = O.momentum_rhs(g, u, 0.01, force, _les_closure("vreman"))
+    for a in range(d):
+        assert _rel(rhs[a], c[f"rhs_cl{a}"]) <= 1e-14
+    bcs = obcs(g)
+    if name == "les_channel":
+        solve = ChannelSolve(g)
+        tol = 1e-12
+    else:
+        solve = O.CGSolve(g, bcs, tol=1e-13, max_iter=5000)
+        tol = 1e-9
+    for tag, tab, kind in (("ssp33", O.SSP33, "wale"), ("rk4", O.RK4, "smagorinsky")):
+        u1, p1 = O.rk_step(g, bcs, solve, vel(c, "u", d), 0.003, tab, 0.01, None, _les_closure(kind))
+        for a in range(d):
+            assert _rel(u1[a], c[f"{tag}_u{a}"]) <= tol, (tag, a)
+    nut = LES.nu_t(g, u, "qr")
+    dt = O.cfl_dt(g, u, 0.01 + float(np.max(nut)), 0.85, 0.85)
+    assert abs(min(dt, 1.0) - float(c["adaptive_dt"])) <= 1e-15 * dt
