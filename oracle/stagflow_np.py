@@ -838,7 +838,7 @@ def step_forward_tape(g, bcs, solve, u0, dt, tab, nu, force=None):
                         acc[a][sl] += (dt * tab.a[j][l]) * ks[l][a][sl]
             y = project_with_tape(g, bcs, solve, acc)
         stages.append(y)
-        ks.append(momentum_rhs(g, y, nu, force, closure))
+        ks.append(momentum_rhs(g, y, nu, force))  # the tape excludes closures (adjoint.py:374)
     acc = [x.copy() for x in u0]
     for a in range(g.dim):
         sl = g.udof(a)
