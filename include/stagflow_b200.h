@@ -152,6 +152,18 @@ int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, v
  * the extended pressure), sfb_project_solve (2) or sfb_slab_forward (3). */
 int sfb_project_launches(const sfb_solver* s, int with_pressure);
 
+/* Eddy-viscosity closures (les.py:58-417).  kind: 1 smagorinsky, 2 vreman,
+ * 3 qr, 4 wale, 5 sigma, 6 s3pqr; c >= 0 the model constant, pexp the s3pqr
+ * exponent.  u needs filled ghosts; nu_t is written on the interior of the
+ * extended scalar nut (ghosts untouched). */
+int sfb_closure_nut(sfb_plan* plan, int kind, double c, double pexp, const void* const* u, void* nut, void* stream);
+/* out (+)= div(2 nu_t S) on the velocity DOFs (les.py:343-417); nut with
+ * filled ghosts (sfb_fill_ghosts_scalar), u with filled ghosts. */
+int sfb_eddy_stress_divergence(sfb_plan* plan, const void* const* u, const void* nut, void* const* out,
+                               int accumulate, void* stream);
+/* min and max over the interior of an extended scalar (synchronises). */
+int sfb_scalar_minmax(sfb_plan* plan, const void* f, double* mn, double* mx, void* stream);
+
 /* Slab-decomposed spectral solve (multi-GPU, axis 0 split over nranks; the
  * plan's axis 0 is SFB_BC_HALO).  One projection =
  *   sfb_slab_forward  : divergence -> R2C (axis 2) -> FFT axis 1   -> spec

@@ -121,6 +121,45 @@ def singular_values(A, extended=True):
     return s1, s2, s3
 
 
+def singular_values_invariant(A):
+    """Check for the product's sigma model (csrc/les.cu): the second
+    singular value from the characteristic invariants (no cancellation),
+    e2 + e3 = (I2 - I3/e1)/e1, e2 e3 = I3/e1, I2 = sum |c_i x c_j|^2, in
+    longdouble.  For nearly two-component gradients this is more accurate
+    than the closed form of les.py:122-148 (whose e2 = 3q - e1 - e3 cancels)."""
+    a = A.astype(np.longdouble)
+    ata = np.einsum("...ki,...kj->...ij", a, a)
+    e1, _ = _sym_eigs(ata)
+    det = np.abs(_det(a))
+    cols = np.swapaxes(a, -1, -2)
+    i2 = np.zeros(a.shape[:-2], dtype=np.longdouble)
+    for i in range(3):
+        for j in range(i + 1, 3):
+            cr = np.cross(cols[..., i, :], cols[..., j, :])
+            i2 = i2 + np.einsum("...k,...k->...", cr, cr)
+    ok = e1 > 0
+    e1s = np.where(ok, e1, 1.0)
+    p23 = det * det / e1s
+    s23 = np.maximum((i2 - p23) / e1s, 0.0)
+    e2 = np.where(ok, 0.5 * (s23 + np.sqrt(np.maximum(s23 * s23 - 4.0 * p23, 0.0))), 0.0)
+    s1 = np.sqrt(np.maximum(e1, 0.0)).astype(np.float64)
+    s2 = np.sqrt(np.maximum(e2, 0.0)).astype(np.float64)
+    det = det.astype(np.float64)
+    prod = s1 * s2
+    s3 = np.minimum(np.where(prod > 0.0, det / np.where(prod > 0.0, prod, 1.0), 0.0), s2)
+    return s1, s2, s3
+
+
+def nu_t_sigma_accurate(g, u, c=None):
+    """The sigma model with singular_values_invariant (see there)."""
+    c = float(MODEL_CONSTANTS["sigma"] if c is None else c)
+    A = gradient_tensor(g, u)
+    s1, s2, s3 = singular_values_invariant(A)
+    ok = s1 > 0
+    val = s3 * (s1 - s2) * (s2 - s3) / np.where(ok, s1 ** 2, 1.0)
+    return (c * filter_width(g)) ** 2 * np.where(ok, np.maximum(val, 0.0), 0.0)
+
+
 def filter_width(g):
     """les.py:297-305 ('geometric'): (prod of the cell widths)^(1/d)."""
     prod = np.ones((1,) * g.dim, dtype=g.dtype)

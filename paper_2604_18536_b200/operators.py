@@ -94,9 +94,8 @@ def constant_force(grid, force):
 
 
 def momentum_rhs(u, nu, force=None, closure=None, t=0.0, out=None, scratch=None):
-    """operators.py:218-238 (no closure support on the GPU path yet)."""
-    if closure is not None:
-        raise ConfigurationError("LES closures are not supported on the GPU path")
+    """operators.py:218-238: convection + diffusion + force in one kernel,
+    then the closure's eddy-stress term (operators.py:236-237)."""
     if nu < 0:
         raise ValueError(f"viscosity must be nonnegative, got {nu}")
     grid = u.grid
@@ -107,6 +106,8 @@ def momentum_rhs(u, nu, force=None, closure=None, t=0.0, out=None, scratch=None)
     if fv is not None:
         fp = (N.ctypes.c_double * 3)(*(fv + [0.0] * (3 - len(fv))))
     N.call("sfb_momentum_rhs", _plan(grid), N.ptr3(u.u), float(nu), fp, N.ptr3(out.u), stream_ptr())
+    if closure is not None:
+        closure.add_rhs(u, out, scratch)
     return out
 
 
