@@ -130,6 +130,22 @@ def case_cg(n=256):
             "ms": ms, "cg_iterations_last_solve": solver.iterations, "cell_updates_per_s": cells / (ms * 1e-3)}
 
 
+def case_les(nx=512, ny=256, nz=256, kind="smagorinsky"):
+    """Channel Re_tau=180 RK4 step with an LES closure (les.py): nu_t kernel +
+    eddy-stress divergence per stage on top of the RHS (generic k-register
+    path), FFT(x,z) x tridiagonal(y) pressure."""
+    import paper_2604_18536_b200 as P
+    from paper_2604_18536_b200 import cases
+
+    setup = cases.channel_setup(nx, ny, nz, gamma=2.0, solver="direct", method="rk4")
+    setup.closure = P.ClosureModel(kind)
+    st = setup.new_state()
+    P.project_into(st.u, setup.solver, setup.bcs)
+    ms = _time(lambda: P.rk_step(st, 1e-3, P.RK4, setup.solver, setup), 5, 2)
+    return {"case": f"channel {nx}x{ny}x{nz} f64 rk4 step with {kind} closure", "ms": ms,
+            "cell_updates_per_s": nx * ny * nz / (ms * 1e-3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default="step512,step512f32,step840f32,vjp512,channel")
@@ -145,6 +161,8 @@ def main():
             f32 = c.endswith("f32")
             n = int(c[5:-3] if f32 else c[5:])
             r = case_solve(n, "f32" if f32 else "f64")
+        elif c.startswith("les"):
+            r = case_les(kind=c[4:] if len(c) > 4 else "smagorinsky")
         elif c.startswith("cg"):
             r = case_cg(int(c[2:]) if len(c) > 2 else 256)
         elif c == "channel":
