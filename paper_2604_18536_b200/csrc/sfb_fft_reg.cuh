@@ -25,6 +25,17 @@
 
 #include <cstdlib>
 
+// minimum resident CTAs of the row kernels (register caps, 3 each): the
+// divergence-fused R2C at 3 CTAs/SM (96 registers, small spills) hides more
+// of its 11 scalar loads per point than 2 CTAs at 130 registers (5.17 vs
+// 5.48 ms at 840^3)
+#ifndef SFB_R2CDIV_MINB
+#define SFB_R2CDIV_MINB 3
+#endif
+#ifndef SFB_ROW_MINB
+#define SFB_ROW_MINB 3
+#endif
+
 namespace sfb {
 
 // W_N^j = exp(-2 pi i j / N) for sub-DFT sizes N <= 32 (index N*32 + j).
@@ -285,7 +296,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<
 // contiguous-axis real transforms, M = A*B complex points per row (N = 2M reals)
 // ---------------------------------------------------------------------------
 template <typename T, int A, int B>
-__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB)
     k_rfft_r2c(const T* __restrict__ in, typename CX<T>::t* __restrict__ out, long long rows, long long in_row,
                long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
   typedef typename CX<T>::t C;
@@ -358,7 +369,7 @@ __device__ __forceinline__ T div_at(const Geo<T>& G, const T* __restrict__ u0, c
 }
 
 template <typename T, int A, int B>
-__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_R2CDIV_MINB)
     k_rfft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, long long rows, long long out_row,
                    const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
   typedef typename CX<T>::t C;
@@ -426,7 +437,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
 }
 
 template <typename T, int A, int B>
-__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R)
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB)
     k_rfft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, long long rows, long long in_row,
                long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
   typedef typename CX<T>::t C;

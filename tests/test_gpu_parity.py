@@ -458,8 +458,9 @@ def test_errors_map_to_reference_exceptions(P):
         P.make_solver("spectral", g, bcs)
     with pytest.raises(ValueError):
         P.diffusion(P.VelocityField(g), -1.0)
+    assert P.make_solver("cg", g, bcs).kind == "cg"  # stretched periodic: the CG path (row f1)
     with pytest.raises(P.ConfigurationError):
-        P.make_solver("cg", g, bcs)
+        P.make_solver("nope", g, bcs)
     wall = P.BoundarySpec.channel()
     gw = P.Grid([P.uniform_grid(0, 1, 8), P.uniform_grid(0, 1, 6), P.uniform_grid(0, 1, 4)], (True, False, True))
     setup = P.Setup(gw, wall, nu=0.01, solver="direct", method="rk4")
