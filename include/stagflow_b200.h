@@ -166,16 +166,20 @@ int sfb_scalar_minmax(sfb_plan* plan, const void* f, double* mn, double* mx, voi
 
 /* Slab-decomposed spectral solve (multi-GPU, axis 0 split over nranks; the
  * plan's axis 0 is SFB_BC_HALO).  One projection =
- *   sfb_slab_forward  : divergence -> R2C (axis 2) -> FFT axis 1   -> spec
- *   caller            : all-to-all spec (m, n1, nh) -> trans (n0, n1/P, nh)
+ *   sfb_slab_forward  : divergence -> R2C (axis 2) -> FFT axis 1 -> xchg in the
+ *                       all-to-all send layout (P, m, n1/P, nh)  [P = 1: spec]
+ *   caller            : all-to-all xchg -> trans (n0, n1/P, nh)   [P = 1: none]
  *   sfb_slab_axis0    : FFT axis 0 -> 1/(Lambda N) -> inverse FFT axis 0 on trans
- *   caller            : all-to-all back trans -> spec
- *   sfb_slab_inverse  : inverse FFT axis 1 -> C2R -> local pressure (m planes)
+ *                       (trans is spec when P = 1)
+ *   caller            : all-to-all back trans -> xchg             [P = 1: none]
+ *   sfb_slab_inverse  : inverse FFT axis 1 (reading xchg) -> C2R -> local
+ *                       pressure (m planes)
  *   caller            : copy the next slab's first pressure plane into p_halo
  *   sfb_slab_correct  : u -= G p (uses p_halo), fill non-halo ghosts, p_ext
  * (poisson.py:167-200, 321-341 split at the two transposes.) */
 int sfb_slab_solver_create(sfb_plan* plan, int n0_global, int rank, int nranks, sfb_solver** out);
-int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** p_local, void** p_halo);
+/* xchg is NULL when nranks == 1 (no exchange; trans aliases spec). */
+int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** xchg, void** p_local, void** p_halo);
 int sfb_slab_forward(sfb_solver* s, void* const* u, void* stream);
 int sfb_slab_axis0(sfb_solver* s, void* stream);
 int sfb_slab_inverse(sfb_solver* s, void* stream);

@@ -540,8 +540,49 @@ template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, co
 
 // ---- slab-decomposed pieces (multi-GPU): F.n = {m local planes, n1, n2},
 // F.ax[0] is the global axis-0 length, F.sc.l1 offset to this rank's k1 chunk.
+// chunked exchange layout of the slab all-to-all: (P, m, c, nh), c = n1 / P;
+// element (q, i, r, k2) = k1 = q c + r of plane i
 template <typename T>
-int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u) {
+__global__ void k_chunk_permute(const typename CX<T>::t* __restrict__ nat, typename CX<T>::t* __restrict__ xch, int m,
+                                int n1, int c, int nh, int to_xchg) {
+  typedef typename CX<T>::t C;
+  const long long total = (long long)m * n1 * nh;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int k2 = (int)(t % nh);
+    const long long r0 = t / nh;
+    const int k1 = (int)(r0 % n1), i = (int)(r0 / n1);
+    const long long x = (((long long)(k1 / c) * m + i) * c + (k1 % c)) * nh + k2;
+    if (to_xchg) xch[x] = nat[t];
+    else ((C*)nat)[t] = xch[x];
+  }
+}
+
+template <typename T>
+static RegCall split_call(const FftSolve& F, int kind, const void* in, void* out, int m, int n1, int c, int nh) {
+  RegCall rc{};
+  rc.kind = kind;
+  rc.in = in;
+  rc.out = out;
+  rc.ncol = nh;
+  rc.nbatch = m;
+  rc.S = nh;  // the natural side's row stride
+  rc.map_c = c;
+  rc.map_sq = (long long)m * c * nh;
+  rc.map_s = nh;
+  if (kind == 6) {  // natural in, chunked out
+    rc.bstride_in = (long long)n1 * nh;
+    rc.bstride = (long long)c * nh;
+  } else {  // chunked in, natural out
+    rc.bstride_in = (long long)c * nh;
+    rc.bstride = (long long)n1 * nh;
+  }
+  rc.twL = F.tw_ax[1];
+  return rc;
+}
+
+template <typename T>
+int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u,
+                     void* xbuf, int nranks) {
   typedef typename CX<T>::t C;
   C* cbuf = (C*)cbuf_v;
   const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], nh = nlast / 2 + 1;
@@ -563,6 +604,18 @@ int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const 
   }
   if (rc) return rc;
   ScaleArgs none{};
+  if (xbuf && nranks > 1) {
+    // axis-1 FFT written straight into the all-to-all send layout
+    const int c = n1 / nranks;
+    if (F.reg_ax[1])
+      return reg_run<T>(SFB_REG(F, 1), split_call<T>(F, 6, cbuf, xbuf, m, n1, c, nh), st);
+    if ((rc = launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                                   (const C*)F.tw_ax[1], none, st, &F.tma_ax1, RegLen{})))
+      return rc;
+    k_chunk_permute<T><<<148 * 8, 256, 0, st>>>(cbuf, (C*)xbuf, m, n1, c, nh, 1);
+    SFB_LAUNCH_CHECK("slab pack");
+    return SFB_OK;
+  }
   return launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
                               (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
 }
@@ -575,24 +628,38 @@ int fft_slab_axis0(FftSolve& F, void* tbuf_v, int n1_chunk, cudaStream_t st) {
                               (const C*)F.tw_ax[0], F.sc, st, &F.tma_ax0, SFB_REG(F, 0));
 }
 template <typename T>
-int fft_slab_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st) {
+int fft_slab_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st, void* xbuf, int nranks) {
   typedef typename CX<T>::t C;
   C* cbuf = (C*)cbuf_v;
-  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], M = nlast / 2, nh = M + 1;
+  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], nh = nlast / 2 + 1;
   ScaleArgs none{};
-  int rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
-                                (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
+  int rc;
+  if (xbuf && nranks > 1) {
+    // inverse axis-1 FFT read straight from the all-to-all receive layout
+    const int c = n1 / nranks;
+    if (F.reg_ax[1]) {
+      rc = reg_run<T>(SFB_REG(F, 1), split_call<T>(F, 7, xbuf, cbuf, m, n1, c, nh), st);
+    } else {
+      k_chunk_permute<T><<<148 * 8, 256, 0, st>>>(cbuf, (C*)xbuf, m, n1, c, nh, 0);
+      SFB_LAUNCH_CHECK("slab unpack");
+      rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                                (const C*)F.tw_ax[1], none, st, &F.tma_ax1, RegLen{});
+    }
+  } else {
+    rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                              (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
+  }
   if (rc) return rc;
-  (void)M;
   return launch_c2r<T>(F, cbuf, rbuf, (long long)m * n1, st);
 }
-template int fft_slab_forward<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*,
-                                      const void* const*);
-template int fft_slab_forward<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*);
+template int fft_slab_forward<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*,
+                                      void*, int);
+template int fft_slab_forward<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*,
+                                     void*, int);
 template int fft_slab_axis0<double>(FftSolve&, void*, int, cudaStream_t);
 template int fft_slab_axis0<float>(FftSolve&, void*, int, cudaStream_t);
-template int fft_slab_inverse<double>(FftSolve&, void*, double*, cudaStream_t);
-template int fft_slab_inverse<float>(FftSolve&, void*, float*, cudaStream_t);
+template int fft_slab_inverse<double>(FftSolve&, void*, double*, cudaStream_t, void*, int);
+template int fft_slab_inverse<float>(FftSolve&, void*, float*, cudaStream_t, void*, int);
 
 template <typename T>
 int fft_set_smem_limits() {

@@ -642,7 +642,8 @@ int sfb_solver_destroy(sfb_solver* s) {
   if (s->has_fwd) cufftDestroy(s->fwd);
   if (s->has_inv) cufftDestroy(s->inv);
   cg_release(s);
-  void* bufs[] = {s->tbuf, s->work, s->rbuf, s->cbuf, s->cprime, s->dscr, s->lam[0], s->lam[1], s->lam[2],
+  if (s->tbuf == s->cbuf) s->tbuf = nullptr;  // P = 1 alias
+  void* bufs[] = {s->tbuf, s->xbuf, s->work, s->rbuf, s->cbuf, s->cprime, s->dscr, s->lam[0], s->lam[1], s->lam[2],
                   s->up, s->lo, s->di, s->dxy, s->tmp, s->fft.tw_half, s->fft.tw_full,
                   s->fft.tw_ax[0], s->fft.tw_ax[1], s->fft.tw_ax[2]};
   for (void* b : bufs)
@@ -729,7 +730,12 @@ int sfb_slab_solver_create(sfb_plan* p, int n0g, int rank, int nranks, sfb_solve
   FftSolve& F = s->fft;
   if ((rc = cuda_check(cudaMalloc(&s->rbuf, esz * (size_t)(m + 1) * n1 * n2), "cudaMalloc(rbuf)"))) goto bad;
   if ((rc = cuda_check(cudaMalloc(&s->cbuf, 2 * esz * ncomplex), "cudaMalloc(spec)"))) goto bad;
-  if ((rc = cuda_check(cudaMalloc(&s->tbuf, 2 * esz * ncomplex), "cudaMalloc(trans)"))) goto bad;
+  if (nranks > 1) {
+    if ((rc = cuda_check(cudaMalloc(&s->tbuf, 2 * esz * ncomplex), "cudaMalloc(trans)"))) goto bad;
+    if ((rc = cuda_check(cudaMalloc(&s->xbuf, 2 * esz * ncomplex), "cudaMalloc(exchange)"))) goto bad;
+  } else {
+    s->tbuf = s->cbuf;  // one rank: the axis-0 pass runs on the spectrum in place
+  }
   for (int a = 0; a < 3; ++a) {
     std::vector<double> lam(ng[a]);
     for (int k = 0; k < ng[a]; ++k) lam[k] = (2.0 * std::cos(2.0 * M_PI * k / ng[a]) - 2.0) / (h[a] * h[a]);
@@ -772,12 +778,13 @@ bad:
   return rc;
 }
 
-int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** p_local, void** p_halo) {
+int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** xchg, void** p_local, void** p_halo) {
   if (!s || !s->slab) return fail(SFB_EINVAL, "not a slab solver");
   sfb_plan* p = s->plan;
   const size_t esz = p->dtype == SFB_F64 ? 8 : 4;
   if (spec) *spec = s->cbuf;
   if (trans) *trans = s->tbuf;
+  if (xchg) *xchg = s->xbuf;
   if (p_local) *p_local = s->rbuf;
   if (p_halo) *p_halo = (char*)s->rbuf + esz * (size_t)p->n[0] * p->n[1] * p->n[2];
   return SFB_OK;
@@ -791,12 +798,12 @@ static int slab_forward(sfb_solver* s, void* const* u, cudaStream_t st) {
   sfb_plan* p = s->plan;
   const Geo<T>& G = geo<T>(p);
   if (fft_divfuse_ok<T>(s->fft, G))
-    return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st, &G, (const void* const*)u);
+    return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st, &G, (const void* const*)u, s->xbuf, s->nranks);
   CV<T> C;
   for (int a = 0; a < 3; ++a) C.c[a] = (const T*)u[a];
   int rc = launch_div<T>(G, C, (T*)s->rbuf, st);
   if (rc) return rc;
-  return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st);
+  return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st, nullptr, nullptr, s->xbuf, s->nranks);
 }
 
 template <typename T>
@@ -832,8 +839,9 @@ int sfb_slab_axis0(sfb_solver* s, void* stream) {
 
 int sfb_slab_inverse(sfb_solver* s, void* stream) {
   if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
-  return s->plan->dtype == SFB_F64 ? fft_slab_inverse<double>(s->fft, s->cbuf, (double*)s->rbuf, (cudaStream_t)stream)
-                                   : fft_slab_inverse<float>(s->fft, s->cbuf, (float*)s->rbuf, (cudaStream_t)stream);
+  return s->plan->dtype == SFB_F64
+             ? fft_slab_inverse<double>(s->fft, s->cbuf, (double*)s->rbuf, (cudaStream_t)stream, s->xbuf, s->nranks)
+             : fft_slab_inverse<float>(s->fft, s->cbuf, (float*)s->rbuf, (cudaStream_t)stream, s->xbuf, s->nranks);
 }
 
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream) {

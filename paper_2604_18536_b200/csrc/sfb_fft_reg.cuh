@@ -192,13 +192,23 @@ __device__ __forceinline__ C tw_mul(C x, const C* lo, const C* hi, int m) {
 // Exchange layout: slot (n2, k1, w) at n2*XS + k1*W + w, XS padded so the
 // rows of one 128-byte shared-memory wavefront fall in distinct banks.
 // ---------------------------------------------------------------------------
+// MODE 3 / 4: forward / inverse out of place, with the transform rows of the
+// output (3) or input (4) placed by a chunked map (slab all-to-all layout,
+// distributed.py): row r at (r / mp.c) * mp.sq + (r % mp.c) * mp.s
+struct RowSplit {
+  int c;
+  long long sq, s;
+};
+
 template <typename T, int A, int B, int MODE>
 __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<typename CX<T>::t, A, B>::MINB_S)
-    k_rfft_strided(typename CX<T>::t* __restrict__ data, long long S, int ncol, long long bstride,
-                   const typename CX<T>::t* __restrict__ twL, ScaleArgs sc) {
+    k_rfft_strided(const typename CX<T>::t* __restrict__ in, typename CX<T>::t* __restrict__ data, long long S,
+                   int ncol, long long bin, long long bstride, RowSplit mp, const typename CX<T>::t* __restrict__ twL,
+                   ScaleArgs sc) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
   constexpr int W = RG::W, XS = RG::XS;
+  constexpr bool MAP_OUT = MODE == 3, MAP_IN = MODE == 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* buf = reinterpret_cast<C*>(smem_raw);
   C* twlo = buf + B * XS;
@@ -207,14 +217,21 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<
   const int col = blockIdx.x * W + w;
   const bool ok = col < ncol;
   C* base = data + (long long)blockIdx.y * bstride + (ok ? col : 0);
-  constexpr bool INV1 = MODE == 1;
+  const C* ibase = in + (long long)blockIdx.y * bin + (ok ? col : 0);
+  constexpr bool INV1 = MODE == 1 || MODE == 4;
   const long long gs = (long long)B * S;
+  auto mapped = [&](int r) -> long long { return (long long)(r / mp.c) * mp.sq + (long long)(r % mp.c) * mp.s; };
   C v[A > B ? A : B];
   // phase 1: thread n2 = t loads its column straight into registers
   if (t < B) {
-    const C* g = base + (long long)t * S;
+    if constexpr (MAP_IN) {
 #pragma unroll
-    for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(g + n1 * gs) : czero<C>();
+      for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(ibase + mapped(B * n1 + t)) : czero<C>();
+    } else {
+      const C* g = ibase + (long long)t * S;
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(g + n1 * gs) : czero<C>();
+    }
   }
   tw_fill(twlo, twhi, twL, A * B);
   __syncthreads();
@@ -273,7 +290,8 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<
       }
     } else if (ok) {
 #pragma unroll
-      for (int k2 = 0; k2 < B; ++k2) __stcs(base + (long long)(k1 + A * k2) * S, v[k2]);
+      for (int k2 = 0; k2 < B; ++k2)
+        __stcs(base + (MAP_OUT ? mapped(k1 + A * k2) : (long long)(k1 + A * k2) * S), v[k2]);
     }
   }
   if constexpr (MODE == 2) {
@@ -503,12 +521,16 @@ struct RegLen {
   int L = 0, A = 0, B = 0;
   bool ok = false;
 };
-// one launch request: kind 0/1/2 strided MODE, 3 R2C, 4 C2R, 5 R2C of the divergence
+// one launch request: kind 0/1/2 strided MODE, 3 R2C, 4 C2R, 5 R2C of the divergence,
+// 6 / 7 strided forward / inverse out of place with the output / input rows
+// split into chunks (map_c rows per chunk, chunk stride map_sq, row stride map_s)
 struct RegCall {
   int kind;
   const void* in;
   void* out;  // strided: in == out (in place)
   long long S, bstride, rows, in_row, out_row;
+  long long bstride_in, map_sq, map_s;
+  int map_c;
   int ncol, nbatch;
   const void* twL;  // plain table exp(-2 pi i m / L), m < L
   const void* twN;  // real trick: exp(-2 pi i k / 2L), k <= L
@@ -540,19 +562,31 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
+    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
+    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
     cudaFuncSetAttribute(k_rfft_r2c<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
     cudaFuncSetAttribute(k_rfft_c2r<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
     cudaFuncSetAttribute(k_rfft_r2c_div<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
     attr = true;
   }
-  if (c.kind <= 2) {
+  if (c.kind <= 2 || c.kind == 6 || c.kind == 7) {
     dim3 grid((c.ncol + RG::W - 1) / RG::W, c.nbatch);
     C* d = (C*)c.out;
+    const C* src = c.in ? (const C*)c.in : d;
+    const long long bin = c.in ? c.bstride_in : c.bstride;
+    const RowSplit mp{c.map_c > 0 ? c.map_c : 1, c.map_sq, c.map_s};
     const C* tw = (const C*)c.twL;
-    if (c.kind == 0) k_rfft_strided<T, A, B, 0><<<grid, RG::NT_S, RG::SMEM_S, st>>>(d, c.S, c.ncol, c.bstride, tw, c.sc);
-    else if (c.kind == 1)
-      k_rfft_strided<T, A, B, 1><<<grid, RG::NT_S, RG::SMEM_S, st>>>(d, c.S, c.ncol, c.bstride, tw, c.sc);
-    else k_rfft_strided<T, A, B, 2><<<grid, RG::NT_S, RG::SMEM_S, st>>>(d, c.S, c.ncol, c.bstride, tw, c.sc);
+#define SFB_STRIDED(M)                                                                                     \
+  k_rfft_strided<T, A, B, M><<<grid, RG::NT_S, RG::SMEM_S, st>>>(src, d, c.S, c.ncol, bin, c.bstride, mp, tw, \
+                                                                 c.sc)
+    switch (c.kind) {
+      case 0: SFB_STRIDED(0); break;
+      case 1: SFB_STRIDED(1); break;
+      case 2: SFB_STRIDED(2); break;
+      case 6: SFB_STRIDED(3); break;
+      default: SFB_STRIDED(4); break;
+    }
+#undef SFB_STRIDED
   } else {
     const unsigned nb = (unsigned)((c.rows + RG::RP - 1) / RG::RP);
     if (c.kind == 3)

@@ -45,7 +45,8 @@ struct sfb_solver {
   // slab decomposition (multi-GPU)
   bool slab = false;
   int n0g = 0, rank = 0, nranks = 1;
-  void* tbuf = nullptr;      // transposed spectrum (n0 global, n1/P, nh)
+  void* tbuf = nullptr;      // transposed spectrum (n0 global, n1/P, nh); aliases cbuf when P = 1
+  void* xbuf = nullptr;      // all-to-all send / receive buffer (P, m, n1/P, nh), P > 1
   // matrix-free CG (SFB_SOLVER_CG)
   double cg_tol = 0.0, cg_wtot = 0.0;
   int cg_max_iter = 0, cg_iters = 0, cg_nb = 0;

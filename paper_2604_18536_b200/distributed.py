@@ -168,12 +168,17 @@ class CudaSlabBackend:
         h = ctypes.c_void_p()
         N.call("sfb_slab_solver_create", self.plan.handle, n0, lay.rank, lay.size, ctypes.byref(h))
         self.handle = h
-        spec, trans, pl, ph = (ctypes.c_void_p() for _ in range(4))
-        N.call("sfb_slab_buffers", h, ctypes.byref(spec), ctypes.byref(trans), ctypes.byref(pl), ctypes.byref(ph))
+        spec, trans, xchg, pl, ph = (ctypes.c_void_p() for _ in range(5))
+        N.call("sfb_slab_buffers", h, ctypes.byref(spec), ctypes.byref(trans), ctypes.byref(xchg), ctypes.byref(pl),
+               ctypes.byref(ph))
         ts = "<f8" if g.dtype == np.float64 else "<f4"
         m, nh = lay.m, n2 // 2 + 1
+        P = lay.size
         self.spec = torch.as_tensor(_DevBuf(spec.value, (m, n1, nh, 2), ts), device="cuda")
-        self.trans = torch.as_tensor(_DevBuf(trans.value, (n0, n1 // lay.size, nh, 2), ts), device="cuda")
+        self.trans = torch.as_tensor(_DevBuf(trans.value, (n0, n1 // P, nh, 2), ts), device="cuda")
+        # all-to-all send / receive buffer in the chunked layout (P, m, n1/P, nh)
+        self.xchg = (torch.as_tensor(_DevBuf(xchg.value, (P, m, n1 // P, nh, 2), ts), device="cuda")
+                     if P > 1 else None)
         self.p_local = torch.as_tensor(_DevBuf(pl.value, (m, n1, n2), ts), device="cuda")
         self.p_halo = torch.as_tensor(_DevBuf(ph.value, (n1, n2), ts), device="cuda")
 
@@ -243,15 +248,15 @@ class CudaSlabBackend:
 # orchestration (backend-agnostic)
 # ---------------------------------------------------------------------------
 class SlabProjector:
+    """One projection of the slab-decomposed field.  The backend's forward
+    transform writes the spectrum straight into the all-to-all send layout
+    ``xchg`` = (P, m, n1/P, nh) (chunk q = the k1 range of rank q) and its
+    inverse reads the receive layout, so the exchange needs no packing copies;
+    with one rank there is no exchange at all."""
+
     def __init__(self, backend, comm):
         self.b = backend
         self.comm = comm
-        lay = comm.layout
-        sp = backend.spec
-        m, n1, nh = sp.shape[0], sp.shape[1], sp.shape[2]
-        P = lay.size
-        self.sendbuf = torch.empty((P, m, n1 // P, nh, 2), dtype=sp.dtype, device=sp.device)
-        self.recvbuf = torch.empty_like(self.sendbuf)
 
     def project(self, u, p_ext=None):
         b, comm = self.b, self.comm
@@ -259,15 +264,15 @@ class SlabProjector:
         P, m = lay.size, lay.m
         comm.halo(u.u)
         b.forward(u)
-        sp = b.spec
-        n1, nh = sp.shape[1], sp.shape[2]
-        # pack (m, n1, nh) -> (P, m, n1/P, nh): chunk q goes to rank q
-        self.sendbuf.copy_(sp.view(m, P, n1 // P, nh, 2).permute(1, 0, 2, 3, 4))
-        # received chunks are ordered by source rank = global plane order
-        comm.all_to_all(b.trans.view(P, m, n1 // P, nh, 2), self.sendbuf)
-        b.axis0()
-        comm.all_to_all(self.recvbuf, b.trans.view(P, m, n1 // P, nh, 2))
-        sp.view(m, P, n1 // P, nh, 2).copy_(self.recvbuf.permute(1, 0, 2, 3, 4))
+        if P > 1:
+            c = b.trans.shape[1]
+            tv = b.trans.view(P, m, c, b.trans.shape[2], 2)
+            # received chunks are ordered by source rank = global plane order
+            comm.all_to_all(tv, b.xchg)
+            b.axis0()
+            comm.all_to_all(b.xchg, tv)
+        else:
+            b.axis0()
         b.inverse()
         comm.plane_from_next(b.p_local[0], b.p_halo)
         b.correct(u, p_ext)

@@ -1,2 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -2
-timeout 300 python bench.py --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('step', d['ms_per_step'], d['roofline']['frac'])"
+timeout 300 python -m pytest tests/test_distributed_gpu.py -q 2>&1 | tail -2
+timeout 300 python bench.py --slab --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('slab', d['ms_per_step'], d['gpu_launches'])"

@@ -33,7 +33,9 @@ class CpuSlabBackend:
         nh = self.n2 // 2 + 1
         P = layout.size
         self.spec = torch.zeros((m, self.n1, nh, 2), dtype=torch.float64)
-        self.trans = torch.zeros((self.n0, self.n1 // P, nh, 2), dtype=torch.float64)
+        # one rank: the axis-0 pass works on the spectrum itself (no exchange)
+        self.trans = torch.zeros((self.n0, self.n1 // P, nh, 2), dtype=torch.float64) if P > 1 else self.spec
+        self.xchg = torch.zeros((P, m, self.n1 // P, nh, 2), dtype=torch.float64) if P > 1 else None
         self.p_local = torch.zeros((m, self.n1, self.n2), dtype=torch.float64)
         self.p_halo = torch.zeros((self.n1, self.n2), dtype=torch.float64)
         lam = []
@@ -84,6 +86,10 @@ class CpuSlabBackend:
         div = O.divergence(self.og, arrs)[self.og.pdof()]
         s = np.fft.fft(np.fft.rfft(div, axis=2), axis=1)
         self.spec.copy_(torch.view_as_real(torch.from_numpy(s)))
+        if self.xchg is not None:
+            P, m = self.lay.size, self.lay.m
+            c = self.n1 // P
+            self.xchg.copy_(self.spec.view(m, P, c, -1, 2).permute(1, 0, 2, 3, 4))
 
     def axis0(self):
         t = torch.view_as_complex(self.trans).numpy()
@@ -101,6 +107,10 @@ class CpuSlabBackend:
         self.trans.copy_(torch.view_as_real(torch.from_numpy(np.fft.ifft(f, axis=0))))
 
     def inverse(self):
+        if self.xchg is not None:
+            P, m = self.lay.size, self.lay.m
+            c = self.n1 // P
+            self.spec.view(m, P, c, -1, 2).copy_(self.xchg.permute(1, 0, 2, 3, 4))
         s = torch.view_as_complex(self.spec).numpy()
         p = np.fft.irfft(np.fft.ifft(s, axis=1), n=self.n2, axis=2)
         self.p_local.copy_(torch.from_numpy(np.ascontiguousarray(p)))
