@@ -178,8 +178,11 @@ int sfb_scalar_minmax(sfb_plan* plan, const void* f, double* mn, double* mx, voi
  *   sfb_slab_correct  : u -= G p (uses p_halo), fill non-halo ghosts, p_ext
  * (poisson.py:167-200, 321-341 split at the two transposes.) */
 int sfb_slab_solver_create(sfb_plan* plan, int n0_global, int rank, int nranks, sfb_solver** out);
-/* xchg is NULL when nranks == 1 (no exchange; trans aliases spec). */
-int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** xchg, void** p_local, void** p_halo);
+/* xchg is NULL when nranks == 1 (no exchange; trans aliases spec).  p_slab:
+ * the slab pressure (m + 3 planes: prev's last, the m local planes = p_local,
+ * next's first = p_halo, next's second), the p_int of an on-the-fly stage. */
+int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** xchg, void** p_slab, void** p_local,
+                     void** p_halo);
 int sfb_slab_forward(sfb_solver* s, void* const* u, void* stream);
 int sfb_slab_axis0(sfb_solver* s, void* stream);
 int sfb_slab_inverse(sfb_solver* s, void* stream);

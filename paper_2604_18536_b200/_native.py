@@ -86,7 +86,7 @@ _SIGS = {
     "sfb_project_launches": [vp, ctypes.c_int],
     "sfb_slab_solver_create": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
     "sfb_slab_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
-                         ctypes.POINTER(vp)],
+                         ctypes.POINTER(vp), ctypes.POINTER(vp)],
     "sfb_slab_forward": [vp, VP3, vp],
     "sfb_slab_axis0": [vp, vp],
     "sfb_slab_inverse": [vp, vp],

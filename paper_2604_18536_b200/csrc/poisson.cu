@@ -728,7 +728,8 @@ int sfb_slab_solver_create(sfb_plan* p, int n0g, int rank, int nranks, sfb_solve
   double h[3] = {p->width0[0], p->width0[1], p->width0[2]};
   int ng[3] = {n0g, n1, n2};
   FftSolve& F = s->fft;
-  if ((rc = cuda_check(cudaMalloc(&s->rbuf, esz * (size_t)(m + 1) * n1 * n2), "cudaMalloc(rbuf)"))) goto bad;
+  // pressure planes [prev's last | m local | next's first two] (ext indices 0..m+2)
+  if ((rc = cuda_check(cudaMalloc(&s->rbuf, esz * (size_t)(m + 3) * n1 * n2), "cudaMalloc(rbuf)"))) goto bad;
   if ((rc = cuda_check(cudaMalloc(&s->cbuf, 2 * esz * ncomplex), "cudaMalloc(spec)"))) goto bad;
   if (nranks > 1) {
     if ((rc = cuda_check(cudaMalloc(&s->tbuf, 2 * esz * ncomplex), "cudaMalloc(trans)"))) goto bad;
@@ -778,32 +779,42 @@ bad:
   return rc;
 }
 
-int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** xchg, void** p_local, void** p_halo) {
+int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** xchg, void** p_slab, void** p_local,
+                     void** p_halo) {
   if (!s || !s->slab) return fail(SFB_EINVAL, "not a slab solver");
   sfb_plan* p = s->plan;
   const size_t esz = p->dtype == SFB_F64 ? 8 : 4;
   if (spec) *spec = s->cbuf;
   if (trans) *trans = s->tbuf;
   if (xchg) *xchg = s->xbuf;
-  if (p_local) *p_local = s->rbuf;
-  if (p_halo) *p_halo = (char*)s->rbuf + esz * (size_t)p->n[0] * p->n[1] * p->n[2];
+  const size_t plane = esz * (size_t)p->n[1] * p->n[2];
+  if (p_slab) *p_slab = s->rbuf;
+  if (p_local) *p_local = (char*)s->rbuf + plane;
+  if (p_halo) *p_halo = (char*)s->rbuf + plane * (1 + (size_t)p->n[0]);
   return SFB_OK;
 }
 
 }  // extern "C"
 
 namespace sfb {
+// the local pressure planes start one plane into the slab pressure buffer
+template <typename T>
+static T* slab_local(sfb_solver* s) {
+  return (T*)s->rbuf + (size_t)s->plan->n[1] * s->plan->n[2];
+}
+
 template <typename T>
 static int slab_forward(sfb_solver* s, void* const* u, cudaStream_t st) {
   sfb_plan* p = s->plan;
   const Geo<T>& G = geo<T>(p);
   if (fft_divfuse_ok<T>(s->fft, G))
-    return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st, &G, (const void* const*)u, s->xbuf, s->nranks);
+    return fft_slab_forward<T>(s->fft, slab_local<T>(s), s->cbuf, st, &G, (const void* const*)u, s->xbuf,
+                               s->nranks);
   CV<T> C;
   for (int a = 0; a < 3; ++a) C.c[a] = (const T*)u[a];
-  int rc = launch_div<T>(G, C, (T*)s->rbuf, st);
+  int rc = launch_div<T>(G, C, slab_local<T>(s), st);
   if (rc) return rc;
-  return fft_slab_forward<T>(s->fft, (T*)s->rbuf, s->cbuf, st, nullptr, nullptr, s->xbuf, s->nranks);
+  return fft_slab_forward<T>(s->fft, slab_local<T>(s), s->cbuf, st, nullptr, nullptr, s->xbuf, s->nranks);
 }
 
 template <typename T>
@@ -813,7 +824,7 @@ static int slab_correct(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t
   MV<T> U;
   for (int a = 0; a < 3; ++a) U.c[a] = (T*)u[a];
   Box B = int_box(G);
-  int rc = launch_grad<T>(G, (const T*)s->rbuf, U, (T*)p_ext, st);
+  int rc = launch_grad<T>(G, (const T*)slab_local<T>(s), U, (T*)p_ext, st);
   if (rc) return rc;
   rc = launch_planes<T>(G, U, 3, 0, st);
   if (rc) return rc;
@@ -840,8 +851,10 @@ int sfb_slab_axis0(sfb_solver* s, void* stream) {
 int sfb_slab_inverse(sfb_solver* s, void* stream) {
   if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
   return s->plan->dtype == SFB_F64
-             ? fft_slab_inverse<double>(s->fft, s->cbuf, (double*)s->rbuf, (cudaStream_t)stream, s->xbuf, s->nranks)
-             : fft_slab_inverse<float>(s->fft, s->cbuf, (float*)s->rbuf, (cudaStream_t)stream, s->xbuf, s->nranks);
+             ? fft_slab_inverse<double>(s->fft, s->cbuf, slab_local<double>(s), (cudaStream_t)stream, s->xbuf,
+                                        s->nranks)
+             : fft_slab_inverse<float>(s->fft, s->cbuf, slab_local<float>(s), (cudaStream_t)stream, s->xbuf,
+                                       s->nranks);
 }
 
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream) {

@@ -148,10 +148,13 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
     }
   }
   const long long ps0 = (long long)n1 * n2;
+  // slab (halo axis 0): y ghost planes exchanged, pressure planes 0..m+2 stored
+  // (sfb_slab_buffers p_slab); otherwise periodic wrap into the n0 planes
+  const bool h0 = G.halo[0] != 0;
   auto load_p = [&](int ip) {
     if constexpr (PROJ) {
       T* dst = pring + (ip & (kPRing - 1)) * PPS + tid;
-      const long long base = (long long)(wrap1(ip, n0) - 1) * ps0;
+      const long long base = (long long)(h0 ? ip : wrap1(ip, n0) - 1) * ps0;
 #pragma unroll
       for (int q = 0; q < NQP; ++q)
         if (q < NQP - 1 || tid + q * NTH < PPS) cp_async_val(dst + q * NTH, psrc[q] + (pok[q] ? base : 0), pok[q]);
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   auto load_plane = [&](int ip, int slot, bool with_p = true) {
     if (ip < 0 || ip >= G.E[0]) return;
     T* dst = ring + slot * NE + tid;
-    const long long base = (long long)(PROJ ? wrap1(ip, n0) : ip) * s0;
+    const long long base = (long long)(PROJ && !h0 ? wrap1(ip, n0) : ip) * s0;
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
       if (q < NQ - 1 || tid + q * NTH < NE) cp_async_val(dst + q * NTH, fsrc[q] + (fok[q] ? base : 0), fok[q]);
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
       T* ys = ring + slot * NE;
       const T* pc = pring + (ip & (kPRing - 1)) * PPS;
       const T* pn = pring + ((ip + 1) & (kPRing - 1)) * PPS;
-      const T r0 = tab(G, 0, T_RDU, wrap1(ip, n0));
+      const T r0 = tab(G, 0, T_RDU, h0 ? ip : wrap1(ip, n0));
 #pragma unroll
       for (int q = 0; q < NR; ++q) {
         const int r = tid + q * NTH;
@@ -377,8 +380,8 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
   A.has_next = a->y_next[0] != nullptr;
   A.s_from_u0 = a->s_in[0] == nullptr;
   A.p_int = (const T*)a->p_int;
-  if (A.p_int && !(G.dim == 3 && p->all_periodic && !G.halo[0]))
-    return fail(SFB_ECONFIG, "on-the-fly projection needs an all-periodic 3D plan");
+  if (A.p_int && !(G.dim == 3 && G.per[0] && G.per[1] && G.per[2] && !G.halo[1] && !G.halo[2]))
+    return fail(SFB_ECONFIG, "on-the-fly projection needs a periodic (or z-slab) 3D plan");
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
   if (G.dim == 3 && (!getenv("SFB_STAGE_GENERIC") || A.p_int)) {

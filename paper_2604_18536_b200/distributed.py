@@ -117,6 +117,9 @@ class Comm:
     def plane_from_next(self, send_plane, recv_plane):
         self._send_recv(send_plane, recv_plane, self.layout.prev, self.layout.next)
 
+    def plane_from_prev(self, send_plane, recv_plane):
+        self._send_recv(send_plane, recv_plane, self.layout.next, self.layout.prev)
+
     def all_to_all(self, out, inp):
         if self.layout.size == 1:
             out.copy_(inp)
@@ -168,9 +171,9 @@ class CudaSlabBackend:
         h = ctypes.c_void_p()
         N.call("sfb_slab_solver_create", self.plan.handle, n0, lay.rank, lay.size, ctypes.byref(h))
         self.handle = h
-        spec, trans, xchg, pl, ph = (ctypes.c_void_p() for _ in range(5))
-        N.call("sfb_slab_buffers", h, ctypes.byref(spec), ctypes.byref(trans), ctypes.byref(xchg), ctypes.byref(pl),
-               ctypes.byref(ph))
+        spec, trans, xchg, ps, pl, ph = (ctypes.c_void_p() for _ in range(6))
+        N.call("sfb_slab_buffers", h, ctypes.byref(spec), ctypes.byref(trans), ctypes.byref(xchg), ctypes.byref(ps),
+               ctypes.byref(pl), ctypes.byref(ph))
         ts = "<f8" if g.dtype == np.float64 else "<f4"
         m, nh = lay.m, n2 // 2 + 1
         P = lay.size
@@ -179,8 +182,10 @@ class CudaSlabBackend:
         # all-to-all send / receive buffer in the chunked layout (P, m, n1/P, nh)
         self.xchg = (torch.as_tensor(_DevBuf(xchg.value, (P, m, n1 // P, nh, 2), ts), device="cuda")
                      if P > 1 else None)
-        self.p_local = torch.as_tensor(_DevBuf(pl.value, (m, n1, n2), ts), device="cuda")
-        self.p_halo = torch.as_tensor(_DevBuf(ph.value, (n1, n2), ts), device="cuda")
+        # slab pressure: [prev's last | m local | next's first two] planes
+        self.p_slab = torch.as_tensor(_DevBuf(ps.value, (m + 3, n1, n2), ts), device="cuda")
+        self.p_local = self.p_slab[1:m + 1]
+        self.p_halo = self.p_slab[m + 1]
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -193,8 +198,9 @@ class CudaSlabBackend:
     def _sp(self):
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
-    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0):
+    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0, p_slab=None):
         a = N.StageArgs()
+        a.p_int = None if p_slab is None else p_slab.data_ptr()
         a.y = N.ptr3(y.u)
         a.u0 = N.ptr3(u0.u if u0 is not None else [None] * 3)
         a.s_in = N.ptr3(s_in.u if s_in is not None else [None] * 3)
@@ -212,6 +218,7 @@ class CudaSlabBackend:
         nfield = 1 + (s_out is not None) + (y_next is not None)
         nfield += (u0 is not None and u0 is not y and (y_next is not None or (s_out is not None and s_in is None)))
         nfield += (s_in is not None and s_out is not None)
+        nfield += (1.0 / 3.0) if p_slab is not None else 0.0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         N.call("sfb_rk_stage", self.plan.handle, ctypes.byref(a), self._sp())
@@ -258,7 +265,7 @@ class SlabProjector:
         self.b = backend
         self.comm = comm
 
-    def project(self, u, p_ext=None):
+    def _solve(self, u):
         b, comm = self.b, self.comm
         lay = comm.layout
         P, m = lay.size, lay.m
@@ -274,11 +281,30 @@ class SlabProjector:
         else:
             b.axis0()
         b.inverse()
+
+    def project(self, u, p_ext=None):
+        """Full projection (poisson.py:321-341) of the slab field."""
+        b, comm = self.b, self.comm
+        self._solve(u)
         comm.plane_from_next(b.p_local[0], b.p_halo)
         b.correct(u, p_ext)
         comm.halo(u.u)
         if p_ext is not None:
             comm.halo([p_ext.data])
+
+    def project_solve(self, u):
+        """Projection split at the gradient subtract (timestep._project_solve):
+        u keeps its exchanged (unprojected) ghost planes, the slab pressure
+        gets the neighbours' planes the next stage kernel's y - G p needs
+        (prev's last, next's first two); returns it."""
+        b, comm = self.b, self.comm
+        m = comm.layout.m
+        self._solve(u)
+        ps = b.p_slab
+        comm.plane_from_next(ps[1], ps[m + 1])
+        comm.plane_from_next(ps[2], ps[m + 2])
+        comm.plane_from_prev(ps[m], ps[0])
+        return ps
 
 
 class SlabState:
@@ -292,7 +318,8 @@ class SlabState:
 
 class SlabSimulation:
     """RK4 on a slab-decomposed periodic box (the fused 4-register scheme of
-    timestep.rk_step, with the slab projector between stages)."""
+    timestep.rk_step, with the slab projector between stages; intermediate
+    projections hand their pressure to the next stage kernel)."""
 
     def __init__(self, backend, comm):
         self.b = backend
@@ -313,14 +340,18 @@ class SlabSimulation:
         acc, y, yn = state.regs
         started = False
         cur = u0
+        p_pending = None
         for j in range(tab.stages):
             bj = tab.b[j]
             nxt = j + 1 < tab.stages
             self.b.stage(cur, u0=u0, s_in=acc if started else None, s_out=acc if bj != 0.0 else None,
-                         y_next=yn if nxt else None, cb=dt * bj, ca=dt * (tab.a[j + 1][j] if nxt else 0.0))
+                         y_next=yn if nxt else None, cb=dt * bj, ca=dt * (tab.a[j + 1][j] if nxt else 0.0),
+                         p_slab=p_pending)
             started = started or bj != 0.0
             if nxt:
-                self.proj.project(yn)
+                # intermediate projection split at the gradient subtract: the
+                # next stage kernel forms y - G p from the slab pressure
+                p_pending = self.proj.project_solve(yn)
                 y, yn = yn, y
                 cur = y
         self.proj.project(acc, p_ext=state.pressure)

@@ -36,8 +36,9 @@ class CpuSlabBackend:
         # one rank: the axis-0 pass works on the spectrum itself (no exchange)
         self.trans = torch.zeros((self.n0, self.n1 // P, nh, 2), dtype=torch.float64) if P > 1 else self.spec
         self.xchg = torch.zeros((P, m, self.n1 // P, nh, 2), dtype=torch.float64) if P > 1 else None
-        self.p_local = torch.zeros((m, self.n1, self.n2), dtype=torch.float64)
-        self.p_halo = torch.zeros((self.n1, self.n2), dtype=torch.float64)
+        self.p_slab = torch.zeros((m + 3, self.n1, self.n2), dtype=torch.float64)
+        self.p_local = self.p_slab[1:m + 1]
+        self.p_halo = self.p_slab[m + 1]
         lam = []
         for bnd, n in ((global_bounds[0], self.n0), (global_bounds[1], self.n1), (global_bounds[2], self.n2)):
             h = float(np.diff(bnd)[0])
@@ -69,9 +70,39 @@ class CpuSlabBackend:
                 x[tuple(sl)] = x[tuple(s2)]
 
     # -- compute
-    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0):
+    def _project_copy(self, y, p_slab):
+        """y - G p on every plane the stencil reads (ghost planes included),
+        from the slab pressure with the neighbours' planes."""
         og = self.og
-        k = O.momentum_rhs(og, self._np(y), self.nu, self.force)
+        m = self.lay.m
+        ys = [x.copy() for x in self._np(y)]
+        self._fill12(ys)
+        pe = np.zeros((m + 3,) + og.ext_shape[1:])
+        pe[:, 1:-1, 1:-1] = p_slab.numpy()
+        self._fill12([pe[:m + 2]])
+        pe[m + 2, 1:-1, 1:-1] = p_slab.numpy()[m + 2]
+        self._fill12([pe[m + 1:m + 3]])
+        n1, n2 = self.n1, self.n2
+        for a in range(3):
+            sl = (slice(0, m + 2), slice(0, n1 + 2), slice(0, n2 + 2))
+            hi = list(sl)
+            if a == 0:
+                hi[0] = slice(1, m + 3)
+                pn = pe[tuple(hi)]
+            else:
+                # periodic wrap along axes 1, 2 for the +1 neighbour of the last ghost
+                idx = np.arange(1, (n1 if a == 1 else n2) + 3)
+                nn = n1 if a == 1 else n2
+                idx = np.where(idx > nn + 1, idx - nn, idx)
+                pn = np.take(pe[:m + 2], idx, axis=a)
+            g = (pn - pe[:m + 2]) / og.col(og.du[a], a, slice(0, og.ext_shape[a]))
+            ys[a] -= g
+        return ys
+
+    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0, p_slab=None):
+        og = self.og
+        yv = self._np(y) if p_slab is None else self._project_copy(y, p_slab)
+        k = O.momentum_rhs(og, yv, self.nu, self.force)
         for a in range(3):
             sl = og.udof(a)
             if s_out is not None:
