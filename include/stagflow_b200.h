@@ -164,6 +164,15 @@ int sfb_eddy_stress_divergence(sfb_plan* plan, const void* const* u, const void*
 /* min and max over the interior of an extended scalar (synchronises). */
 int sfb_scalar_minmax(sfb_plan* plan, const void* f, double* mn, double* mx, void* stream);
 
+/* Channel statistics (stats.py:55-167): plane sums over the homogeneous
+ * directions at every wall index j = 1..n_wall, into a device fp64 array out.
+ * mode 0: raw component sums (dim x n_wall); mode 1: the 7 fluctuation
+ * moments of stats.cu (7 x n_wall), u being the fluctuation field with ghosts
+ * filled by the homogeneous conditions.  Deterministic two-pass sums. */
+int sfb_plane_sums(sfb_plan* plan, int wall_axis, const void* const* u, int mode, double* out, void* stream);
+/* u_a -= mean[a * n_wall + j - 1] at every position of wall index j (device mean). */
+int sfb_sub_plane_mean(sfb_plan* plan, int wall_axis, void* const* u, const double* mean, void* stream);
+
 /* Slab-decomposed spectral solve (multi-GPU, axis 0 split over nranks; the
  * plan's axis 0 is SFB_BC_HALO).  One projection =
  *   sfb_slab_forward  : divergence -> R2C (axis 2) -> FFT axis 1 -> xchg in the

@@ -75,6 +75,8 @@ _SIGS = {
     "sfb_closure_nut": [vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, VP3, vp, vp],
     "sfb_eddy_stress_divergence": [vp, VP3, vp, VP3, ctypes.c_int, vp],
     "sfb_scalar_minmax": [vp, vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), vp],
+    "sfb_plane_sums": [vp, ctypes.c_int, VP3, ctypes.c_int, vp, vp],
+    "sfb_sub_plane_mean": [vp, ctypes.c_int, VP3, vp, vp],
     "sfb_cg_configure": [vp, ctypes.c_double, ctypes.c_int],
     "sfb_cg_info": [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                     ctypes.POINTER(ctypes.c_int)],
@@ -149,6 +151,7 @@ KERNELS_PER_CALL = {
     "sfb_diffusion": 1, "sfb_momentum_rhs": 1, "sfb_weighted_scale": 1, "sfb_kinetic_energy": 2,
     "sfb_weighted_inner": 2, "sfb_cfl_conv": 2, "sfb_solver_solve": 1,
     "sfb_closure_nut": 1, "sfb_eddy_stress_divergence": 1, "sfb_scalar_minmax": 2,
+    "sfb_plane_sums": 2, "sfb_sub_plane_mean": 1,
     "sfb_divergence_pullback": 2, "sfb_pressure_gradient_pullback": 2, "sfb_diffusion_pullback": 2,
     "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4, "sfb_project_pullback_ex": 4,
     "sfb_slab_axis0": 1, "sfb_slab_inverse": 2, "sfb_slab_correct": 2,

@@ -264,6 +264,28 @@ def main():
     poisson.project_into(u, setup.solver, setup.bcs)
     les_case("les_channel", g, setup.bcs, setup.solver, u)
 
+    # ---- channel statistics (stats.py): three snapshots of a channel run
+    # with a closure, with and without eddy-viscosity profiles
+    from stagflow import stats
+
+    setup = cases.channel_setup(8, 6, 4, gamma=2.0, solver="direct", closure=les.ClosureModel("smagorinsky"))
+    st = setup.new_state()
+    poisson.project_into(st.u, setup.solver, setup.bcs)
+    snaps, nuts = [], []
+    for _ in range(3):
+        ts.run_steps(setup, 2, dt=0.002, state=st)
+        snaps.append(st.u.copy())
+        nuts.append(setup.closure.nu_t(st.u))
+    out = dict(grid_meta(setup.grid), nu=setup.nu)
+    for i, sn in enumerate(snaps):
+        out.update(vel(f"snap{i}_", sn))
+        out[f"nut{i}"] = nuts[i].data.copy()
+    for tag, ns in (("plain", None), ("nut", nuts)):
+        prof = stats.accumulate_stats(snaps, setup.bcs, setup.nu, nut_snapshots=ns)
+        out[f"{tag}_rows"] = prof.rows()
+        out[f"{tag}_u_tau"] = prof.u_tau
+    save("stats_channel", **out)
+
     # ---- adjoint: project pullback and unrolled gradient (RK4, 1 and 2 steps)
     rng = np.random.default_rng(3)
     g = mkgrid((6, 5, 4), False)
