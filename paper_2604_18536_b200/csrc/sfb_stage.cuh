@@ -1,4 +1,4 @@
-// Shared pieces of the RK-stage kernels (stage.cu, stage_pair.cu).
+// Shared pieces of the RK-stage kernels (stage.cu).
 #pragma once
 
 #include "sfb_kernels.cuh"
@@ -54,7 +54,6 @@ __device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
 // branch-free stencil evaluation, stores predicated on the tile bounds only
 enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16, FL_PER = 32 };
 
-template <typename T>
-int stage_pair(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st);
+
 
 }  // namespace sfb

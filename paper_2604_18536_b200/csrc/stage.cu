@@ -385,10 +385,6 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
   if (G.dim == 3 && (!getenv("SFB_STAGE_GENERIC") || A.p_int)) {
-    if (getenv("SFB_PAIR") && !A.p_int) {
-      const int rcp = stage_pair<T>(G, A, st);
-      if (rcp >= 0) return rcp;
-    }
     const int rc = stage_march<T>(G, A, st);
     if (rc >= 0) return rc;
     if (A.p_int) return fail(SFB_ECONFIG, "on-the-fly projection: unsupported stage variant");
