@@ -300,7 +300,13 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   cp_wait<0>();
 }
 
-constexpr int kTJ = 8, kTK = 32, kCPT = 2;
+#ifndef SFB_STAGE_TJ
+#define SFB_STAGE_TJ 8
+#endif
+#ifndef SFB_STAGE_CPT
+#define SFB_STAGE_CPT 2
+#endif
+constexpr int kTJ = SFB_STAGE_TJ, kTK = 32, kCPT = SFB_STAGE_CPT;
 
 template <typename T, int FL>
 static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
