@@ -149,7 +149,7 @@ int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream);
  * sfb_rk_stage (sfb_stage_args.p_int), which applies u - G p on the fly. */
 int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, void* stream);
 /* Number of kernels (ours) launched by sfb_project (mode 0: without, 1: with
- * the extended pressure), sfb_project_solve (2) or sfb_slab_forward (3). */
+ * the extended pressure), sfb_project_solve (2) or sfb_slab_r2c (3). */
 int sfb_project_launches(const sfb_solver* s, int with_pressure);
 
 /* Eddy-viscosity closures (les.py:58-417).  kind: 1 smagorinsky, 2 vreman,
@@ -174,27 +174,34 @@ int sfb_plane_sums(sfb_plan* plan, int wall_axis, const void* const* u, int mode
 int sfb_sub_plane_mean(sfb_plan* plan, int wall_axis, void* const* u, const double* mean, void* stream);
 
 /* Slab-decomposed spectral solve (multi-GPU, axis 0 split over nranks; the
- * plan's axis 0 is SFB_BC_HALO).  One projection =
- *   sfb_slab_forward  : divergence -> R2C (axis 2) -> FFT axis 1 -> xchg in the
- *                       all-to-all send layout (P, m, n1/P, nh)  [P = 1: spec]
- *   caller            : all-to-all xchg -> trans (n0, n1/P, nh)   [P = 1: none]
- *   sfb_slab_axis0    : FFT axis 0 -> 1/(Lambda N) -> inverse FFT axis 0 on trans
- *                       (trans is spec when P = 1)
- *   caller            : all-to-all back trans -> xchg             [P = 1: none]
- *   sfb_slab_inverse  : inverse FFT axis 1 (reading xchg) -> C2R -> local
- *                       pressure (m planes)
- *   caller            : copy the next slab's first pressure plane into p_halo
+ * plan's axis 0 is SFB_BC_HALO).  One projection, with the nh half-spectrum
+ * columns split into K chunks so each chunk's exchange overlaps the next
+ * chunk's transform:
+ *   sfb_slab_r2c      : divergence -> R2C (axis 2) -> spec
+ *   sfb_slab_axis1(k) : FFT axis 1 of chunk k -> xchg block k, laid out
+ *                       (P, m, n1/P, w_k) (rank q's k1 range contiguous)
+ *   caller            : all-to-all xchg block k -> trans block k (n0, n1/P, w_k)
+ *   sfb_slab_axis0(k) : FFT axis 0 -> 1/(Lambda N) -> inverse FFT axis 0 on trans block k
+ *   caller            : all-to-all back trans block k -> xchg block k
+ *   sfb_slab_axis1(k, inverse) : inverse FFT axis 1 reading xchg block k -> spec
+ *   sfb_slab_c2r      : C2R -> local pressure (m planes)
+ *   caller            : the neighbours' pressure planes (p_slab)
  *   sfb_slab_correct  : u -= G p (uses p_halo), fill non-halo ghosts, p_ext
- * (poisson.py:167-200, 321-341 split at the two transposes.) */
+ * With one rank there is no exchange: axis 1 / axis 0 run on spec in place
+ * (chunk arguments ignored).  (poisson.py:167-200, 321-341 split at the two
+ * transposes.) */
 int sfb_slab_solver_create(sfb_plan* plan, int n0_global, int rank, int nranks, sfb_solver** out);
 /* xchg is NULL when nranks == 1 (no exchange; trans aliases spec).  p_slab:
  * the slab pressure (m + 3 planes: prev's last, the m local planes = p_local,
  * next's first = p_halo, next's second), the p_int of an on-the-fly stage. */
 int sfb_slab_buffers(sfb_solver* s, void** spec, void** trans, void** xchg, void** p_slab, void** p_local,
                      void** p_halo);
-int sfb_slab_forward(sfb_solver* s, void* const* u, void* stream);
-int sfb_slab_axis0(sfb_solver* s, void* stream);
-int sfb_slab_inverse(sfb_solver* s, void* stream);
+/* Largest useful K (1 when the axis-1 length has no register FFT engine). */
+int sfb_slab_max_chunks(const sfb_solver* s);
+int sfb_slab_r2c(sfb_solver* s, void* const* u, void* stream);
+int sfb_slab_axis1(sfb_solver* s, int chunk, int nchunks, int inverse, void* stream);
+int sfb_slab_axis0(sfb_solver* s, int chunk, int nchunks, void* stream);
+int sfb_slab_c2r(sfb_solver* s, void* stream);
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream);
 
 /* Pullbacks (adjoint.py:114-349), periodic grids. Mutating semantics of the

@@ -89,9 +89,11 @@ _SIGS = {
     "sfb_slab_solver_create": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
     "sfb_slab_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
                          ctypes.POINTER(vp), ctypes.POINTER(vp)],
-    "sfb_slab_forward": [vp, VP3, vp],
-    "sfb_slab_axis0": [vp, vp],
-    "sfb_slab_inverse": [vp, vp],
+    "sfb_slab_r2c": [vp, VP3, vp],
+    "sfb_slab_max_chunks": [vp],
+    "sfb_slab_axis1": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
+    "sfb_slab_axis0": [vp, ctypes.c_int, ctypes.c_int, vp],
+    "sfb_slab_c2r": [vp, vp],
     "sfb_slab_correct": [vp, VP3, vp, vp],
     "sfb_divergence_pullback": [vp, vp, VP3, vp],
     "sfb_pressure_gradient_pullback": [vp, VP3, vp, vp],
@@ -154,7 +156,7 @@ KERNELS_PER_CALL = {
     "sfb_plane_sums": 2, "sfb_sub_plane_mean": 1,
     "sfb_divergence_pullback": 2, "sfb_pressure_gradient_pullback": 2, "sfb_diffusion_pullback": 2,
     "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4, "sfb_project_pullback_ex": 4,
-    "sfb_slab_axis0": 1, "sfb_slab_inverse": 2, "sfb_slab_correct": 2,
+    "sfb_slab_axis0": 1, "sfb_slab_axis1": 1, "sfb_slab_c2r": 1, "sfb_slab_correct": 2,
 }
 launches = 0
 
@@ -162,9 +164,9 @@ launches = 0
 def call(name, *args):
     global launches
     check(getattr(lib, name)(*args))
-    if name in ("sfb_project", "sfb_project_solve", "sfb_slab_forward"):
+    if name in ("sfb_project", "sfb_project_solve", "sfb_slab_r2c"):
         with_p = name == "sfb_project" and args[2] is not None and args[2] != 0
-        mode = {"sfb_project_solve": 2, "sfb_slab_forward": 3}.get(name, int(with_p))
+        mode = {"sfb_project_solve": 2, "sfb_slab_r2c": 3}.get(name, int(with_p))
         k = lib.sfb_project_launches(args[0], mode)
         launches += k
         return

@@ -557,37 +557,19 @@ __global__ void k_chunk_permute(const typename CX<T>::t* __restrict__ nat, typen
   }
 }
 
-template <typename T>
-static RegCall split_call(const FftSolve& F, int kind, const void* in, void* out, int m, int n1, int c, int nh) {
-  RegCall rc{};
-  rc.kind = kind;
-  rc.in = in;
-  rc.out = out;
-  rc.ncol = nh;
-  rc.nbatch = m;
-  rc.S = nh;  // the natural side's row stride
-  rc.map_c = c;
-  rc.map_sq = (long long)m * c * nh;
-  rc.map_s = nh;
-  if (kind == 6) {  // natural in, chunked out
-    rc.bstride_in = (long long)n1 * nh;
-    rc.bstride = (long long)c * nh;
-  } else {  // chunked in, natural out
-    rc.bstride_in = (long long)c * nh;
-    rc.bstride = (long long)n1 * nh;
-  }
-  rc.twL = F.tw_ax[1];
-  return rc;
+// column chunk k of K over the nh half-spectrum columns
+static void chunk_cols(int nh, int k, int K, int& c0, int& w) {
+  const int base = (nh + K - 1) / K;
+  c0 = k * base;
+  w = nh - c0 < base ? nh - c0 : base;
 }
 
 template <typename T>
-int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u,
-                     void* xbuf, int nranks) {
+int fft_slab_r2c(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u) {
   typedef typename CX<T>::t C;
   C* cbuf = (C*)cbuf_v;
-  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], nh = nlast / 2 + 1;
+  const int m = F.n[0], n1 = F.n[1], nh = F.n[2] / 2 + 1;
   const long long rows = (long long)m * n1;
-  int rc;
   if (G && fft_divfuse_ok(F, *G)) {
     RegCall c{};
     c.kind = 5;
@@ -598,68 +580,98 @@ int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const 
     c.twN = F.tw_full;
     c.geo = G;
     for (int a = 0; a < 3; ++a) c.u[a] = u[a];
-    rc = reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
-  } else {
-    rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
+    return reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
   }
-  if (rc) return rc;
+  return launch_r2c<T>(F, rbuf, cbuf, rows, st);
+}
+
+// Axis-1 FFT of column chunk k of K.  One rank: in place on the natural
+// spectrum (the whole width).  P ranks: forward writes / inverse reads the
+// chunk's all-to-all block of xbuf, laid out (P, m, n1/P, w) (rank q's k1
+// range contiguous), so the exchange needs no packing.
+template <typename T>
+int fft_slab_axis1(FftSolve& F, void* cbuf_v, void* xbuf, int nranks, int k, int K, bool inverse, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  C* cbuf = (C*)cbuf_v;
+  const int m = F.n[0], n1 = F.n[1], nh = F.n[2] / 2 + 1;
   ScaleArgs none{};
-  if (xbuf && nranks > 1) {
-    // axis-1 FFT written straight into the all-to-all send layout
-    const int c = n1 / nranks;
-    if (F.reg_ax[1])
-      return reg_run<T>(SFB_REG(F, 1), split_call<T>(F, 6, cbuf, xbuf, m, n1, c, nh), st);
-    if ((rc = launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
-                                   (const C*)F.tw_ax[1], none, st, &F.tma_ax1, RegLen{})))
-      return rc;
-    k_chunk_permute<T><<<148 * 8, 256, 0, st>>>(cbuf, (C*)xbuf, m, n1, c, nh, 1);
+  if (!xbuf || nranks <= 1) {
+    if (inverse)
+      return launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                                  (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
+    return launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                                (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
+  }
+  const int c = n1 / nranks;
+  int c0, w;
+  chunk_cols(nh, k, K, c0, w);
+  if (w <= 0) return SFB_OK;
+  C* xk = (C*)xbuf + (long long)nranks * m * c * c0;
+  if (!F.reg_ax[1]) {
+    // Stockham / cuFFT-length fallback: whole-width transform + permute copy
+    if (K != 1) return fail(SFB_EINVAL, "chunked slab exchange needs the register FFT engine");
+    if (inverse) {
+      k_chunk_permute<T><<<148 * 8, 256, 0, st>>>(cbuf, xk, m, n1, c, nh, 0);
+      SFB_LAUNCH_CHECK("slab unpack");
+      return launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                                  (const C*)F.tw_ax[1], none, st, &F.tma_ax1, RegLen{});
+    }
+    int rc = launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
+                                  (const C*)F.tw_ax[1], none, st, &F.tma_ax1, RegLen{});
+    if (rc) return rc;
+    k_chunk_permute<T><<<148 * 8, 256, 0, st>>>(cbuf, xk, m, n1, c, nh, 1);
     SFB_LAUNCH_CHECK("slab pack");
     return SFB_OK;
   }
-  return launch_strided<T, 0>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
-                              (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
+  RegCall rc{};
+  rc.kind = inverse ? 7 : 6;
+  rc.in = inverse ? (const void*)xk : (const void*)(cbuf + c0);
+  rc.out = inverse ? (void*)(cbuf + c0) : (void*)xk;
+  rc.ncol = w;
+  rc.nbatch = m;
+  rc.S = nh;  // the natural side's row stride
+  rc.map_c = c;
+  rc.map_sq = (long long)m * c * w;
+  rc.map_s = w;
+  rc.bstride_in = inverse ? (long long)c * w : (long long)n1 * nh;
+  rc.bstride = inverse ? (long long)n1 * nh : (long long)c * w;
+  rc.twL = F.tw_ax[1];
+  return reg_run<T>(SFB_REG(F, 1), rc, st);
 }
+
+// Axis-0 forward -> 1/(Lambda N) -> inverse on column chunk k of K of the
+// transposed spectrum (n0, n1/P, w) (the whole spectrum in place when P = 1)
 template <typename T>
-int fft_slab_axis0(FftSolve& F, void* tbuf_v, int n1_chunk, cudaStream_t st) {
+int fft_slab_axis0(FftSolve& F, void* tbuf_v, int n1_chunk, int nranks, int k, int K, cudaStream_t st) {
   typedef typename CX<T>::t C;
   const int nh = F.n[2] / 2 + 1;
-  const int ncol = n1_chunk * nh;
-  return launch_strided<T, 2>((C*)tbuf_v, F.ax[0], pick_w(F.ax[0].L, sizeof(C)), ncol, ncol, 0, 1,
-                              (const C*)F.tw_ax[0], F.sc, st, &F.tma_ax0, SFB_REG(F, 0));
+  int c0 = 0, w = nh;
+  if (nranks > 1) chunk_cols(nh, k, K, c0, w);
+  if (w <= 0) return SFB_OK;
+  C* tk = (C*)tbuf_v + (long long)F.ax[0].L * n1_chunk * c0;
+  ScaleArgs sc = F.sc;
+  sc.nh = w;
+  sc.l2 = F.sc.l2 + c0;
+  sc.zero_ok = F.sc.zero_ok && c0 == 0;
+  const int ncol = n1_chunk * w;
+  return launch_strided<T, 2>(tk, F.ax[0], pick_w(F.ax[0].L, sizeof(C)), ncol, ncol, 0, 1, (const C*)F.tw_ax[0], sc,
+                              st, K == 1 ? &F.tma_ax0 : nullptr, SFB_REG(F, 0));
 }
+
 template <typename T>
-int fft_slab_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st, void* xbuf, int nranks) {
+int fft_slab_c2r(FftSolve& F, void* cbuf, T* rbuf, cudaStream_t st) {
   typedef typename CX<T>::t C;
-  C* cbuf = (C*)cbuf_v;
-  const int m = F.n[0], n1 = F.n[1], nlast = F.n[2], nh = nlast / 2 + 1;
-  ScaleArgs none{};
-  int rc;
-  if (xbuf && nranks > 1) {
-    // inverse axis-1 FFT read straight from the all-to-all receive layout
-    const int c = n1 / nranks;
-    if (F.reg_ax[1]) {
-      rc = reg_run<T>(SFB_REG(F, 1), split_call<T>(F, 7, xbuf, cbuf, m, n1, c, nh), st);
-    } else {
-      k_chunk_permute<T><<<148 * 8, 256, 0, st>>>(cbuf, (C*)xbuf, m, n1, c, nh, 0);
-      SFB_LAUNCH_CHECK("slab unpack");
-      rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
-                                (const C*)F.tw_ax[1], none, st, &F.tma_ax1, RegLen{});
-    }
-  } else {
-    rc = launch_strided<T, 1>(cbuf, F.ax[1], pick_w(n1, sizeof(C)), nh, nh, (long long)n1 * nh, m,
-                              (const C*)F.tw_ax[1], none, st, &F.tma_ax1, SFB_REG(F, 1));
-  }
-  if (rc) return rc;
-  return launch_c2r<T>(F, cbuf, rbuf, (long long)m * n1, st);
+  return launch_c2r<T>(F, (const C*)cbuf, rbuf, (long long)F.n[0] * F.n[1], st);
 }
-template int fft_slab_forward<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*,
-                                      void*, int);
-template int fft_slab_forward<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*,
-                                     void*, int);
-template int fft_slab_axis0<double>(FftSolve&, void*, int, cudaStream_t);
-template int fft_slab_axis0<float>(FftSolve&, void*, int, cudaStream_t);
-template int fft_slab_inverse<double>(FftSolve&, void*, double*, cudaStream_t, void*, int);
-template int fft_slab_inverse<float>(FftSolve&, void*, float*, cudaStream_t, void*, int);
+
+#define SFB_SLAB_INST(T)                                                                                          \
+  template int fft_slab_r2c<T>(FftSolve&, T*, void*, cudaStream_t, const Geo<T>*, const void* const*);            \
+  template int fft_slab_axis1<T>(FftSolve&, void*, void*, int, int, int, bool, cudaStream_t);                     \
+  template int fft_slab_axis0<T>(FftSolve&, void*, int, int, int, int, cudaStream_t);                             \
+  template int fft_slab_c2r<T>(FftSolve&, void*, T*, cudaStream_t);
+SFB_SLAB_INST(double)
+SFB_SLAB_INST(float)
+#undef SFB_SLAB_INST
 
 template <typename T>
 int fft_set_smem_limits() {

@@ -678,7 +678,7 @@ int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, v
 int sfb_project_launches(const sfb_solver* s, int mode) {
   if (!s) return 0;
   const bool fused = s->plan->dtype == SFB_F64 ? divfused<double>(s) : divfused<float>(s);
-  if (mode == 3) return fused ? 2 : 3;  // sfb_slab_forward
+  if (mode == 3) return fused ? 1 : 2;  // sfb_slab_r2c
   int n;
   if (s->fft.enabled) n = (s->plan->dim == 3 ? 5 : 3) + (fused ? 0 : 1);
   else if (s->kind == SFB_SOLVER_CG) n = 1 + 4 + 7 * s->cg_iters;  // divergence, CG init, CG iterations
@@ -804,17 +804,16 @@ static T* slab_local(sfb_solver* s) {
 }
 
 template <typename T>
-static int slab_forward(sfb_solver* s, void* const* u, cudaStream_t st) {
+static int slab_r2c(sfb_solver* s, void* const* u, cudaStream_t st) {
   sfb_plan* p = s->plan;
   const Geo<T>& G = geo<T>(p);
   if (fft_divfuse_ok<T>(s->fft, G))
-    return fft_slab_forward<T>(s->fft, slab_local<T>(s), s->cbuf, st, &G, (const void* const*)u, s->xbuf,
-                               s->nranks);
+    return fft_slab_r2c<T>(s->fft, slab_local<T>(s), s->cbuf, st, &G, (const void* const*)u);
   CV<T> C;
   for (int a = 0; a < 3; ++a) C.c[a] = (const T*)u[a];
   int rc = launch_div<T>(G, C, slab_local<T>(s), st);
   if (rc) return rc;
-  return fft_slab_forward<T>(s->fft, slab_local<T>(s), s->cbuf, st, nullptr, nullptr, s->xbuf, s->nranks);
+  return fft_slab_r2c<T>(s->fft, slab_local<T>(s), s->cbuf, st, nullptr, nullptr);
 }
 
 template <typename T>
@@ -835,26 +834,38 @@ static int slab_correct(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t
 
 extern "C" {
 
-int sfb_slab_forward(sfb_solver* s, void* const* u, void* stream) {
+int sfb_slab_r2c(sfb_solver* s, void* const* u, void* stream) {
   if (!s || !s->slab || !u || !u[0] || !u[1] || !u[2]) return fail(SFB_EINVAL, "bad slab call");
-  return s->plan->dtype == SFB_F64 ? slab_forward<double>(s, u, (cudaStream_t)stream)
-                                   : slab_forward<float>(s, u, (cudaStream_t)stream);
+  return s->plan->dtype == SFB_F64 ? slab_r2c<double>(s, u, (cudaStream_t)stream)
+                                   : slab_r2c<float>(s, u, (cudaStream_t)stream);
 }
 
-int sfb_slab_axis0(sfb_solver* s, void* stream) {
-  if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
-  const int chunk = s->plan->n[1] / s->nranks;
-  return s->plan->dtype == SFB_F64 ? fft_slab_axis0<double>(s->fft, s->tbuf, chunk, (cudaStream_t)stream)
-                                   : fft_slab_axis0<float>(s->fft, s->tbuf, chunk, (cudaStream_t)stream);
+int sfb_slab_max_chunks(const sfb_solver* s) {
+  if (!s || !s->slab) return 0;
+  return s->fft.reg_ax[1] ? s->plan->n[2] / 2 + 1 : 1;
 }
 
-int sfb_slab_inverse(sfb_solver* s, void* stream) {
-  if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
+int sfb_slab_axis1(sfb_solver* s, int chunk, int nchunks, int inverse, void* stream) {
+  if (!s || !s->slab || nchunks < 1 || chunk < 0 || chunk >= nchunks) return fail(SFB_EINVAL, "bad slab call");
   return s->plan->dtype == SFB_F64
-             ? fft_slab_inverse<double>(s->fft, s->cbuf, slab_local<double>(s), (cudaStream_t)stream, s->xbuf,
-                                        s->nranks)
-             : fft_slab_inverse<float>(s->fft, s->cbuf, slab_local<float>(s), (cudaStream_t)stream, s->xbuf,
-                                       s->nranks);
+             ? fft_slab_axis1<double>(s->fft, s->cbuf, s->xbuf, s->nranks, chunk, nchunks, inverse != 0,
+                                      (cudaStream_t)stream)
+             : fft_slab_axis1<float>(s->fft, s->cbuf, s->xbuf, s->nranks, chunk, nchunks, inverse != 0,
+                                     (cudaStream_t)stream);
+}
+
+int sfb_slab_axis0(sfb_solver* s, int chunk, int nchunks, void* stream) {
+  if (!s || !s->slab || nchunks < 1 || chunk < 0 || chunk >= nchunks) return fail(SFB_EINVAL, "bad slab call");
+  const int c = s->plan->n[1] / s->nranks;
+  return s->plan->dtype == SFB_F64
+             ? fft_slab_axis0<double>(s->fft, s->tbuf, c, s->nranks, chunk, nchunks, (cudaStream_t)stream)
+             : fft_slab_axis0<float>(s->fft, s->tbuf, c, s->nranks, chunk, nchunks, (cudaStream_t)stream);
+}
+
+int sfb_slab_c2r(sfb_solver* s, void* stream) {
+  if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
+  return s->plan->dtype == SFB_F64 ? fft_slab_c2r<double>(s->fft, s->cbuf, slab_local<double>(s), (cudaStream_t)stream)
+                                   : fft_slab_c2r<float>(s->fft, s->cbuf, slab_local<float>(s), (cudaStream_t)stream);
 }
 
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream) {

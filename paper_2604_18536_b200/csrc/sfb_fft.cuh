@@ -68,17 +68,16 @@ int fft_tma_make(FftTma& M, void* base, bool f64, int rank, long long inner_comp
                  int L);
 template <typename T, int MODE>
 int fft_tma_pass(const FftTma& M, const FftLen& P, const void* tw, const ScaleArgs& sc, cudaStream_t st);
-// divergence of u fused into the R2C pass when G/u are given and supported;
-// with xbuf (nranks > 1) the axis-1 transform is written in the all-to-all
-// send layout (P, m, n1/P, nh)
+// slab-decomposed pieces (multi-GPU, fft.cu): R2C (divergence fused when
+// G/u given), axis-1 FFT of a column chunk into / out of the all-to-all
+// layout, axis-0 solve of a column chunk, C2R
 template <typename T>
-int fft_slab_forward(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const Geo<T>* G = nullptr,
-                     const void* const* u = nullptr, void* xbuf = nullptr, int nranks = 1);
+int fft_slab_r2c(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const Geo<T>* G, const void* const* u);
 template <typename T>
-int fft_slab_axis0(FftSolve& F, void* tbuf, int n1_chunk, cudaStream_t st);
-// with xbuf (nranks > 1) the inverse axis-1 transform reads the all-to-all
-// receive layout
+int fft_slab_axis1(FftSolve& F, void* cbuf, void* xbuf, int nranks, int k, int K, bool inverse, cudaStream_t st);
 template <typename T>
-int fft_slab_inverse(FftSolve& F, void* cbuf, T* rbuf, cudaStream_t st, void* xbuf = nullptr, int nranks = 1);
+int fft_slab_axis0(FftSolve& F, void* tbuf, int n1_chunk, int nranks, int k, int K, cudaStream_t st);
+template <typename T>
+int fft_slab_c2r(FftSolve& F, void* cbuf, T* rbuf, cudaStream_t st);
 
 }  // namespace sfb

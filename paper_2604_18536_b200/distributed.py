@@ -5,11 +5,11 @@ survey's "z" in its [z][y][x] naming) into P slabs of m = n0/P planes, one
 process per GPU (``torch.distributed``, NCCL over NVLink).  Per projection:
 
     halo(u)            exchange the +-1 ghost planes of u with the neighbours
-    forward            divergence -> R2C (axis 2) -> FFT axis 1 (local)
-    all_to_all         spectrum (m, n1, nh) -> transposed (n0, n1/P, nh)
-    axis0              FFT axis 0 -> 1/(Lambda N) -> inverse FFT axis 0
-    all_to_all         back to (m, n1, nh)
-    inverse            inverse FFT axis 1 -> C2R (local pressure)
+    r2c                divergence -> R2C (axis 2)
+    per column chunk:  FFT axis 1 -> all_to_all (m, n1, w) -> (n0, n1/P, w)
+                       -> FFT axis 0 -> 1/(Lambda N) -> inverse FFT axis 0
+                       -> all_to_all back -> inverse FFT axis 1 (pipelined)
+    c2r                C2R (local pressure)
     p halo             next slab's first pressure plane
     correct            u -= G p, ghost fill of axes 1, 2
     halo(u)            for the next stencil
@@ -84,6 +84,11 @@ class SlabGrid(Grid):
 # ---------------------------------------------------------------------------
 # communication
 # ---------------------------------------------------------------------------
+class _Done:
+    def wait(self):
+        return True
+
+
 class Comm:
     """Halo exchange, all-to-all and all-reduce over a process group.
     ``stage_host=True`` stages CUDA tensors through host memory (gloo)."""
@@ -121,15 +126,22 @@ class Comm:
         self._send_recv(send_plane, recv_plane, self.layout.next, self.layout.prev)
 
     def all_to_all(self, out, inp):
+        self.all_to_all_async(out, inp).wait()
+
+    def all_to_all_async(self, out, inp):
+        """Equal-split all-to-all over dim 0; returns a handle whose wait()
+        orders later work on the current stream after the exchange (NCCL:
+        the exchange runs on NCCL's stream, overlapping the caller's next
+        kernels)."""
         if self.layout.size == 1:
             out.copy_(inp)
-            return
+            return _Done()
         if self.stage_host:
             o = torch.empty(out.shape, dtype=out.dtype)
             dist.all_to_all_single(o, inp.cpu(), group=self.group)
             out.copy_(o)
-        else:
-            dist.all_to_all_single(out, inp, group=self.group)
+            return _Done()
+        return dist.all_to_all_single(out, inp, group=self.group, async_op=True)
 
     def allreduce(self, value, op="sum"):
         if self.layout.size == 1:
@@ -225,14 +237,20 @@ class CudaSlabBackend:
         e1.record()
         TS.STAGE_EVENTS.append((e0, e1, nfield * 3 * self.grid.dtype.itemsize))
 
-    def forward(self, u):
-        N.call("sfb_slab_forward", self.handle, N.ptr3(u.u), self._sp())
+    def max_chunks(self):
+        return int(N.lib.sfb_slab_max_chunks(self.handle))
 
-    def axis0(self):
-        N.call("sfb_slab_axis0", self.handle, self._sp())
+    def r2c(self, u):
+        N.call("sfb_slab_r2c", self.handle, N.ptr3(u.u), self._sp())
 
-    def inverse(self):
-        N.call("sfb_slab_inverse", self.handle, self._sp())
+    def axis1(self, k, nchunks, inverse=False):
+        N.call("sfb_slab_axis1", self.handle, int(k), int(nchunks), 1 if inverse else 0, self._sp())
+
+    def axis0(self, k=0, nchunks=1):
+        N.call("sfb_slab_axis0", self.handle, int(k), int(nchunks), self._sp())
+
+    def c2r(self):
+        N.call("sfb_slab_c2r", self.handle, self._sp())
 
     def correct(self, u, p_ext=None):
         N.call("sfb_slab_correct", self.handle, N.ptr3(u.u), None if p_ext is None else p_ext.data.data_ptr(), self._sp())
@@ -255,32 +273,75 @@ class CudaSlabBackend:
 # orchestration (backend-agnostic)
 # ---------------------------------------------------------------------------
 class SlabProjector:
-    """One projection of the slab-decomposed field.  The backend's forward
-    transform writes the spectrum straight into the all-to-all send layout
-    ``xchg`` = (P, m, n1/P, nh) (chunk q = the k1 range of rank q) and its
-    inverse reads the receive layout, so the exchange needs no packing copies;
-    with one rank there is no exchange at all."""
+    """One projection of the slab-decomposed field.
 
-    def __init__(self, backend, comm):
+    The half-spectrum columns are split into K chunks.  The axis-1 transform
+    of chunk k writes its all-to-all send block directly (``xchg`` block k,
+    laid out (P, m, n1/P, w_k)), so the exchange needs no packing, and the
+    chunks are pipelined: the exchange of chunk k runs on NCCL's stream
+    while chunk k+1 is transformed, the axis-0 solve of chunk k while the
+    exchanges of later chunks are in flight, and so on.  With one rank there
+    is no exchange at all."""
+
+    def __init__(self, backend, comm, chunks=None):
+        import os
+
         self.b = backend
         self.comm = comm
+        if chunks is None:
+            chunks = int(os.environ.get("SFB_SLAB_CHUNKS", "4"))
+        self.K = max(1, min(chunks, backend.max_chunks())) if comm.layout.size > 1 else 1
+
+    def _blocks(self):
+        """(xchg block, trans block) views of chunk k, flat per rank."""
+        b, lay = self.b, self.comm.layout
+        P, m = lay.size, lay.m
+        n0, c, nh = b.trans.shape[0], b.trans.shape[1], b.trans.shape[2]
+        xf = b.xchg.reshape(-1)
+        tf = b.trans.reshape(-1)
+        base = (nh + self.K - 1) // self.K
+        out = []
+        for k in range(self.K):
+            c0 = k * base
+            w = min(base, nh - c0)
+            if w <= 0:
+                out.append(None)
+                continue
+            off, n = 2 * P * m * c * c0, 2 * P * m * c * w
+            out.append((xf[off:off + n].view(P, -1), tf[off:off + n].view(P, -1)))
+        return out
 
     def _solve(self, u):
         b, comm = self.b, self.comm
-        lay = comm.layout
-        P, m = lay.size, lay.m
+        P = comm.layout.size
         comm.halo(u.u)
-        b.forward(u)
-        if P > 1:
-            c = b.trans.shape[1]
-            tv = b.trans.view(P, m, c, b.trans.shape[2], 2)
-            # received chunks are ordered by source rank = global plane order
-            comm.all_to_all(tv, b.xchg)
-            b.axis0()
-            comm.all_to_all(b.xchg, tv)
+        b.r2c(u)
+        if P == 1:
+            b.axis1(0, 1)
+            b.axis0(0, 1)
+            b.axis1(0, 1, inverse=True)
         else:
-            b.axis0()
-        b.inverse()
+            K = self.K
+            blocks = self._blocks()
+            fwd = [None] * K
+            for k in range(K):
+                if blocks[k] is None:
+                    continue
+                b.axis1(k, K)
+                fwd[k] = comm.all_to_all_async(blocks[k][1], blocks[k][0])
+            back = [None] * K
+            for k in range(K):
+                if blocks[k] is None:
+                    continue
+                fwd[k].wait()
+                b.axis0(k, K)
+                back[k] = comm.all_to_all_async(blocks[k][0], blocks[k][1])
+            for k in range(K):
+                if blocks[k] is None:
+                    continue
+                back[k].wait()
+                b.axis1(k, K, inverse=True)
+        b.c2r()
 
     def project(self, u, p_ext=None):
         """Full projection (poisson.py:321-341) of the slab field."""

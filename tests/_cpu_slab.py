@@ -111,39 +111,75 @@ class CpuSlabBackend:
             if y_next is not None:
                 y_next.u[a].numpy()[sl] = u0.u[a].numpy()[sl] + k[a][sl] * ca
 
-    def forward(self, u):
+    # -- spectral solve in column chunks (the CUDA backend's interface)
+    def max_chunks(self):
+        return self.n2 // 2 + 1
+
+    def _chunk(self, k, K):
+        nh = self.n2 // 2 + 1
+        base = (nh + K - 1) // K
+        c0 = k * base
+        return c0, min(base, nh - c0)
+
+    def _blocks(self, k, K):
+        """xchg block k as (P, m, c, w) and trans block k as (n0, c, w), complex."""
+        P, m = self.lay.size, self.lay.m
+        c = self.n1 // P
+        c0, w = self._chunk(k, K)
+        off, n = 2 * P * m * c * c0, 2 * P * m * c * w
+        xb = self.xchg.reshape(-1)[off:off + n].view(P, m, c, w, 2)
+        tb = self.trans.reshape(-1)[off:off + n].view(self.n0, c, w, 2)
+        return xb, tb, c0, w
+
+    def r2c(self, u):
         arrs = self._np(u)
         self._fill12(arrs)
         div = O.divergence(self.og, arrs)[self.og.pdof()]
-        s = np.fft.fft(np.fft.rfft(div, axis=2), axis=1)
-        self.spec.copy_(torch.view_as_real(torch.from_numpy(s)))
-        if self.xchg is not None:
-            P, m = self.lay.size, self.lay.m
-            c = self.n1 // P
-            self.xchg.copy_(self.spec.view(m, P, c, -1, 2).permute(1, 0, 2, 3, 4))
+        self.spec.copy_(torch.view_as_real(torch.from_numpy(np.fft.rfft(div, axis=2))))
 
-    def axis0(self):
-        t = torch.view_as_complex(self.trans).numpy()
-        f = np.fft.fft(t, axis=0)
+    def axis1(self, k, K, inverse=False):
+        s = torch.view_as_complex(self.spec).numpy()
+        if self.xchg is None:
+            s[...] = np.fft.ifft(s, axis=1) if inverse else np.fft.fft(s, axis=1)
+            return
+        P, m = self.lay.size, self.lay.m
+        c = self.n1 // P
+        xb, _, c0, w = self._blocks(k, K)
+        if w <= 0:
+            return
+        if inverse:
+            blk = torch.view_as_complex(xb.contiguous()).numpy()  # (P, m, c, w)
+            nat = blk.transpose(1, 0, 2, 3).reshape(m, self.n1, w)
+            s[:, :, c0:c0 + w] = np.fft.ifft(nat, axis=1)
+        else:
+            f = np.fft.fft(s[:, :, c0:c0 + w], axis=1).reshape(m, P, c, w).transpose(1, 0, 2, 3)
+            xb.copy_(torch.view_as_real(torch.from_numpy(np.ascontiguousarray(f))))
+
+    def axis0(self, k=0, K=1):
         P, q = self.lay.size, self.lay.rank
         c = self.n1 // P
-        k1 = np.arange(q * c, (q + 1) * c)
         nh = self.n2 // 2 + 1
-        lam = (self.lam[0][:, None, None] + self.lam[1][k1][None, :, None]) + self.lam[2][:nh][None, None, :]
-        if q == 0:
+        if self.xchg is None:
+            tb, c0, w = self.trans, 0, nh
+        else:
+            _, tb, c0, w = self._blocks(k, K)
+            if w <= 0:
+                return
+        t = torch.view_as_complex(tb.contiguous()).numpy()
+        f = np.fft.fft(t, axis=0)
+        k1 = np.arange(q * c, (q + 1) * c)
+        lam = (self.lam[0][:, None, None] + self.lam[1][k1][None, :, None]) + self.lam[2][c0:c0 + w][None, None, :]
+        zero = q == 0 and c0 == 0
+        if zero:
             lam[0, 0, 0] = 1.0
         f = f / lam
-        if q == 0:
+        if zero:
             f[0, 0, 0] = 0.0
-        self.trans.copy_(torch.view_as_real(torch.from_numpy(np.fft.ifft(f, axis=0))))
+        tb.copy_(torch.view_as_real(torch.from_numpy(np.fft.ifft(f, axis=0))))
 
-    def inverse(self):
-        if self.xchg is not None:
-            P, m = self.lay.size, self.lay.m
-            c = self.n1 // P
-            self.spec.view(m, P, c, -1, 2).copy_(self.xchg.permute(1, 0, 2, 3, 4))
+    def c2r(self):
         s = torch.view_as_complex(self.spec).numpy()
-        p = np.fft.irfft(np.fft.ifft(s, axis=1), n=self.n2, axis=2)
+        p = np.fft.irfft(s, n=self.n2, axis=2)
         self.p_local.copy_(torch.from_numpy(np.ascontiguousarray(p)))
 
     def correct(self, u, p_ext=None):
