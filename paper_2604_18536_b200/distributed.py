@@ -112,12 +112,23 @@ class Comm:
 
     def halo(self, tensors):
         """Ghost planes along axis 0: plane 0 <- prev's last plane,
-        plane m+1 <- next's first plane."""
+        plane m+1 <- next's first plane (all tensors' planes in one batch of
+        P2P operations over NCCL)."""
         lay = self.layout
         m = lay.m
+        if lay.size == 1 or self.stage_host:
+            for t in tensors:
+                self._send_recv(t[m], t[0], lay.next, lay.prev)
+                self._send_recv(t[1], t[m + 1], lay.prev, lay.next)
+            return
+        ops = []
         for t in tensors:
-            self._send_recv(t[m], t[0], lay.next, lay.prev)
-            self._send_recv(t[1], t[m + 1], lay.prev, lay.next)
+            ops.append(dist.P2POp(dist.isend, t[m], lay.next, self.group))
+            ops.append(dist.P2POp(dist.irecv, t[0], lay.prev, self.group))
+            ops.append(dist.P2POp(dist.isend, t[1], lay.prev, self.group))
+            ops.append(dist.P2POp(dist.irecv, t[m + 1], lay.next, self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
 
     def plane_from_next(self, send_plane, recv_plane):
         self._send_recv(send_plane, recv_plane, self.layout.prev, self.layout.next)
