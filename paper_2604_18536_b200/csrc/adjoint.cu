@@ -221,6 +221,12 @@ __global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, C
                                                             int chunk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);  // [slot][6][PS]: vbar0..2, u0..2
+  // stencil tables staged in shared memory (wrapped indices, see below):
+  // axis 1 per tile row, axis 2 per tile column, axis 0 per plane (two
+  // alternating sets of planes i-1, i, i+1)
+  T* tbj = ring + kPbRing * kPbNE;      // [SFB_NTAB][kPbPH]
+  T* tbk = tbj + SFB_NTAB * kPbPH;      // [SFB_NTAB][kPbPW]
+  T* tbi = tbk + SFB_NTAB * kPbPW;      // [2][SFB_NTAB][3]
   const int tk = threadIdx.x, tj = threadIdx.y, tid = tj * kPbTK + tk;
   const int k0 = 1 + blockIdx.x * kPbTK, j0 = 1 + blockIdx.y * kPbTJ;
   const int ib = 1 + blockIdx.z * chunk;
@@ -250,9 +256,15 @@ __global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, C
   };
   const int j = j0 + tj, k = k0 + tk;
   const bool inside = j <= n1 && k <= n2;
-  // wrapped neighbour indices for the per-axis tables (own_lo at n+1 is not
-  // a periodic image in the reference tables, so always index wrapped)
-  const int jm = wr(j - 1, n1), jp = wr(j + 1, n1), km = wr(k - 1, n2), kp = wr(k + 1, n2);
+  for (int e = tid; e < SFB_NTAB * kPbPH; e += kPbNT) {
+    const int sl = e / kPbPH, r = e - sl * kPbPH;
+    tbj[e] = tab(G, 1, sl, wr(min(j0 - 1 + r, n1 + 1), n1));
+  }
+  for (int e = tid; e < SFB_NTAB * kPbPW; e += kPbNT) {
+    const int sl = e / kPbPW, r = e - sl * kPbPW;
+    tbk[e] = tab(G, 2, sl, wr(min(k0 - 1 + r, n2 + 1), n2));
+  }
+
 
   int sl_m = (ib - 1) % kPbRing;
   load_plane(ib - 1, sl_m);
@@ -264,6 +276,10 @@ __global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, C
   const int c0 = (tj + 1) * kPbPW + (tk + 1);
   long long x = (long long)ib * s0 + (long long)j * s1 + k;
   for (int i = ib; i < ie; ++i, x += s0) {
+    if (tid < SFB_NTAB * 3) {
+      const int sl = tid / 3, o = tid - sl * 3;
+      tbi[((i & 1) * SFB_NTAB + sl) * 3 + o] = tab(G, 0, sl, wr(i - 1 + o, n0));
+    }
     T accin[3] = {T(0), T(0), T(0)};
     if (ACC && inside) {
 #pragma unroll
@@ -282,17 +298,22 @@ __global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, C
       const T* P[3] = {ring + sl_m * kPbNE + c0, ring + s1i * kPbNE + c0, ring + s2i * kPbNE + c0};
       // field f at offset (d0, d1, d2), f in 0..2 vbar, 3..5 u
       auto R = [&](int f, int d0, int d1, int d2) -> T { return P[1 + d0][f * kPbPS + d1 * kPbPW + d2]; };
-      const int im = wr(i - 1, n0), ipn = wr(i + 1, n0);
-      const int Jc[3] = {i, j, k}, Jm[3] = {im, jm, km}, Jp[3] = {ipn, jp, kp};
+      // table value of axis ax, slot sl at the cell's index + off (wrapped)
+      const T* ti = tbi + (i & 1) * SFB_NTAB * 3;
+      auto TB = [&](int ax, int sl, int off) -> T {
+        if (ax == 0) return ti[sl * 3 + 1 + off];
+        if (ax == 1) return tbj[sl * kPbPH + tj + 1 + off];
+        return tbk[sl * kPbPW + tk + 1 + off];
+      };
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         int ec[3] = {0, 0, 0};
         ec[c] = 1;
         T acc = T(0);
         {  // (i) a = b = c
-          const T l_m = R(c, -ec[0], -ec[1], -ec[2]) * tab(G, c, T_RDU, Jm[c]);
-          const T l_0 = R(c, 0, 0, 0) * tab(G, c, T_RDU, Jc[c]);
-          const T l_p = R(c, ec[0], ec[1], ec[2]) * tab(G, c, T_RDU, Jp[c]);
+          const T l_m = R(c, -ec[0], -ec[1], -ec[2]) * TB(c, T_RDU, -1);
+          const T l_0 = R(c, 0, 0, 0) * TB(c, T_RDU, 0);
+          const T l_p = R(c, ec[0], ec[1], ec[2]) * TB(c, T_RDU, 1);
           const T u_m = R(3 + c, -ec[0], -ec[1], -ec[2]);
           const T u_0 = R(3 + c, 0, 0, 0);
           const T u_p = R(3 + c, ec[0], ec[1], ec[2]);
@@ -304,27 +325,27 @@ __global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, C
           int eb[3] = {0, 0, 0};
           eb[b] = 1;
           {  // (ii) a = c, b != c
-            const T l_m = R(c, -eb[0], -eb[1], -eb[2]) * tab(G, b, T_RDX, Jm[b]);
-            const T l_0 = R(c, 0, 0, 0) * tab(G, b, T_RDX, Jc[b]);
-            const T l_p = R(c, eb[0], eb[1], eb[2]) * tab(G, b, T_RDX, Jp[b]);
-            const T wl = tab(G, c, T_WLO, Jc[c]), wh = tab(G, c, T_WHI, Jc[c]);
+            const T l_m = R(c, -eb[0], -eb[1], -eb[2]) * TB(b, T_RDX, -1);
+            const T l_0 = R(c, 0, 0, 0) * TB(b, T_RDX, 0);
+            const T l_p = R(c, eb[0], eb[1], eb[2]) * TB(b, T_RDX, 1);
+            const T wl = TB(c, T_WLO, 0), wh = TB(c, T_WHI, 0);
             const T V0 = wl * R(3 + b, 0, 0, 0) + wh * R(3 + b, ec[0], ec[1], ec[2]);
             const T Vm = wl * R(3 + b, -eb[0], -eb[1], -eb[2]) + wh * R(3 + b, ec[0] - eb[0], ec[1] - eb[1], ec[2] - eb[2]);
             acc += T(0.5) * ((l_p - l_0) * V0 + (l_0 - l_m) * Vm);
           }
           {  // (iii) transporting component c inside F_ac, a = b
             const int a = b;
-            const T rc0 = tab(G, c, T_RDX, Jc[c]);
-            const T rcp = tab(G, c, T_RDX, Jp[c]);
+            const T rc0 = TB(c, T_RDX, 0);
+            const T rcp = TB(c, T_RDX, 1);
             {
               const T fb = R(a, ec[0], ec[1], ec[2]) * rcp - R(a, 0, 0, 0) * rc0;
               const T tt = (R(3 + a, 0, 0, 0) + R(3 + a, ec[0], ec[1], ec[2])) * T(0.5);
-              acc += fb * tt * tab(G, a, T_WLO, Jc[a]);
+              acc += fb * tt * TB(a, T_WLO, 0);
             }
             {
               const T fb = R(a, ec[0] - eb[0], ec[1] - eb[1], ec[2] - eb[2]) * rcp - R(a, -eb[0], -eb[1], -eb[2]) * rc0;
               const T tt = (R(3 + a, -eb[0], -eb[1], -eb[2]) + R(3 + a, ec[0] - eb[0], ec[1] - eb[1], ec[2] - eb[2])) * T(0.5);
-              acc += fb * tt * tab(G, a, T_WHI, Jm[a]);
+              acc += fb * tt * TB(a, T_WHI, -1);
             }
           }
         }
@@ -338,8 +359,8 @@ __global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, C
             const int shi = (b == c) ? T_OHI : T_THI, slo = (b == c) ? T_OLO : T_TLO;
             const T vm = R(c, -eb[0], -eb[1], -eb[2]);
             const T vp = R(c, eb[0], eb[1], eb[2]);
-            ad += vm * tab(G, b, shi, Jm[b]) - vc * (tab(G, b, shi, Jc[b]) + tab(G, b, slo, Jc[b])) +
-                  vp * tab(G, b, slo, Jp[b]);
+            ad += vm * TB(b, shi, -1) - vc * (TB(b, shi, 0) + TB(b, slo, 0)) +
+                  vp * TB(b, slo, 1);
           }
           acc += nu * ad;
         }
@@ -354,7 +375,7 @@ __global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, C
 
 template <typename T>
 static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int diff, int accumulate, cudaStream_t st) {
-  const size_t smem = (size_t)kPbRing * kPbNE * sizeof(T);
+  const size_t smem = ((size_t)kPbRing * kPbNE + SFB_NTAB * (kPbPH + kPbPW + 6)) * sizeof(T);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_rhs_pb_march<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
