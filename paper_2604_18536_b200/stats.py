@@ -123,3 +123,77 @@ def accumulate_stats(snapshots, bcs, nu, wall_axis=1, nut_snapshots=None):
     return StatProfile(y=y, y_plus=y / nu, u_mean=u_mean, rms=_tmean(per["rms"]), u3=_tmean(per["u3"]),
                        u4=_tmean(per["u4"]), uuv=_tmean(per["uuv"]), uw=_tmean(per["uw"]), nut_over_nu=nut_over_nu,
                        u_tau=u_tau, n_snapshots=len(snapshots))
+
+
+# ---------------------------------------------------------------------------
+# file formats (stats.py:170-228, csvio.py:1-31): the reference's byte layout,
+# so profiles and snapshots written here are read by stagflow and vice versa
+# ---------------------------------------------------------------------------
+def _atomic_write(path, data, mode):
+    import os
+    import tempfile
+
+    d = os.path.dirname(os.path.abspath(path))
+    fd, tmp = tempfile.mkstemp(dir=d, prefix=".tmp-")
+    try:
+        with os.fdopen(fd, mode) as fh:
+            if callable(data):
+                data(fh)
+            else:
+                fh.write(data)
+        os.replace(tmp, path)
+    except BaseException:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+        raise
+
+
+def write_profile_csv(path, profile):
+    """stats.py:170-178 + csvio.write_csv: schema comment, header, full-
+    precision floats, one row per wall-normal point."""
+    names = profile.column_names()
+    lines = ["# stagflow-csv v1 stat-profile", ",".join(names)]
+    for r in profile.rows():
+        lines.append(",".join(repr(float(v)) for v in r))
+    _atomic_write(str(path), "\n".join(lines) + "\n", "w")
+
+
+def _host_components(u):
+    comps = []
+    for c in u.u:
+        a = c.detach().cpu().numpy() if hasattr(c, "detach") else np.asarray(c)
+        comps.append(np.ascontiguousarray(a, dtype=a.dtype.newbyteorder("<")))
+    return comps
+
+
+def write_snapshot(path_base, u, t):
+    """stats.py:181-211: raw little-endian dump of the extended components
+    plus a text sidecar (time, dtype, components, shapes), both atomic."""
+    comps = _host_components(u)
+
+    def dump(fh):
+        for c in comps:
+            c.tofile(fh)
+
+    _atomic_write(str(path_base) + ".bin", dump, "wb")
+    lines = [f"time {t!r}", f"dtype {comps[0].dtype.name}", f"components {len(comps)}"]
+    for i, c in enumerate(comps):
+        lines.append(f"shape{i} " + " ".join(str(n) for n in c.shape))
+    _atomic_write(str(path_base) + ".txt", "\n".join(lines) + "\n", "w")
+
+
+def read_snapshot(path_base):
+    """stats.py:214-228: inverse of write_snapshot; returns (arrays, time)."""
+    meta = {}
+    with open(str(path_base) + ".txt") as fh:
+        for line in fh:
+            key, _, rest = line.strip().partition(" ")
+            meta[key] = rest
+    dtype = np.dtype(meta["dtype"]).newbyteorder("<")
+    n = int(meta["components"])
+    shapes = [tuple(int(v) for v in meta[f"shape{i}"].split()) for i in range(n)]
+    arrays = []
+    with open(str(path_base) + ".bin", "rb") as fh:
+        for shape in shapes:
+            arrays.append(np.fromfile(fh, dtype=dtype, count=int(np.prod(shape))).reshape(shape))
+    return arrays, float(meta["time"])

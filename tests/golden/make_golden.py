@@ -285,6 +285,9 @@ def main():
         out[f"{tag}_rows"] = prof.rows()
         out[f"{tag}_u_tau"] = prof.u_tau
     save("stats_channel", **out)
+    # the reference's file formats for the same profile / snapshot
+    stats.write_profile_csv(os.path.join(OUT, "stats_profile_ref.csv"), prof)
+    stats.write_snapshot(os.path.join(OUT, "snapshot_ref"), snaps[0], 0.125)
 
     # ---- adjoint: project pullback and unrolled gradient (RK4, 1 and 2 steps)
     rng = np.random.default_rng(3)
