@@ -8,6 +8,7 @@ namespace sfb {
 // lengths with an instantiated (A, B) engine (fft_reg_{d,f}{1,2}.cu)
 bool reg_factor(int L, RegLen& R) {
   static const int tab[][3] = {{840, 28, 30}, {420, 20, 21}, {512, 16, 32}, {256, 16, 16}, {1024, 32, 32},
+                               {1680, 40, 42},
                                {16, 4, 4},    {20, 4, 5},    {24, 4, 6},    {32, 4, 8},    {40, 5, 8},
                                {48, 6, 8},    {64, 8, 8},    {96, 8, 12},   {128, 8, 16},  {192, 12, 16},
                                {384, 16, 24}};

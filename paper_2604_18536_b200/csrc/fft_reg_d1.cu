@@ -12,6 +12,7 @@ int reg_tu_d1(int L, const RegCall& c, cudaStream_t st) {
     case 512: return reg_launch<double, 16, 32>(c, st);
     case 256: return reg_launch<double, 16, 16>(c, st);
     case 1024: return reg_launch<double, 32, 32>(c, st);
+    case 1680: return reg_launch<double, 40, 42>(c, st);
     default: return -1;
   }
 }

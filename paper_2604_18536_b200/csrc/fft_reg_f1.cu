@@ -12,6 +12,7 @@ int reg_tu_f1(int L, const RegCall& c, cudaStream_t st) {
     case 512: return reg_launch<float, 16, 32>(c, st);
     case 256: return reg_launch<float, 16, 16>(c, st);
     case 1024: return reg_launch<float, 32, 32>(c, st);
+    case 1680: return reg_launch<float, 40, 42>(c, st);
     default: return -1;
   }
 }

@@ -38,18 +38,19 @@
 
 namespace sfb {
 
-// W_N^j = exp(-2 pi i j / N) for sub-DFT sizes N <= 32 (index N*32 + j).
+// W_N^j = exp(-2 pi i j / N) for sub-DFT sizes N <= kTwN (index N*kTwN + j).
 // Internal linkage: every translation unit that instantiates kernels owns a
 // copy and uploads it through its reg_tu_*_init() (fft_reg.cu calls them all).
-static __constant__ double2 c_twd[33 * 32];
-static __constant__ float2 c_twf[33 * 32];
+constexpr int kTwN = 42;  // largest sub-DFT (1680 = 40 x 42)
+static __constant__ double2 c_twd[(kTwN + 1) * kTwN];
+static __constant__ float2 c_twf[(kTwN + 1) * kTwN];
 
 template <typename C>
 __device__ __forceinline__ C ctw(int N, int j);
 template <>
-__device__ __forceinline__ double2 ctw<double2>(int N, int j) { return c_twd[N * 32 + j]; }
+__device__ __forceinline__ double2 ctw<double2>(int N, int j) { return c_twd[N * kTwN + j]; }
 template <>
-__device__ __forceinline__ float2 ctw<float2>(int N, int j) { return c_twf[N * 32 + j]; }
+__device__ __forceinline__ float2 ctw<float2>(int N, int j) { return c_twf[N * kTwN + j]; }
 
 __host__ __device__ constexpr bool rdft_base(int N) { return N == 2 || N == 3 || N == 4 || N == 5 || N == 7 || N == 8; }
 
@@ -103,6 +104,7 @@ __device__ __forceinline__ C twmul_c(C x, int j) {
 // In-register DFT of N points (natural order in, natural order out).
 template <typename C, int N, bool INV>
 __device__ __forceinline__ void rdft(C* v) {
+  static_assert(N <= kTwN, "rdft: sub-DFT larger than the twiddle table");
 #ifdef SFB_REG_NOCOMPUTE
   if (true) return;
 #endif
@@ -540,13 +542,13 @@ struct RegCall {
 };
 
 static int reg_upload_tables() {
-  static double2 hd[33 * 32];
-  static float2 hf[33 * 32];
-  for (int N = 1; N <= 32; ++N)
-    for (int j = 0; j < 32; ++j) {
+  static double2 hd[(kTwN + 1) * kTwN];
+  static float2 hf[(kTwN + 1) * kTwN];
+  for (int N = 1; N <= kTwN; ++N)
+    for (int j = 0; j < kTwN; ++j) {
       const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)(j % N) / (long double)N;
-      hd[N * 32 + j] = make_double2((double)cosl(a), (double)sinl(a));
-      hf[N * 32 + j] = make_float2((float)cosl(a), (float)sinl(a));
+      hd[N * kTwN + j] = make_double2((double)cosl(a), (double)sinl(a));
+      hf[N * kTwN + j] = make_float2((float)cosl(a), (float)sinl(a));
     }
   if (cudaMemcpyToSymbol(c_twd, hd, sizeof(hd)) != cudaSuccess) return -1;
   if (cudaMemcpyToSymbol(c_twf, hf, sizeof(hf)) != cudaSuccess) return -1;

@@ -1,5 +1,5 @@
-timeout 600 python -m pytest tests/test_distributed_gpu.py -q 2>&1 | tail -2
-SFB_SLAB_CHUNKS=1 timeout 600 python -m pytest tests/test_distributed_gpu.py -q 2>&1 | tail -1
-SFB_SLAB_CHUNKS=3 timeout 600 python -m pytest tests/test_distributed_gpu.py -q 2>&1 | tail -1
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -1
-timeout 300 python bench.py --slab --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('slab', d['ms_per_step'], d['gpu_launches'])"
+rb() { SFB_NVCC_FLAGS="$1" python -c "
+import sys; sys.path.insert(0,'.')
+import runpy; m=runpy.run_path('paper_2604_18536_b200/build.py'); m['build'](force=True)"; }
+st() { ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"k_stage" -s 8 -c 8 --csv --log-file gpurun_out/nc.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; python profiles/parse_launches.py gpurun_out/nc.csv | head -5; }
+rb "-DSFB_STAGE_NOFILL"; st

@@ -48,10 +48,10 @@ def _solve(P, shape, dtype, monkeypatch, stockham):
     return got, ref
 
 
-# strided lengths 840 (28x30), 512 (16x32), 420 (20x21), 256, 96, 64, 48, 40;
+# strided lengths 1680 (40x42), 840 (28x30), 512 (16x32), 420 (20x21), 256, 96, 64, 48, 40;
 # real-trick half lengths 420, 256, 128, 48, 24, 20, 16
 @pytest.mark.parametrize("shape", [(840, 6, 8), (6, 840, 40), (512, 4, 16), (4, 420, 48), (256, 8, 840),
-                                   (96, 64, 512), (48, 40, 32), (840, 32)])
+                                   (96, 64, 512), (48, 40, 32), (840, 32), (1680, 4, 16), (6, 1680, 8)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_register_fft_solve_vs_oracle_and_stockham(P, shape, dtype, monkeypatch):
     got, ref = _solve(P, shape, dtype, monkeypatch, stockham=False)
