@@ -96,3 +96,13 @@ def test_fused_projection_paths(P, n, dtype, monkeypatch):
         assert rel(p, ref_p) <= 10 * t
     for a in range(3):
         assert rel(runs[0][0][a], runs[2][0][a]) <= t
+
+
+def test_rk4_step_at_256_cubed_vs_oracle(P, monkeypatch):
+    """One full RK4 step at 256^3 fp64 (16.8M cells, every default fusion on)
+    against the CPU oracle, cell for cell: parity at a production-sized grid,
+    not only at the small golden sizes (the oracle takes ~30 s here)."""
+    u, p, ref_u, ref_p = _rk4(P, (256, 256, 256), np.float64, monkeypatch, ())
+    for a in range(3):
+        assert rel(u[a], ref_u[a]) <= 1e-12, a
+    assert rel(p, ref_p) <= 1e-11
