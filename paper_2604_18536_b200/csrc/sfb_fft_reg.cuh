@@ -25,16 +25,21 @@
 
 #include <cstdlib>
 
-// minimum resident CTAs of the row kernels (register caps, 3 each): the
-// divergence-fused R2C at 3 CTAs/SM (96 registers, small spills) hides more
-// of its 11 scalar loads per point than 2 CTAs at 130 registers (5.17 vs
-// 5.48 ms at 840^3)
+// minimum resident CTAs of the row kernels.  fp64: 2 CTAs of 192 threads.
+// At 3 CTAs x 6 warps one SM sub-partition holds 5 warps, so ptxas caps the
+// row kernels at 96 registers and spills (the C2R's 104-byte stack); at 2 CTAs
+// they get 168 (840^3 step, 4 launches each: R2C+div 20.7 -> 19.0 ms, C2R
+// 9.4 -> 7.7 ms).  fp32 fits 96 registers without spills: 3 CTAs.
 #ifndef SFB_R2CDIV_MINB
-#define SFB_R2CDIV_MINB 3
+#define SFB_R2CDIV_MINB 2
 #endif
 #ifndef SFB_ROW_MINB
-#define SFB_ROW_MINB 3
+#define SFB_ROW_MINB 2
 #endif
+#ifndef SFB_ROW_MINB_F32
+#define SFB_ROW_MINB_F32 3
+#endif
+#define SFB_ROW_MINB_T(T, M) (sizeof(T) == 8 ? (M) : SFB_ROW_MINB_F32)
 
 namespace sfb {
 
@@ -149,16 +154,37 @@ struct RegGeo {
 #define SFB_REG_MINB 3
 #endif
   static constexpr int E = (int)(128 / sizeof(C));  // elements per 128-byte wavefront
-  static constexpr int W0 = (int)(SFB_REG_SEG / sizeof(C));
+#ifndef SFB_REG_SEG_F32
+#define SFB_REG_SEG_F32 SFB_REG_SEG
+#endif
+#ifndef SFB_REG_MINB_F32
+#define SFB_REG_MINB_F32 SFB_REG_MINB
+#endif
+#ifndef SFB_REG_MINB2
+#define SFB_REG_MINB2 SFB_REG_MINB
+#endif
+#ifndef SFB_REG_MINB2_F32
+#define SFB_REG_MINB2_F32 2
+#endif
+  static constexpr int SEG = sizeof(C) == 16 ? SFB_REG_SEG : SFB_REG_SEG_F32;
+  static constexpr int MB = sizeof(C) == 16 ? SFB_REG_MINB : SFB_REG_MINB_F32;
+  static constexpr int W0 = (int)(SEG / sizeof(C));
   static constexpr int W = (size_t)L * W0 * sizeof(C) <= 112 * 1024 ? W0 : W0 / 2;
   static constexpr int XS = A * W + (W < E ? ((W - (A * W) % E) % E + E) % E : 0);
   static constexpr int NT_S = W * TT;
   static constexpr size_t SMEM_S = ((size_t)B * XS + 32 + (L + 31) / 32) * sizeof(C);
-  static constexpr int MINB_S = SMEM_S * SFB_REG_MINB <= 220 * 1024 ? SFB_REG_MINB : 1;
+  static constexpr int MINB_S = SMEM_S * MB <= 220 * 1024 ? MB : 1;
+  // the fused fwd-scale-inverse axis-0 pass (MODE 2) holds two transforms'
+  // state; in fp32 it spills at 3 CTAs (80 registers at 8 warps per CTA)
+  static constexpr int MB2 = sizeof(C) == 16 ? SFB_REG_MINB2 : SFB_REG_MINB2_F32;
+  static constexpr int MINB_S2 = SMEM_S * MB2 <= 220 * 1024 ? MB2 : 1;
   // row passes: RP rows per CTA; exchange rows padded to an odd stride
   static constexpr int AP = (A % 2 == 0) ? A + 1 : A;
   static constexpr int ROWBUF = (B * AP > L + 1 ? B * AP : L + 1);
-  static constexpr int RP = (192 / TT) > 0 ? 192 / TT : 1;
+#ifndef SFB_ROW_NT
+#define SFB_ROW_NT 192
+#endif
+  static constexpr int RP = (SFB_ROW_NT / TT) > 0 ? SFB_ROW_NT / TT : 1;
   static constexpr int NT_R = RP * TT;
   static constexpr size_t SMEM_R = (size_t)RP * ROWBUF * sizeof(C);
 };
@@ -203,7 +229,8 @@ struct RowSplit {
 };
 
 template <typename T, int A, int B, int MODE>
-__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<typename CX<T>::t, A, B>::MINB_S)
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
+                                  MODE == 2 ? RegGeo<typename CX<T>::t, A, B>::MINB_S2 : RegGeo<typename CX<T>::t, A, B>::MINB_S)
     k_rfft_strided(const typename CX<T>::t* __restrict__ in, typename CX<T>::t* __restrict__ data, long long S,
                    int ncol, long long bin, long long bstride, RowSplit mp, const typename CX<T>::t* __restrict__ twL,
                    ScaleArgs sc) {
@@ -316,7 +343,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S, RegGeo<
 // contiguous-axis real transforms, M = A*B complex points per row (N = 2M reals)
 // ---------------------------------------------------------------------------
 template <typename T, int A, int B>
-__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB)
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_ROW_MINB))
     k_rfft_r2c(const T* __restrict__ in, typename CX<T>::t* __restrict__ out, long long rows, long long in_row,
                long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
   typedef typename CX<T>::t C;
@@ -389,7 +416,7 @@ __device__ __forceinline__ T div_at(const Geo<T>& G, const T* __restrict__ u0, c
 }
 
 template <typename T, int A, int B>
-__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_R2CDIV_MINB)
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_R2CDIV_MINB))
     k_rfft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, long long rows, long long out_row,
                    const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
   typedef typename CX<T>::t C;
@@ -457,7 +484,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_R2C
 }
 
 template <typename T, int A, int B>
-__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB)
+__global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_ROW_MINB))
     k_rfft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, long long rows, long long in_row,
                long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
   typedef typename CX<T>::t C;
