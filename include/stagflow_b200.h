@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SFB_ABI_VERSION 2
+#define SFB_ABI_VERSION 3
 
 enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4, SFB_ECONVERGE = 5 };
 enum { SFB_F64 = 0, SFB_F32 = 1 };
@@ -63,6 +63,7 @@ typedef struct sfb_grid_desc {
 
 typedef struct sfb_plan sfb_plan;
 typedef struct sfb_solver sfb_solver;
+typedef struct sfb_fft sfb_fft;
 
 /* Fused RK stage (timestep.py:186-207 + operators.py:218-238):
  *   k      = momentum_rhs(y)                  on velocity DOFs
@@ -220,6 +221,19 @@ int sfb_project_pullback(sfb_solver* s, void* const* vbar, void* const* out, voi
 /* Same, with out optional (NULL) and, if acc != NULL, acc += result on DOFs
  * (the g0 accumulation of step_backward, adjoint.py:412-415, fused). */
 int sfb_project_pullback_ex(sfb_solver* s, void* const* vbar, void* const* out, void* const* acc, void* stream);
+
+/* Real FFT backend (replaces stagflow.transforms.rfftn / irfftn,
+ * transforms.py:9-12, looked up by poisson.py:196,199): all axes of a
+ * contiguous C-order array of shape n[0..dim-1], dim 1..3.  rfftn writes the
+ * (n[0], .., n[dim-1]/2+1) half spectrum (interleaved complex); irfftn reads
+ * it (left untouched) and writes the real array normalised by 1/prod(n), as
+ * scipy.fft does.  2/3/5/7-smooth shapes with an even last axis run the
+ * hand-written engine, others cuFFT (sfb_fft_uses_own tells which). */
+int sfb_fft_create(int dim, const int* n, int dtype, sfb_fft** out);
+int sfb_fft_destroy(sfb_fft* f);
+int sfb_fft_uses_own(const sfb_fft* f);
+int sfb_rfftn(sfb_fft* f, const void* in, void* out, void* stream);
+int sfb_irfftn(sfb_fft* f, const void* in, void* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ SFB_F64, SFB_F32 = 0, 1
 SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC, SFB_BC_HALO = 0, 1, 2, 3
 SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL, SFB_SOLVER_CG = 0, 1, 2
 SFB_NTAB = 10
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 vp = ctypes.c_void_p
 VP3 = vp * 3
@@ -102,6 +102,11 @@ _SIGS = {
     "sfb_rhs_pullback": [vp, VP3, VP3, ctypes.c_double, VP3, ctypes.c_double, ctypes.c_int, vp],
     "sfb_project_pullback": [vp, VP3, VP3, vp],
     "sfb_project_pullback_ex": [vp, VP3, ctypes.POINTER(VP3), ctypes.POINTER(VP3), vp],
+    "sfb_fft_create": [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(vp)],
+    "sfb_fft_destroy": [vp],
+    "sfb_fft_uses_own": [vp],
+    "sfb_rfftn": [vp, vp, vp, vp],
+    "sfb_irfftn": [vp, vp, vp, vp],
 }
 
 EXPORTED = sorted(list(_SIGS) + ["sfb_abi_version", "sfb_last_error"])
@@ -159,6 +164,7 @@ KERNELS_PER_CALL = {
     "sfb_slab_axis0": 1, "sfb_slab_axis1": 1, "sfb_slab_c2r": 1, "sfb_slab_correct": 2,
 }
 launches = 0
+_FFT_PASSES = {}  # sfb_fft handle -> hand-written kernels per transform (transforms.py)
 
 
 def call(name, *args):
@@ -171,6 +177,9 @@ def call(name, *args):
         launches += k
         return
     k = KERNELS_PER_CALL.get(name, 0)
+    if name in ("sfb_rfftn", "sfb_irfftn"):
+        # engine passes (0 on the cuFFT path) + irfftn's normalisation kernel
+        k = _FFT_PASSES.get(args[0], 0) + (name == "sfb_irfftn")
     if name in ("sfb_project_pullback", "sfb_project_pullback_ex", "sfb_solver_solve"):
         own = lib.sfb_solver_uses_own_fft(args[0])
         k += 4 if own else 0

@@ -538,6 +538,61 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
 template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*);
 template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*);
 
+// Standalone unnormalised real transforms (the `transforms.rfftn/irfftn`
+// plugin, transforms.py:9-12): R2C along the contiguous axis, then forward
+// C2C passes along axes d-2 .. 0; the inverse runs the mirror image and
+// overwrites its complex input.
+template <typename T>
+int fft_forward(FftSolve& F, const T* in, void* out_v, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  C* out = (C*)out_v;
+  const size_t csz = sizeof(C);
+  const int dim = F.dim, nlast = F.n[dim - 1], nh = nlast / 2 + 1;
+  int rc;
+  if ((rc = launch_r2c<T>(F, in, out, F.total / nlast, st))) return rc;
+  ScaleArgs none{};
+  if (dim == 3) {
+    const int n0 = F.n[0], n1 = F.n[1];
+    if ((rc = launch_strided<T, 0>(out, F.ax[1], pick_w(n1, csz), nh, nh, (long long)n1 * nh, n0,
+                                   (const C*)F.tw_ax[1], none, st, nullptr, SFB_REG(F, 1))))
+      return rc;
+    return launch_strided<T, 0>(out, F.ax[0], pick_w(n0, csz), (long long)n1 * nh, n1 * nh, 0, 1,
+                                (const C*)F.tw_ax[0], none, st, nullptr, SFB_REG(F, 0));
+  }
+  if (dim == 2)
+    return launch_strided<T, 0>(out, F.ax[0], pick_w(F.n[0], csz), nh, nh, 0, 1, (const C*)F.tw_ax[0], none, st,
+                                nullptr, SFB_REG(F, 0));
+  return SFB_OK;
+}
+template int fft_forward<double>(FftSolve&, const double*, void*, cudaStream_t);
+template int fft_forward<float>(FftSolve&, const float*, void*, cudaStream_t);
+
+template <typename T>
+int fft_inverse(FftSolve& F, void* in_v, T* out, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  C* in = (C*)in_v;
+  const size_t csz = sizeof(C);
+  const int dim = F.dim, nlast = F.n[dim - 1], nh = nlast / 2 + 1;
+  int rc;
+  ScaleArgs none{};
+  if (dim == 3) {
+    const int n0 = F.n[0], n1 = F.n[1];
+    if ((rc = launch_strided<T, 1>(in, F.ax[0], pick_w(n0, csz), (long long)n1 * nh, n1 * nh, 0, 1,
+                                   (const C*)F.tw_ax[0], none, st, nullptr, SFB_REG(F, 0))))
+      return rc;
+    if ((rc = launch_strided<T, 1>(in, F.ax[1], pick_w(n1, csz), nh, nh, (long long)n1 * nh, n0,
+                                   (const C*)F.tw_ax[1], none, st, nullptr, SFB_REG(F, 1))))
+      return rc;
+  } else if (dim == 2) {
+    if ((rc = launch_strided<T, 1>(in, F.ax[0], pick_w(F.n[0], csz), nh, nh, 0, 1, (const C*)F.tw_ax[0], none, st,
+                                   nullptr, SFB_REG(F, 0))))
+      return rc;
+  }
+  return launch_c2r<T>(F, in, out, F.total / nlast, st);
+}
+template int fft_inverse<double>(FftSolve&, void*, double*, cudaStream_t);
+template int fft_inverse<float>(FftSolve&, void*, float*, cudaStream_t);
+
 // ---- slab-decomposed pieces (multi-GPU): F.n = {m local planes, n1, n2},
 // F.ax[0] is the global axis-0 length, F.sc.l1 offset to this rank's k1 chunk.
 // chunked exchange layout of the slab all-to-all: (P, m, c, nh), c = n1 / P;

@@ -60,6 +60,12 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const G
                       const void* const* u = nullptr);
 template <typename T>
 int fft_set_smem_limits();
+// unnormalised real transforms of a contiguous array (fft.cu): forward
+// R2C + C2C passes; inverse overwrites its complex input
+template <typename T>
+int fft_forward(FftSolve& F, const T* in, void* out, cudaStream_t st);
+template <typename T>
+int fft_inverse(FftSolve& F, void* in, T* out, cudaStream_t st);
 // the register engine can fuse the divergence of u into the R2C pass
 template <typename T>
 bool fft_divfuse_ok(const FftSolve& F, const Geo<T>& G);
