@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256, 4) k_fft_strided(typename CX<T>::t* __res
             v.x = 0;
             v.y = 0;
           } else {
-            const T f = T(1) / (T)lam * (T)sc.invN;
+            const T f = spec_rcp<T>(lam) * (T)sc.invN;
             v.x *= f;
             v.y *= f;
           }
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256, 4) k_fft_strided(typename CX<T>::t* __res
             v.x = 0;
             v.y = 0;
           } else {
-            const T f = T(1) / (T)lam * (T)sc.invN;
+            const T f = spec_rcp<T>(lam) * (T)sc.invN;
             v.x *= f;
             v.y *= f;
           }

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_tma(const __grid_constant__ CUten
             v.x = 0;
             v.y = 0;
           } else {
-            const T f = T(1) / (T)lam * (T)sc.invN;
+            const T f = spec_rcp<T>(lam) * (T)sc.invN;
             v.x *= f;
             v.y *= f;
           }

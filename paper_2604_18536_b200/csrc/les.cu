@@ -1,8 +1,9 @@
 // Eddy-viscosity closures on the GPU (les.py:58-417): the velocity gradient
 // at the pressure points, the six models' nu_t, and the divergence of the
 // modelled stress 2 nu_t S on the velocity DOFs.  One thread per cell; every
-// formula keeps the reference's operands and order (divisions by the width
-// tables, the four-corner averages, the degenerate-denominator rules).
+// formula keeps the reference's operands and order (the four-corner
+// averages, the degenerate-denominator rules); divisions by the width tables
+// are multiplications by their reciprocal tables (one rounding apart).
 // The sigma model's singular values are formed in fp64 from the
 // characteristic invariants (the reference uses numpy longdouble, les.py:168).
 #include <cmath>
@@ -21,7 +22,7 @@ __device__ __forceinline__ void grad_tensor(const Geo<T>& G, const CV<T>& U, con
 #pragma unroll
     for (int j = 0; j < 3; ++j) A[i][j] = T(0);
 #pragma unroll
-  for (int i = 0; i < D; ++i) A[i][i] = (U.c[i][x] - U.c[i][x - G.s[i]]) / tab(G, i, T_DX, I[i]);
+  for (int i = 0; i < D; ++i) A[i][i] = (U.c[i][x] - U.c[i][x - G.s[i]]) * tab(G, i, T_RDX, I[i]);
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -35,7 +36,7 @@ __device__ __forceinline__ void grad_tensor(const Geo<T>& G, const CV<T>& U, con
 #pragma unroll
         for (int oj = 0; oj < 2; ++oj) {
           const long long c = x + (long long)(oi - 1) * G.s[i] + (long long)(oj - 1) * G.s[j];
-          const T part = (U.c[i][c + G.s[j]] - U.c[i][c]) / tab(G, j, T_DU, I[j] - 1 + oj);
+          const T part = (U.c[i][c + G.s[j]] - U.c[i][c]) * tab(G, j, T_RDU, I[j] - 1 + oj);
           acc = first ? part : acc + part;
           first = false;
         }
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256) k_nut(Geo<T> G, CV<T> U, T c, T pexp, T* 
   T prod = T(1);
 #pragma unroll
   for (int a = 0; a < D; ++a) prod = prod * tab(G, a, T_DX, I[a]);
-  const T delta = pow(prod, T(1.0 / D));
+  const T delta = D == 3 ? cbrt(prod) : D == 2 ? sqrt(prod) : prod;
   const T cd2 = (c * delta) * (c * delta);
   T val = T(0);
   if (KIND == LES_SMAG || KIND == LES_QR) {
@@ -279,11 +280,11 @@ __global__ void __launch_bounds__(256) k_eddy(Geo<T> G, CV<T> U, const T* __rest
 #pragma unroll
         for (int o = 0; o < 2; ++o) {
           const long long c = x + o * sa;
-          T g = (ua[c] - ua[c - sa]) / tab(G, a, T_DX, I[a] + o);
+          T g = (ua[c] - ua[c - sa]) * tab(G, a, T_RDX, I[a] + o);
           g = g * nut[c];
           fl[o] = g * T(2);
         }
-        t = (fl[1] - fl[0]) / tab(G, a, T_DU, I[a]);
+        t = (fl[1] - fl[0]) * tab(G, a, T_RDU, I[a]);
       } else {
         // corner fluxes 2 nu_t S_ab at corners I_b - 1 and I_b along b
         const T* __restrict__ ub = U.c[b];
@@ -292,14 +293,14 @@ __global__ void __launch_bounds__(256) k_eddy(Geo<T> G, CV<T> U, const T* __rest
 #pragma unroll
         for (int o = 0; o < 2; ++o) {
           const long long c = x + (long long)(o - 1) * sb;
-          T sab = (ua[c + sb] - ua[c]) / tab(G, b, T_DU, I[b] - 1 + o);
-          sab = sab + (ub[c + sa] - ub[c]) / tab(G, a, T_DU, I[a]);
+          T sab = (ua[c + sb] - ua[c]) * tab(G, b, T_RDU, I[b] - 1 + o);
+          sab = sab + (ub[c + sa] - ub[c]) * tab(G, a, T_RDU, I[a]);
           T nc = nut[c] + nut[c + sa];
           nc = nc + (nut[c + sb] + nut[c + sa + sb]);
           nc = nc * T(0.25);
           fl[o] = sab * nc;
         }
-        t = (fl[1] - fl[0]) / tab(G, b, T_DX, I[b]);
+        t = (fl[1] - fl[0]) * tab(G, b, T_RDX, I[b]);
       }
       v += t;
     }

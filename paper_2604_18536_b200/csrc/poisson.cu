@@ -278,11 +278,12 @@ __global__ void k_spec_scale(typename CT<T>::type* __restrict__ c, const double*
 // channel: batched tridiagonal along y per (kx, kz)
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void k_tridiag(typename CT<T>::type* __restrict__ c, double2* __restrict__ dd, double* __restrict__ cp,
+__global__ void k_tridiag(typename CT<T>::type* c, double2* dd, double* __restrict__ cp,
                           const double* __restrict__ up, const double* __restrict__ lo, const double* __restrict__ di,
                           const double* __restrict__ dxy, const double* __restrict__ lx, const double* __restrict__ lz,
                           int n0, int n1, int nh, double invN) {
-  // dd: fp64 forward-sweep storage; aliases c for fp64 plans
+  // dd: fp64 forward-sweep storage; aliases c for fp64 plans (so neither is
+  // __restrict__: the chunked loads must stay ahead of the aliased stores)
   const int kz = blockIdx.x * blockDim.x + threadIdx.x;
   const int k0 = blockIdx.y;
   if (kz >= nh) return;
@@ -307,41 +308,64 @@ __global__ void k_tridiag(typename CT<T>::type* __restrict__ c, double2* __restr
   // (0,0): consistent singular Neumann system; drop the last row and pin
   // x_{n1-1} = 0, then restore the weighted zero mean below
   const int m = zero_mode ? n1 - 1 : n1;
+  // the sweeps are serial in j: loads are issued kTdU rows ahead so only one
+  // memory latency is exposed per kTdU steps
+  constexpr int kTdU = 8;
   double cprev = 0.0, dr = 0.0, dm = 0.0;
-  for (int j = 0; j < m; ++j) {
-    const typename CT<T>::type v = c[base + j * st];
-    const double l = lo[j + 1];
-    double b = di[j + 1] + (zero_mode ? 0.0 : lam);
-    if (j > 0) b -= l * cprev;
-    const double ib = 1.0 / b;
-    const double cj = up[j + 1] * ib;
-    dr = ((double)v.x - mr - l * dr) * ib;
-    dm = ((double)v.y - mi - l * dm) * ib;
-    cp[base + j * st] = cj;
-    cprev = cj;
-    dd[base + j * st] = make_double2(dr, dm);
+  for (int j0 = 0; j0 < m; j0 += kTdU) {
+    typename CT<T>::type vb[kTdU];
+#pragma unroll
+    for (int u = 0; u < kTdU; ++u)
+      if (j0 + u < m) vb[u] = c[base + (long long)(j0 + u) * st];
+#pragma unroll
+    for (int u = 0; u < kTdU; ++u) {
+      const int j = j0 + u;
+      if (j >= m) break;
+      const double l = lo[j + 1];
+      double b = di[j + 1] + (zero_mode ? 0.0 : lam);
+      if (j > 0) b -= l * cprev;
+      const double ib = 1.0 / b;
+      const double cj = up[j + 1] * ib;
+      dr = ((double)vb[u].x - mr - l * dr) * ib;
+      dm = ((double)vb[u].y - mi - l * dm) * ib;
+      cp[base + (long long)j * st] = cj;
+      cprev = cj;
+      dd[base + (long long)j * st] = make_double2(dr, dm);
+    }
   }
   double xr = 0.0, xi = 0.0;
   double sr = 0.0, si = 0.0, sw = 0.0;
-  for (int j = m - 1; j >= 0; --j) {
-    const double2 v = dd[base + j * st];
-    if (j == m - 1) {
-      xr = v.x;
-      xi = v.y;
-    } else {
-      const double cj = cp[base + j * st];
-      xr = v.x - cj * xr;
-      xi = v.y - cj * xi;
-    }
-    if (zero_mode) {
-      dd[base + j * st] = make_double2(xr, xi);
-      sr += dxy[j] * xr;
-      si += dxy[j] * xi;
-    } else {
-      typename CT<T>::type w;
-      w.x = (T)(xr * invN);
-      w.y = (T)(xi * invN);
-      c[base + j * st] = w;
+  for (int j1 = m - 1; j1 >= 0; j1 -= kTdU) {
+    double2 db[kTdU];
+    double cb[kTdU];
+#pragma unroll
+    for (int u = 0; u < kTdU; ++u)
+      if (j1 - u >= 0) {
+        db[u] = dd[base + (long long)(j1 - u) * st];
+        cb[u] = cp[base + (long long)(j1 - u) * st];
+      }
+#pragma unroll
+    for (int u = 0; u < kTdU; ++u) {
+      const int j = j1 - u;
+      if (j < 0) break;
+      const double2 v = db[u];
+      if (j == m - 1) {
+        xr = v.x;
+        xi = v.y;
+      } else {
+        xr = v.x - cb[u] * xr;
+        xi = v.y - cb[u] * xi;
+      }
+      if (zero_mode) {
+        dd[base + (long long)j * st] = make_double2(xr, xi);
+        sr += dxy[j] * xr;
+        si += dxy[j] * xi;
+      } else {
+        typename CT<T>::type w;
+        w.x = (T)(xr * invN);
+        w.y = (T)(xi * invN);
+        c[base + (long long)j * st] = w;
+      }
     }
   }
   if (zero_mode) {

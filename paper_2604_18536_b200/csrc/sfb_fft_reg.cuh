@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
         if (m == 0 && zmode) {
           v[k2] = czero<C>();
         } else {
-          const T f = T(1) / (T)lam * (T)sc.invN;
+          const T f = spec_rcp<T>(lam) * (T)sc.invN;
           v[k2].x *= f;
           v[k2].y *= f;
         }
