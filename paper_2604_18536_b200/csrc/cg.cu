@@ -12,8 +12,12 @@
 //
 // One iteration = 4 fused passes over the interior arrays (apply + p.Ap,
 // update + sums, centre + |r|^2, new direction) with deterministic two-pass
-// fp64 reductions that stay on the device; the host reads one small vector
-// per iteration for the convergence test (poisson.py:289-297).
+// fp64 reductions that stay on the device.  The stopping test
+// (poisson.py:289-297) runs on the device too: iterations are enqueued in
+// batches of kCgBatch (one captured CUDA graph), every kernel of an
+// iteration after convergence returns at once, and the host reads the
+// done flag once per batch -- same iterates, same iteration count and
+// residual history as one host round trip per iteration.
 #include <cmath>
 #include <cstdlib>
 
@@ -24,8 +28,9 @@ namespace sfb {
 
 namespace {
 constexpr int kCgNT = 256;
+constexpr int kCgBatch = 16;
 // device scalar slots
-enum { S_DENOM = 0, S_ALPHA, S_MX, S_MR, S_RR, S_N };
+enum { S_DENOM = 0, S_ALPHA, S_MX, S_MR, S_RR, S_BETA, S_TOLB, S_IT, S_DONE, S_FAIL, S_N };
 
 template <int NT>
 __device__ __forceinline__ double bsum(double v) {
@@ -69,7 +74,8 @@ __device__ __forceinline__ T weight(const Geo<T>& G, const int I[3]) {
 // ap = -W L p ; partial sums of p.ap
 template <typename T, int D>
 __global__ void __launch_bounds__(kCgNT) k_cg_apply(Geo<T> G, const T* __restrict__ p, T* __restrict__ ap,
-                                                    double* __restrict__ part) {
+                                                    double* __restrict__ part, const double* __restrict__ sc) {
+  if (sc[S_DONE] != 0.0) return;
   const long long total = (long long)G.n[0] * G.n[1] * (D == 3 ? G.n[2] : 1);
   long long ps[3];
   ps[D - 1] = 1;
@@ -114,6 +120,7 @@ template <typename T, int D, int MODE>
 __global__ void __launch_bounds__(kCgNT) k_cg_vec(Geo<T> G, const T* __restrict__ b, T* __restrict__ x,
                                                   T* __restrict__ r, T* __restrict__ p, const T* __restrict__ ap,
                                                   const double* __restrict__ sc, double* __restrict__ part, int nb) {
+  if ((MODE == 3 || MODE == 4) && sc[S_DONE] != 0.0) return;
   const long long total = (long long)G.n[0] * G.n[1] * (D == 3 ? G.n[2] : 1);
   double a0 = 0.0, a1 = 0.0;
   T alpha = T(0), mx = T(0), mr = T(0), m = T(0);
@@ -160,7 +167,10 @@ __global__ void __launch_bounds__(kCgNT) k_cg_vec(Geo<T> G, const T* __restrict_
 
 // p = p*beta + r
 template <typename T>
-__global__ void __launch_bounds__(kCgNT) k_cg_dir(T* __restrict__ p, const T* __restrict__ r, T beta, long long total) {
+__global__ void __launch_bounds__(kCgNT) k_cg_dir(T* __restrict__ p, const T* __restrict__ r,
+                                                  const double* __restrict__ sc, long long total) {
+  if (sc[S_DONE] != 0.0) return;
+  const T beta = (T)sc[S_BETA];
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x)
     p[t] = p[t] * beta + r[t];
 }
@@ -168,9 +178,12 @@ __global__ void __launch_bounds__(kCgNT) k_cg_dir(T* __restrict__ p, const T* __
 // second pass of the reductions; what = which scalars to form
 //  0: S_MX = sum/wtot (weighted mean of b)   1: S_RR = sum (|b|^2)
 //  2: S_DENOM, S_ALPHA = S_RR / S_DENOM       3: S_MX = sum0/wtot, S_MR = sum1/N
-//  4: S_RR = sum
+//  4: the end of an iteration (poisson.py:289-297): a non-positive p.Ap
+//     fails; else record |r|, stop at |r| <= tol |b|, else
+//     beta = |r_new|^2 / |r|^2
 __global__ void __launch_bounds__(kCgNT) k_cg_finish(const double* __restrict__ part, int nb, int what, double wtot,
-                                                     double ntot, double* __restrict__ sc) {
+                                                     double ntot, double* __restrict__ sc, double* __restrict__ hist) {
+  if (what >= 2 && sc[S_DONE] != 0.0) return;
   double a0 = 0.0, a1 = 0.0;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
     a0 += part[i];
@@ -184,8 +197,77 @@ __global__ void __launch_bounds__(kCgNT) k_cg_finish(const double* __restrict__ 
     case 1: sc[S_RR] = a0; break;
     case 2: sc[S_DENOM] = a0; sc[S_ALPHA] = sc[S_RR] / a0; break;  // r.r of the previous iterate
     case 3: sc[S_MX] = a0 / wtot; sc[S_MR] = a1 / ntot; break;
-    default: sc[S_RR] = a0; break;
+    default: {
+      if (!(sc[S_DENOM] > 0.0)) {
+        sc[S_FAIL] = 1.0;
+        sc[S_DONE] = 1.0;
+        break;
+      }
+      const int it = (int)sc[S_IT] + 1;
+      sc[S_IT] = it;
+      const double res = sqrt(a0);
+      hist[it] = res;
+      if (res <= sc[S_TOLB]) {
+        sc[S_DONE] = 1.0;
+      } else {
+        sc[S_BETA] = a0 / sc[S_RR];
+        sc[S_RR] = a0;
+      }
+      break;
+    }
   }
+}
+
+// arm the device-side stopping test after the initial residual
+__global__ void k_cg_arm(double* __restrict__ sc, double* __restrict__ hist, double tol) {
+  const double b_norm = sqrt(sc[S_RR]);
+  hist[0] = b_norm;
+  sc[S_TOLB] = tol * b_norm;
+  sc[S_IT] = 0.0;
+  sc[S_DONE] = 0.0;
+  sc[S_FAIL] = 0.0;
+}
+
+template <typename T>
+static void cg_iteration(sfb_solver* s, const Geo<T>& G, int nb, cudaStream_t st) {
+  T* x = (T*)s->cg_x;
+  T* r = (T*)s->cg_r;
+  T* pd = (T*)s->cg_p;
+  T* ap = (T*)s->cg_ap;
+  double* part = s->cg_part;
+  double* sc = s->cg_dsc;
+  const double wtot = s->cg_wtot, ntot = (double)s->plan->int_count;
+  SFB_DISPATCH_DIM(G.dim, D, (k_cg_apply<T, D><<<nb, kCgNT, 0, st>>>(G, pd, ap, part, sc)));
+  k_cg_finish<<<1, kCgNT, 0, st>>>(part, nb, 2, wtot, ntot, sc, s->cg_dhist);
+  SFB_DISPATCH_DIM(G.dim, D, (k_cg_vec<T, D, 3><<<nb, kCgNT, 0, st>>>(G, x, x, r, pd, ap, sc, part, nb)));
+  k_cg_finish<<<1, kCgNT, 0, st>>>(part, nb, 3, wtot, ntot, sc, s->cg_dhist);
+  SFB_DISPATCH_DIM(G.dim, D, (k_cg_vec<T, D, 4><<<nb, kCgNT, 0, st>>>(G, x, x, r, pd, ap, sc, part, nb)));
+  k_cg_finish<<<1, kCgNT, 0, st>>>(part, nb, 4, wtot, ntot, sc, s->cg_dhist);
+  k_cg_dir<T><<<nb, kCgNT, 0, st>>>(pd, r, sc, s->plan->int_count);
+}
+
+// capture kCgBatch iterations once per solver (all pointers are solver-owned)
+template <typename T>
+static void cg_capture(sfb_solver* s, const Geo<T>& G, int nb) {
+  s->cg_graph_tried = true;
+  if (getenv("SFB_CG_NOGRAPH")) return;
+  cudaStream_t cap = nullptr;
+  if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  s->cg_cap_stream = cap;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  for (int k = 0; k < kCgBatch; ++k) cg_iteration<T>(s, G, nb, cap);
+  cudaGraphExec_t ex = nullptr;
+  if (cudaStreamEndCapture(cap, &g) == cudaSuccess && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess)
+    s->cg_graph = ex;
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
 }
 
 template <typename T>
@@ -203,50 +285,69 @@ int cg_solve(sfb_solver* s, T* buf, cudaStream_t st) {
   double* sc = s->cg_dsc;
   double* hs = s->cg_hsc;
   const double wtot = s->cg_wtot, ntot = (double)total;
-  auto finish = [&](int what) {
-    k_cg_finish<<<1, kCgNT, 0, st>>>(part, nb, what, wtot, ntot, sc);
-  };
+  int rc;
+  if (s->cg_dhist_cap < s->cg_max_iter + 1) {
+    if (s->cg_dhist) cudaFree(s->cg_dhist);
+    s->cg_dhist = nullptr;
+    // the captured batch holds the old history pointer
+    if (s->cg_graph) cudaGraphExecDestroy((cudaGraphExec_t)s->cg_graph);
+    s->cg_graph = nullptr;
+    s->cg_graph_tried = false;
+    s->cg_dhist_cap = 0;
+    if ((rc = cuda_check(cudaMalloc(&s->cg_dhist, sizeof(double) * (s->cg_max_iter + 1)), "cudaMalloc(cg history)")))
+      return rc;
+    s->cg_dhist_cap = s->cg_max_iter + 1;
+  }
   auto pull = [&]() -> int {
-    int rc = cuda_check(cudaMemcpyAsync(hs, sc, sizeof(double) * S_N, cudaMemcpyDeviceToHost, st), "cg d2h");
-    if (rc) return rc;
+    int rc2 = cuda_check(cudaMemcpyAsync(hs, sc, sizeof(double) * S_N, cudaMemcpyDeviceToHost, st), "cg d2h");
+    if (rc2) return rc2;
     return cuda_check(cudaStreamSynchronize(st), "cg sync");
   };
-  int rc;
+  auto history = [&](int n) -> int {
+    s->cg_hist.assign(n + 1, 0.0);
+    int rc2 = cuda_check(cudaMemcpyAsync(s->cg_hist.data(), s->cg_dhist, sizeof(double) * (n + 1),
+                                         cudaMemcpyDeviceToHost, st), "cg history");
+    if (rc2) return rc2;
+    s->cg_iters = n;
+    return cuda_check(cudaStreamSynchronize(st), "cg sync");
+  };
   s->cg_hist.clear();
   s->cg_iters = 0;
   // b = -W (rhs - wmean(rhs)),  p = r = b
   SFB_DISPATCH_DIM(G.dim, D, (k_cg_vec<T, D, 0><<<nb, kCgNT, 0, st>>>(G, buf, x, r, pd, ap, sc, part, nb)));
-  finish(0);
+  k_cg_finish<<<1, kCgNT, 0, st>>>(part, nb, 0, wtot, ntot, sc, s->cg_dhist);
   SFB_DISPATCH_DIM(G.dim, D, (k_cg_vec<T, D, 1><<<nb, kCgNT, 0, st>>>(G, buf, x, r, pd, ap, sc, part, nb)));
-  finish(1);
+  k_cg_finish<<<1, kCgNT, 0, st>>>(part, nb, 1, wtot, ntot, sc, s->cg_dhist);
   if ((rc = cuda_check(cudaMemsetAsync(x, 0, sizeof(T) * total, st), "cg x = 0"))) return rc;
+  k_cg_arm<<<1, 1, 0, st>>>(sc, s->cg_dhist, s->cg_tol);
   SFB_LAUNCH_CHECK("cg init");
   if ((rc = pull())) return rc;
-  const double b_norm = std::sqrt(hs[S_RR]);
-  s->cg_hist.push_back(b_norm);
-  if (b_norm == 0.0) return cuda_check(cudaMemsetAsync(buf, 0, sizeof(T) * total, st), "cg zero");
-  double rs = hs[S_RR];
-  for (int it = 1; it <= s->cg_max_iter; ++it) {
-    SFB_DISPATCH_DIM(G.dim, D, (k_cg_apply<T, D><<<nb, kCgNT, 0, st>>>(G, pd, ap, part)));
-    finish(2);
-    SFB_DISPATCH_DIM(G.dim, D, (k_cg_vec<T, D, 3><<<nb, kCgNT, 0, st>>>(G, buf, x, r, pd, ap, sc, part, nb)));
-    finish(3);
-    SFB_DISPATCH_DIM(G.dim, D, (k_cg_vec<T, D, 4><<<nb, kCgNT, 0, st>>>(G, buf, x, r, pd, ap, sc, part, nb)));
-    finish(4);
-    SFB_LAUNCH_CHECK("cg iteration");
-    if ((rc = pull())) return rc;
-    if (!(hs[S_DENOM] > 0.0)) return fail(SFB_ENUMERIC, "pressure operator lost positive definiteness");
-    const double res = std::sqrt(hs[S_RR]);
-    s->cg_hist.push_back(res);
-    s->cg_iters = it;
-    if (res <= s->cg_tol * b_norm)
-      return cuda_check(cudaMemcpyAsync(buf, x, sizeof(T) * total, cudaMemcpyDeviceToDevice, st), "cg out");
-    const double rs_new = hs[S_RR];
-    const double beta = rs_new / rs;
-    rs = rs_new;
-    k_cg_dir<T><<<nb, kCgNT, 0, st>>>(pd, r, (T)beta, total);
-    SFB_LAUNCH_CHECK("cg direction");
+  if (std::sqrt(hs[S_RR]) == 0.0) {
+    s->cg_hist.assign(1, 0.0);
+    return cuda_check(cudaMemsetAsync(buf, 0, sizeof(T) * total, st), "cg zero");
   }
+  if (!s->cg_graph_tried) cg_capture<T>(s, G, nb);
+  int issued = 0;
+  while (issued < s->cg_max_iter) {
+    const int k = std::min(kCgBatch, s->cg_max_iter - issued);
+    if (k == kCgBatch && s->cg_graph) {
+      if ((rc = cuda_check(cudaGraphLaunch((cudaGraphExec_t)s->cg_graph, st), "cg graph launch"))) return rc;
+    } else {
+      for (int i = 0; i < k; ++i) cg_iteration<T>(s, G, nb, st);
+      SFB_LAUNCH_CHECK("cg iterations");
+    }
+    issued += k;
+    if ((rc = pull())) return rc;
+    if (hs[S_FAIL] != 0.0) {
+      if ((rc = history((int)hs[S_IT]))) return rc;
+      return fail(SFB_ENUMERIC, "pressure operator lost positive definiteness");
+    }
+    if (hs[S_DONE] != 0.0) {
+      if ((rc = history((int)hs[S_IT]))) return rc;
+      return cuda_check(cudaMemcpyAsync(buf, x, sizeof(T) * total, cudaMemcpyDeviceToDevice, st), "cg out");
+    }
+  }
+  if ((rc = history((int)hs[S_IT]))) return rc;
   char msg[160];
   snprintf(msg, sizeof msg, "pressure CG did not reach tol=%g in %d iterations", s->cg_tol, s->cg_max_iter);
   return fail(SFB_ECONVERGE, msg);
@@ -286,9 +387,11 @@ int cg_setup(sfb_solver* s) {
 }
 
 void cg_release(sfb_solver* s) {
-  void* bufs[] = {s->cg_x, s->cg_r, s->cg_p, s->cg_ap, s->cg_part, s->cg_dsc};
+  void* bufs[] = {s->cg_x, s->cg_r, s->cg_p, s->cg_ap, s->cg_part, s->cg_dsc, s->cg_dhist};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  if (s->cg_graph) cudaGraphExecDestroy((cudaGraphExec_t)s->cg_graph);
+  if (s->cg_cap_stream) cudaStreamDestroy((cudaStream_t)s->cg_cap_stream);
   if (s->cg_hsc) cudaFreeHost(s->cg_hsc);
 }
 

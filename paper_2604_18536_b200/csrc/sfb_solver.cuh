@@ -53,4 +53,11 @@ struct sfb_solver {
   void *cg_x = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_ap = nullptr;
   double *cg_part = nullptr, *cg_dsc = nullptr, *cg_hsc = nullptr;
   std::vector<double> cg_hist;
+  // device-driven iteration batches (cg.cu): residual history on the device,
+  // a captured graph of kCgBatch iterations, the stream it was captured on
+  double* cg_dhist = nullptr;
+  int cg_dhist_cap = 0;
+  void* cg_graph = nullptr;  // cudaGraphExec_t
+  void* cg_cap_stream = nullptr;
+  bool cg_graph_tried = false;
 };
