@@ -177,7 +177,9 @@ struct RegGeo {
   // the fused fwd-scale-inverse axis-0 pass (MODE 2) holds two transforms'
   // state; in fp32 it spills at 3 CTAs (80 registers at 8 warps per CTA)
   static constexpr int MB2 = sizeof(C) == 16 ? SFB_REG_MINB2 : SFB_REG_MINB2_F32;
-  static constexpr int MINB_S2 = SMEM_S * MB2 <= 220 * 1024 ? MB2 : 1;
+  // MODE 2 also stages the axis-0 eigenvalues (L doubles) in shared memory
+  static constexpr size_t SMEM_S2 = SMEM_S + (size_t)L * sizeof(double);
+  static constexpr int MINB_S2 = SMEM_S2 * MB2 <= 220 * 1024 ? MB2 : 1;
   // row passes: RP rows per CTA; exchange rows padded to an odd stride
   static constexpr int AP = (A % 2 == 0) ? A + 1 : A;
   static constexpr int ROWBUF = (B * AP > L + 1 ? B * AP : L + 1);
@@ -263,6 +265,12 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
     }
   }
   tw_fill(twlo, twhi, twL, A * B);
+  // MODE 2: the axis-0 eigenvalues in shared memory (kept out of registers:
+  // a per-thread preload of B of them spilled the fused pass)
+  double* l0s = reinterpret_cast<double*>(twhi + (A * B + 31) / 32);
+  if constexpr (MODE == 2) {
+    for (int i = threadIdx.x; i < A * B; i += blockDim.x) l0s[i] = __ldg(sc.l0 + i);
+  }
   __syncthreads();
   if (t < B) {
     const int n2 = t;
@@ -277,11 +285,6 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
   __syncthreads();
   if (t < A) {
     const int k1 = t;
-    double l0v[MODE == 2 ? B : 1];
-    if constexpr (MODE == 2) {
-#pragma unroll
-      for (int k2 = 0; k2 < B; ++k2) l0v[k2] = __ldg(sc.l0 + k1 + A * k2);
-    }
 #pragma unroll
     for (int n2 = 0; n2 < B; ++n2) v[n2] = buf[n2 * XS + k1 * W + w];
     rdft<C, B, INV1>(v);
@@ -299,7 +302,8 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
 #pragma unroll
       for (int k2 = 0; k2 < B; ++k2) {
         const int m = k1 + A * k2;
-        const double lam = sc.dim == 3 ? (l0v[k2] + lc) + l2v : l0v[k2] + lc;
+        const double l0 = l0s[m];
+        const double lam = sc.dim == 3 ? (l0 + lc) + l2v : l0 + lc;
         if (m == 0 && zmode) {
           v[k2] = czero<C>();
         } else {
@@ -590,7 +594,7 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
   if (!attr) {
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
-    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
+    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S2);
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
     cudaFuncSetAttribute(k_rfft_strided<T, A, B, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
     cudaFuncSetAttribute(k_rfft_r2c<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
@@ -606,7 +610,7 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     const RowSplit mp{c.map_c > 0 ? c.map_c : 1, c.map_sq, c.map_s};
     const C* tw = (const C*)c.twL;
 #define SFB_STRIDED(M)                                                                                     \
-  k_rfft_strided<T, A, B, M><<<grid, RG::NT_S, RG::SMEM_S, st>>>(src, d, c.S, c.ncol, bin, c.bstride, mp, tw, \
+  k_rfft_strided<T, A, B, M><<<grid, RG::NT_S, M == 2 ? RG::SMEM_S2 : RG::SMEM_S, st>>>(src, d, c.S, c.ncol, bin, c.bstride, mp, tw, \
                                                                  c.sc)
     switch (c.kind) {
       case 0: SFB_STRIDED(0); break;
