@@ -212,12 +212,18 @@ __global__ void __launch_bounds__(256) k_rhs_pb(Geo<T> G, CV<T> Vb, CV<T> U, MV<
 // periodically wrapped source indices (so no ghost values are read).  Same
 // arithmetic as conv_pb + diff_pb above.
 // ---------------------------------------------------------------------------
-constexpr int kPbTJ = 8, kPbTK = 32, kPbRing = 5;
+#ifndef SFB_PB_TJ
+#define SFB_PB_TJ 4
+#endif
+#ifndef SFB_PB_MINB
+#define SFB_PB_MINB 3
+#endif
+constexpr int kPbTJ = SFB_PB_TJ, kPbTK = 32, kPbRing = 5;
 constexpr int kPbPW = kPbTK + 2, kPbPH = kPbTJ + 2, kPbPS = kPbPW * kPbPH, kPbNE = 6 * kPbPS;
 constexpr int kPbNT = kPbTJ * kPbTK, kPbNQ = (kPbNE + kPbNT - 1) / kPbNT;
 
 template <typename T, int ACC>
-__global__ void __launch_bounds__(kPbNT, 2) k_rhs_pb_march(Geo<T> G, CV<T> Vb, CV<T> U, MV<T> O, T nu, int diff,
+__global__ void __launch_bounds__(kPbNT, SFB_PB_MINB) k_rhs_pb_march(Geo<T> G, CV<T> Vb, CV<T> U, MV<T> O, T nu, int diff,
                                                             int chunk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);  // [slot][6][PS]: vbar0..2, u0..2
