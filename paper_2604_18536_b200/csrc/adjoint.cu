@@ -70,10 +70,11 @@ __global__ void k_grad_pb(Geo<T> G, CV<T> V, T* __restrict__ out, Box B, T sign,
     }
     acc = sign * acc;
     if (divw) {
-      T w = T(1);
+      // 1 / W as the product of the reciprocal widths (no fp64 division)
+      T rw = T(1);
 #pragma unroll
-      for (int b = 0; b < D; ++b) w = w * tab(G, b, T_DX, J[b]);
-      acc = acc / w;
+      for (int b = 0; b < D; ++b) rw = rw * tab(G, b, T_RDX, J[b]);
+      acc = acc * rw;
     }
   }
   if (interior_out) {

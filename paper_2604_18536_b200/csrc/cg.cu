@@ -51,6 +51,18 @@ __device__ __forceinline__ double bsum(double v) {
 // interior cell t (row-major over n) -> 1-based indices
 template <int D>
 __device__ __forceinline__ void cell(const int n[3], long long t, int I[3]) {
+  if (t < (1LL << 32)) {  // 32-bit index arithmetic (64-bit division is a long sequence)
+    unsigned r = (unsigned)t;
+    if (D == 3) {
+      I[2] = 1 + (int)(r % (unsigned)n[2]);
+      r /= (unsigned)n[2];
+    } else {
+      I[2] = 0;
+    }
+    I[1] = 1 + (int)(r % (unsigned)n[1]);
+    I[0] = 1 + (int)(r / (unsigned)n[1]);
+    return;
+  }
   if (D == 3) {
     I[2] = 1 + (int)(t % n[2]);
     t /= n[2];

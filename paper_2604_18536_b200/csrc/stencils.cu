@@ -298,22 +298,37 @@ __device__ __forceinline__ double block_min(double v) {
   return v;
 }
 
-// mode 0: sum w*u*v  (KE when v == u), mode 1: min du/|u|
+// mode 0: sum w*u*v  (KE when v == u), mode 1: min du/|u|, reduced as
+// min(-|u|/du) = -max(|u| * (1/du)) (no fp64 division per point; the finish
+// inverts once)
 template <typename T, int D>
 __global__ void __launch_bounds__(256) k_reduce(Geo<T> G, CV<T> U, CV<T> V, int mode, double* __restrict__ part) {
   const long long total = (long long)G.n[0] * G.n[1] * (D == 3 ? G.n[2] : 1);
-  double acc = mode == 0 ? 0.0 : INFINITY;
+  const bool small = total < (1LL << 32);
+  double acc = 0.0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     int I[3];
-    long long r = t;
-    if (D == 3) {
-      I[2] = 1 + (int)(r % G.n[2]);
-      r /= G.n[2];
+    if (small) {  // 32-bit index arithmetic (64-bit division is a long sequence)
+      unsigned r = (unsigned)t;
+      if (D == 3) {
+        I[2] = 1 + (int)(r % (unsigned)G.n[2]);
+        r /= (unsigned)G.n[2];
+      } else {
+        I[2] = 0;
+      }
+      I[1] = 1 + (int)(r % (unsigned)G.n[1]);
+      I[0] = 1 + (int)(r / (unsigned)G.n[1]);
     } else {
-      I[2] = 0;
+      long long r = t;
+      if (D == 3) {
+        I[2] = 1 + (int)(r % G.n[2]);
+        r /= G.n[2];
+      } else {
+        I[2] = 0;
+      }
+      I[1] = 1 + (int)(r % G.n[1]);
+      I[0] = 1 + (int)(r / G.n[1]);
     }
-    I[1] = 1 + (int)(r % G.n[1]);
-    I[0] = 1 + (int)(r / G.n[1]);
     const long long x = lin<T, D>(G, I);
 #pragma unroll
     for (int a = 0; a < D; ++a) {
@@ -326,7 +341,7 @@ __global__ void __launch_bounds__(256) k_reduce(Geo<T> G, CV<T> U, CV<T> V, int 
         acc += (double)(w * ua * V.c[a][x]);
       } else {
         const T sp = ua < T(0) ? -ua : ua;
-        if (sp > T(0)) acc = fmin(acc, (double)(tab(G, a, T_DU, I[a]) / sp));
+        acc = fmin(acc, -(double)(sp * tab(G, a, T_RDU, I[a])));
       }
     }
   }
@@ -338,7 +353,7 @@ __global__ void k_finish(const double* __restrict__ part, int n, int mode, doubl
   double acc = mode == 0 ? 0.0 : INFINITY;
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc = mode == 0 ? acc + part[i] : fmin(acc, part[i]);
   double r = mode == 0 ? block_sum<256>(acc) : block_min<256>(acc);
-  if (threadIdx.x == 0) out[0] = r;
+  if (threadIdx.x == 0) out[0] = mode == 0 ? r : (r < 0.0 ? -1.0 / r : INFINITY);
 }
 
 template <typename T>
