@@ -391,7 +391,11 @@ static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int d
   }
   const int bx = (G.n[2] + kPbTK - 1) / kPbTK, by = (G.n[1] + kPbTJ - 1) / kPbTJ;
   const long long bps = (long long)bx * by;
-  long long want = (4LL * 148 * 2 + bps - 1) / bps;
+  // >= ~30 waves of resident CTAs (tail of the last partial wave), chunks of
+  // >= 64 planes (stage.cu: the same split)
+  long long want = (30LL * 148 * SFB_PB_MINB + bps - 1) / bps;
+  if (want > G.n[0] / 64) want = G.n[0] / 64;
+  if (want < 1) want = 1;
   int chunk = (int)((G.n[0] + want - 1) / want);
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;

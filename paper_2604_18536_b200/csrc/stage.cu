@@ -328,7 +328,15 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
   }
   const int bx = (G.n[2] + kTK - 1) / kTK, by = (G.n[1] + kTJ - 1) / kTJ;
   const long long bps = (long long)bx * by;
-  long long want = (4LL * 148 * MINB + bps - 1) / bps;  // ~4 waves of resident CTAs
+  // split the march into bz chunks so the launch is >= ~30 waves of resident
+  // CTAs: with one chunk (840^3: 2835 CTAs = 6.4 waves of 444) the last
+  // partial wave idled most of the GPU for a whole CTA lifetime (stage
+  // kernels 62.2 -> 57.4 ms per step at bz = 5); chunks stay >= 64 planes so
+  // the 3-plane ring refill per chunk costs < 5 %
+  long long want = (30LL * 148 * MINB + bps - 1) / bps;
+  if (want > G.n[0] / 64) want = G.n[0] / 64;
+  if (want < 1) want = 1;
+  if (getenv("SFB_STAGE_BZ")) want = atoi(getenv("SFB_STAGE_BZ"));
   int chunk = (int)((G.n[0] + want - 1) / want);
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;
