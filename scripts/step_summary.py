@@ -10,7 +10,7 @@ import parse_launches as PL  # noqa: E402
 k = PL.load(sys.argv[1])
 starts = [i for (i, name) in k if "k_stage_march" in name and ", 46," in name]
 first, last = starts[1], starts[2] - 1
-print(f"# one RK4 step (launch IDs {first}-{last} of {sys.argv[1]}), 840^3 fp64; ncu --metrics "
+print(f"# one RK4 step (launch IDs {first}-{last} of {sys.argv[1]}); ncu --metrics "
       "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
       "(serialised, cold-cache: compare shares)")
 sys.stdout.flush()
