@@ -204,7 +204,9 @@ static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t
     dim3 blk(64, 4);
     const int bx = (G.n[2] + 63) / 64, by = (G.n[1] + 3) / 4;
     const long long bps = (long long)bx * by;
-    long long want = (4LL * 148 * 8 + bps - 1) / bps;
+    long long want = (30LL * 148 * 8 + bps - 1) / bps;  // >= ~30 waves (stage.cu)
+    if (want > G.n[0] / 32) want = G.n[0] / 32;
+    if (want < 1) want = 1;
     int chunk = (int)((G.n[0] + want - 1) / want);
     if (chunk < 8) chunk = 8;
     const int bz = (G.n[0] + chunk - 1) / chunk;
