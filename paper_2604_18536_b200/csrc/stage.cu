@@ -306,7 +306,10 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
 #ifndef SFB_STAGE_CPT
 #define SFB_STAGE_CPT 2
 #endif
-constexpr int kTJ = SFB_STAGE_TJ, kTK = 32, kCPT = SFB_STAGE_CPT;
+#ifndef SFB_STAGE_TK
+#define SFB_STAGE_TK 32
+#endif
+constexpr int kTJ = SFB_STAGE_TJ, kTK = SFB_STAGE_TK, kCPT = SFB_STAGE_CPT;
 
 template <typename T, int FL>
 static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
