@@ -350,7 +350,9 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
 
 template <typename T>
 static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st, bool allow_per = true) {
-  const bool per = allow_per && G.per[0] && G.per[1] && G.per[2] && !G.halo[0] && !G.halo[1] && !G.halo[2] &&
+  // a halo axis 0 (z-slab) has no walls either: every local cell is a DOF, so
+  // the branch-free variant applies (its ring reads the exchanged ghost planes)
+  const bool per = allow_per && G.per[0] && G.per[1] && G.per[2] && !G.halo[1] && !G.halo[2] &&
                    !getenv("SFB_STAGE_NOPER");
   const int fl = (A.has_k ? FL_K : 0) | (A.has_s ? FL_S : 0) | (A.has_s && A.s_from_u0 ? FL_SU0 : 0) |
                  (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0) | (per ? FL_PER : 0);
