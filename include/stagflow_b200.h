@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SFB_ABI_VERSION 3
+#define SFB_ABI_VERSION 4
 
 enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4, SFB_ECONVERGE = 5 };
 enum { SFB_F64 = 0, SFB_F32 = 1 };
@@ -85,6 +85,10 @@ typedef struct sfb_stage_args {
    * forms y - G p on the fly, so the gradient-subtract pass and the ghost fill
    * of y are skipped.  All-periodic 3D plans only. */
   const void* p_int;
+  /* Optional per-DOF body force (sample_force of a callable,
+   * operators.py:241-259): extended arrays, one per component (all or none);
+   * replaces force[] and is added after diffusion (operators.py:228-235). */
+  const void* force_field[3];
 } sfb_stage_args;
 
 int sfb_abi_version(void);
@@ -104,7 +108,10 @@ int sfb_divergence(sfb_plan* plan, const void* const* u, void* out, void* stream
 int sfb_pressure_gradient(sfb_plan* plan, const void* p, void* const* out, void* stream);
 int sfb_convection(sfb_plan* plan, const void* const* u, void* const* out, int accumulate, void* stream);
 int sfb_diffusion(sfb_plan* plan, const void* const* u, double nu, void* const* out, int accumulate, void* stream);
-int sfb_momentum_rhs(sfb_plan* plan, const void* const* u, double nu, const double* force, void* const* out, void* stream);
+/* force: per-component constants (NULL = none); force_field: per-DOF
+ * extended force arrays (NULL, or NULL entries = use the constant). */
+int sfb_momentum_rhs(sfb_plan* plan, const void* const* u, double nu, const double* force,
+                     const void* const* force_field, void* const* out, void* stream);
 
 /* RK building blocks (timestep.py:166-214). */
 int sfb_rk_stage(sfb_plan* plan, const sfb_stage_args* args, void* stream);
@@ -204,6 +211,18 @@ int sfb_slab_axis1(sfb_solver* s, int chunk, int nchunks, int inverse, void* str
 int sfb_slab_axis0(sfb_solver* s, int chunk, int nchunks, void* stream);
 int sfb_slab_c2r(sfb_solver* s, void* stream);
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream);
+
+/* Adjoints of the ghost fills (adjoint.py:53-111): accumulate every ghost
+ * entry onto its source and zero the ghosts, axes in reverse order, for the
+ * plan's boundary kinds (periodic, Dirichlet, symmetric).  Any BCs. */
+int sfb_fold_ghosts_velocity(sfb_plan* plan, void* const* u, void* stream);
+int sfb_fold_ghosts_scalar(sfb_plan* plan, void* f, void* stream);
+/* zero_non_dofs_velocity / zero_ghosts_scalar (adjoint.py:32-50). */
+int sfb_zero_non_dofs_velocity(sfb_plan* plan, void* const* u, void* stream);
+int sfb_zero_ghosts_scalar(sfb_plan* plan, void* f, void* stream);
+/* poisson_solve_transpose (adjoint.py:236-250): out = W S W^-1 pbar on the
+ * interior of extended scalars (out's ghosts zeroed); any non-slab solver. */
+int sfb_solve_transpose(sfb_solver* s, const void* pbar, void* out, void* stream);
 
 /* Pullbacks (adjoint.py:114-349), periodic grids. Mutating semantics of the
  * reference are kept: divergence_pullback zeroes pbar's ghosts;

@@ -315,7 +315,8 @@ def convection(g, u, out=None):
 
 def momentum_rhs(g, u, nu, force=None, closure=None):
     """operators.py:218-238; ``force`` is a d-vector of constants
-    (operators.py:241-259 casts them to the grid dtype); ``closure`` is a
+    (operators.py:241-259 casts them to the grid dtype) or of DOF-shaped
+    arrays (a sampled callable, operators.py:249-258, operators.py:232-233); ``closure`` is a
     callable (g, u, out) that accumulates the eddy-stress term
     (operators.py:236-237, oracle/les_np.py)."""
     out = convection(g, u)
@@ -323,9 +324,12 @@ def momentum_rhs(g, u, nu, force=None, closure=None):
         diffusion(g, u, nu, out=out)
     if force is not None:
         for a in range(g.dim):
-            fa = g.dtype.type(force[a])
-            if fa != 0.0:
-                out[a][g.udof(a)] += fa
+            if np.ndim(force[a]) == 0:
+                fa = g.dtype.type(force[a])
+                if fa != 0.0:
+                    out[a][g.udof(a)] += fa
+            else:  # sampled per-DOF array (sample_force of a callable, operators.py:249-258)
+                out[a][g.udof(a)] += force[a]
     if closure is not None:
         closure(g, u, out)
     return out

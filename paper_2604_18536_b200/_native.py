@@ -17,7 +17,7 @@ SFB_F64, SFB_F32 = 0, 1
 SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC, SFB_BC_HALO = 0, 1, 2, 3
 SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL, SFB_SOLVER_CG = 0, 1, 2
 SFB_NTAB = 10
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 vp = ctypes.c_void_p
 VP3 = vp * 3
@@ -50,6 +50,7 @@ class StageArgs(ctypes.Structure):
         ("nu", ctypes.c_double),
         ("force", ctypes.c_double * 3),
         ("p_int", vp),
+        ("force_field", VP3),
     ]
 
 
@@ -63,7 +64,7 @@ _SIGS = {
     "sfb_pressure_gradient": [vp, vp, VP3, vp],
     "sfb_convection": [vp, VP3, VP3, ctypes.c_int, vp],
     "sfb_diffusion": [vp, VP3, ctypes.c_double, VP3, ctypes.c_int, vp],
-    "sfb_momentum_rhs": [vp, VP3, ctypes.c_double, ctypes.POINTER(ctypes.c_double), VP3, vp],
+    "sfb_momentum_rhs": [vp, VP3, ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(VP3), VP3, vp],
     "sfb_rk_stage": [vp, ctypes.POINTER(StageArgs), vp],
     "sfb_combine": [vp, VP3, VP3, ctypes.c_int, ctypes.POINTER(VP3), ctypes.POINTER(ctypes.c_double), vp],
     "sfb_wray_update": [vp, VP3, VP3, VP3, ctypes.c_double, ctypes.c_double, vp],
@@ -95,6 +96,11 @@ _SIGS = {
     "sfb_slab_axis0": [vp, ctypes.c_int, ctypes.c_int, vp],
     "sfb_slab_c2r": [vp, vp],
     "sfb_slab_correct": [vp, VP3, vp, vp],
+    "sfb_fold_ghosts_velocity": [vp, VP3, vp],
+    "sfb_fold_ghosts_scalar": [vp, vp, vp],
+    "sfb_zero_non_dofs_velocity": [vp, VP3, vp],
+    "sfb_zero_ghosts_scalar": [vp, vp, vp],
+    "sfb_solve_transpose": [vp, vp, vp, vp],
     "sfb_divergence_pullback": [vp, vp, VP3, vp],
     "sfb_pressure_gradient_pullback": [vp, VP3, vp, vp],
     "sfb_diffusion_pullback": [vp, VP3, ctypes.c_double, VP3, vp],
@@ -161,6 +167,8 @@ KERNELS_PER_CALL = {
     "sfb_plane_sums": 2, "sfb_sub_plane_mean": 1,
     "sfb_divergence_pullback": 2, "sfb_pressure_gradient_pullback": 2, "sfb_diffusion_pullback": 2,
     "sfb_convection_pullback": 2, "sfb_rhs_pullback": 2, "sfb_project_pullback": 4, "sfb_project_pullback_ex": 4,
+    "sfb_fold_ghosts_velocity": 3, "sfb_fold_ghosts_scalar": 3, "sfb_zero_non_dofs_velocity": 1,
+    "sfb_zero_ghosts_scalar": 1, "sfb_solve_transpose": 3,
     "sfb_slab_axis0": 1, "sfb_slab_axis1": 1, "sfb_slab_c2r": 1, "sfb_slab_correct": 2,
 }
 launches = 0
@@ -180,7 +188,7 @@ def call(name, *args):
     if name in ("sfb_rfftn", "sfb_irfftn"):
         # engine passes (0 on the cuFFT path) + irfftn's normalisation kernel
         k = _FFT_PASSES.get(args[0], 0) + (name == "sfb_irfftn")
-    if name in ("sfb_project_pullback", "sfb_project_pullback_ex", "sfb_solver_solve"):
+    if name in ("sfb_project_pullback", "sfb_project_pullback_ex", "sfb_solver_solve", "sfb_solve_transpose"):
         own = lib.sfb_solver_uses_own_fft(args[0])
         k += 4 if own else 0
     launches += k

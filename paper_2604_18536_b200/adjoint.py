@@ -25,28 +25,36 @@ def _require_periodic(bcs):
         raise ConfigurationError("the differentiable time-stepping path supports periodic boundaries only")
 
 
+def _grid_plan(grid, bcs=None):
+    from .operators import default_bcs
+
+    return get_plan(grid, bcs if bcs is not None else default_bcs(grid)).handle
+
+
 def zero_ghosts_scalar(f):
-    """adjoint.py:32-37"""
-    d = f.grid.dim
-    for a, n in enumerate(f.grid.shape):
-        idx = [slice(None)] * d
-        for i in (0, n + 1):
-            idx[a] = i
-            f.data[tuple(idx)] = 0.0
+    """adjoint.py:32-37 (one plane kernel)."""
+    N.call("sfb_zero_ghosts_scalar", _grid_plan(f.grid), f.data.data_ptr(), stream_ptr())
     return f
 
 
 def zero_non_dofs_velocity(v):
-    """adjoint.py:40-50"""
-    grid = v.grid
-    d = grid.dim
-    for c in range(d):
-        for a, n in enumerate(grid.shape):
-            idx = [slice(None)] * d
-            planes = [0, n + 1] + ([n] if (c == a and not grid.periodic[a]) else [])
-            for i in planes:
-                idx[a] = i
-                v.u[c][tuple(idx)] = 0.0
+    """adjoint.py:40-50 (one plane kernel)."""
+    N.call("sfb_zero_non_dofs_velocity", _grid_plan(v.grid), N.ptr3(v.u), stream_ptr())
+    return v
+
+
+def fold_ghosts_scalar(f, bcs):
+    """adjoint.py:53-71: adjoint of the scalar ghost fill -- every ghost is
+    accumulated onto its source and zeroed, axes in reverse order (one
+    kernel per axis)."""
+    N.call("sfb_fold_ghosts_scalar", get_plan(f.grid, bcs).handle, f.data.data_ptr(), stream_ptr())
+    return f
+
+
+def fold_ghosts_velocity(v, bcs):
+    """adjoint.py:74-111: adjoint of the velocity ghost fill (periodic,
+    Dirichlet and symmetric sides; reversed axis order)."""
+    N.call("sfb_fold_ghosts_velocity", get_plan(v.grid, bcs).handle, N.ptr3(v.u), stream_ptr())
     return v
 
 
@@ -111,25 +119,13 @@ def poisson_pullback(pbar, solver):
     return solver.solve(pbar)
 
 
-def _pweights(grid):
-    w = getattr(grid, "_pw_dev", None)
-    if w is None:
-        from .operators import pressure_weights
-
-        w = torch.from_numpy(pressure_weights(grid)).to(device=torch.device("cuda", torch.cuda.current_device()))
-        grid._pw_dev = w
-    return w
-
-
 def poisson_solve_transpose(pbar, solver):
-    """adjoint.py:236-250: W S W^-1 (exact on stretched grids too)."""
-    grid = pbar.grid
-    w = _pweights(grid)
-    tmp = ScalarField(grid)
-    tmp.interior.copy_(pbar.interior / w)
-    res = solver.solve(tmp)
-    out = ScalarField(grid)
-    out.interior.copy_(res.interior * w)
+    """adjoint.py:236-250: W S W^-1 (exact on stretched grids too): the
+    1/W scaling, the solve and the W scaling run natively
+    (``sfb_solve_transpose``)."""
+    s = _native_solver(solver, solver.bcs)
+    out = ScalarField(pbar.grid, empty=True)
+    N.call("sfb_solve_transpose", s.handle, pbar.data.data_ptr(), out.data.data_ptr(), stream_ptr())
     return out
 
 

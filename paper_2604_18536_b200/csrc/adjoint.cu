@@ -383,12 +383,9 @@ __global__ void __launch_bounds__(kPbNT, SFB_PB_MINB) k_rhs_pb_march(Geo<T> G, C
 template <typename T>
 static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int diff, int accumulate, cudaStream_t st) {
   const size_t smem = ((size_t)kPbRing * kPbNE + SFB_NTAB * (kPbPH + kPbPW + 6)) * sizeof(T);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_rhs_pb_march<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_rhs_pb_march<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  cudaError_t e = ensure_smem((const void*)k_rhs_pb_march<T, 0>, smem);
+  if (e == cudaSuccess) e = ensure_smem((const void*)k_rhs_pb_march<T, 1>, smem);
+  if (e != cudaSuccess) return cuda_check(e, "rhs pullback: shared-memory attribute");
   const int bx = (G.n[2] + kPbTK - 1) / kPbTK, by = (G.n[1] + kPbTJ - 1) / kPbTJ;
   const long long bps = (long long)bx * by;
   // >= ~30 waves of resident CTAs (tail of the last partial wave), chunks of
@@ -438,6 +435,41 @@ __global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T
     if (O.c[0]) O.c[a][x] = r;
     if (Acc.c[0]) Acc.c[a][x] += r;  // g0 += ybar_j (adjoint.py:414-415)
   }
+}
+
+// poisson_solve_transpose (adjoint.py:236-250): W S W^-1.  In: the interior
+// of an extended cotangent divided by the pressure volume W (the reference's
+// true division, W = dx0*dx1[*dx2] in the grid dtype); out: S's result times
+// W on the interior of an extended array, ghosts zero.
+template <typename T, int D>
+__global__ void k_wconj(Geo<T> G, const T* __restrict__ src, T* __restrict__ dst, Box B, int into_ext) {
+  int J[3];
+  if (!box_coords<D>(B, J)) return;
+  const bool dof = is_pdof<T, D>(G, J);
+  long long o = 0;
+  T w = T(1);
+  if (dof) {
+    o = (long long)(J[0] - 1) * G.n[1] + (J[1] - 1);
+    if (D == 3) o = o * G.n[2] + (J[2] - 1);
+#pragma unroll
+    for (int b = 0; b < D; ++b) w = w * tab(G, b, T_DX, J[b]);
+  }
+  if (into_ext) dst[lin<T, D>(G, J)] = dof ? src[o] * w : T(0);
+  else if (dof) dst[o] = src[lin<T, D>(G, J)] / w;
+}
+
+template <typename T>
+static int solve_transpose(sfb_solver* s, const T* pbar, T* out, cudaStream_t st) {
+  const Geo<T>& G = geo<T>(s->plan);
+  T* rb = (T*)s->rbuf;
+  Box B = int_box(G);
+  SFB_DISPATCH_DIM(G.dim, D, (k_wconj<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, pbar, rb, B, 0)));
+  SFB_LAUNCH_CHECK("solve transpose: 1/W");
+  if (int rc = solve_inplace<T>(s, rb, st)) return rc;
+  Box E = ext_box(G);
+  SFB_DISPATCH_DIM(G.dim, D, (k_wconj<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, out, E, 1)));
+  SFB_LAUNCH_CHECK("solve transpose: W");
+  return SFB_OK;
 }
 
 template <typename T>
@@ -496,7 +528,7 @@ int sfb_divergence_pullback(sfb_plan* p, void* pbar, void* const* out, void* str
   cudaStream_t st = (cudaStream_t)stream;
   return SFB_TYPED(p, ([&]() {
     const Geo<T>& G = geo<T>(p);
-    int rc = launch_planes<T>(G, MV<T>{{(T*)pbar, nullptr, nullptr}}, 1, 2, st);  // zero_ghosts_scalar(pbar)
+    int rc = launch_planes<T>(G, MV<T>{{(T*)pbar, nullptr, nullptr}}, 1, 3, st);  // zero_ghosts_scalar(pbar)
     if (rc) return rc;
     Box E = ext_box(G);
     SFB_DISPATCH_DIM(G.dim, D, (k_div_pb<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, (const T*)pbar, mvp<T>(p, out), E)));
@@ -561,7 +593,8 @@ int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, doubl
     const Geo<T>& G = geo<T>(p);
     int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);
     if (rc) return rc;
-    if (G.dim == 3 && !getenv("SFB_PB_GENERIC"))
+    static const bool pb_generic = env_int("SFB_PB_GENERIC") != 0;
+    if (G.dim == 3 && !pb_generic)
       return rhs_pb_march<T>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), mvp<T>(p, out), (T)nu, nu != 0.0,
                              accumulate, st);
     Box E = ext_box(G);
@@ -569,6 +602,13 @@ int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, doubl
     SFB_LAUNCH_CHECK("rhs pullback");
     return (int)SFB_OK;
   })());
+}
+
+int sfb_solve_transpose(sfb_solver* s, const void* pbar, void* out, void* stream) {
+  if (!s || !pbar || !out) return fail(SFB_EINVAL, "null argument");
+  if (s->slab) return fail(SFB_ECONFIG, "solve transpose: not available on a slab solver");
+  return s->plan->dtype == SFB_F64 ? solve_transpose<double>(s, (const double*)pbar, (double*)out, (cudaStream_t)stream)
+                                   : solve_transpose<float>(s, (const float*)pbar, (float*)out, (cudaStream_t)stream);
 }
 
 int sfb_project_pullback(sfb_solver* s, void* const* vbar, void* const* out, void* stream) {

@@ -263,12 +263,16 @@ template <typename T>
 static void cg_capture(sfb_solver* s, const Geo<T>& G, int nb) {
   s->cg_graph_tried = true;
   if (getenv("SFB_CG_NOGRAPH")) return;
-  cudaStream_t cap = nullptr;
-  if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
-    cudaGetLastError();
-    return;
+  // one capture stream per solver, created on the first capture and reused
+  // when sfb_cg_configure forces a re-capture (destroyed with the solver)
+  cudaStream_t cap = (cudaStream_t)s->cg_cap_stream;
+  if (!cap) {
+    if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    s->cg_cap_stream = cap;
   }
-  s->cg_cap_stream = cap;
   cudaGraph_t g = nullptr;
   if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     cudaGetLastError();

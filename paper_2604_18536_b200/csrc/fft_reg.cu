@@ -1,5 +1,6 @@
 // Host dispatch of the register-resident FFT engine (sfb_fft_reg.cuh).
 #include <cstdlib>
+#include <mutex>
 
 #include "sfb_fft_reg.cuh"
 
@@ -28,7 +29,9 @@ bool reg_factor(int L, RegLen& R) {
 int fft_reg_init() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(SFB_ECUDA, "cudaGetDevice");
+  static std::mutex mu;
   static bool done[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
   if (dev < 64 && done[dev]) return SFB_OK;
   if (reg_tu_d1_init() || reg_tu_d2_init() || reg_tu_f1_init() || reg_tu_f2_init())
     return fail(SFB_ECUDA, "upload of the register-FFT twiddle tables failed");

@@ -228,13 +228,10 @@ int fft_tma_pass(const FftTma& M, const FftLen& P, const void* tw, const ScaleAr
   typedef typename CX<T>::t C;
   constexpr int W = sizeof(T) == 8 ? 4 : 8;
   static int nsm = 0;
-  static bool attr = false;
   const size_t smem = 3 * (size_t)M.nbox * M.lb * W * sizeof(C) + 64 + (size_t)P.twn * sizeof(C);
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  if (!attr) {
-    cudaFuncSetAttribute(k_fft_tma<T, MODE, W, kTmaNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem((const void*)k_fft_tma<T, MODE, W, kTmaNT>, 227 * 1024))
+    return cuda_check(e, "fft tma: shared-memory attribute");
   TmaTile tt{M.rank, M.nbox, M.lb, M.ncol, M.nbatch};
   const long long ntiles = (long long)((M.ncol + W - 1) / W) * M.nbatch;
   const int g = (int)(ntiles < nsm ? ntiles : nsm);

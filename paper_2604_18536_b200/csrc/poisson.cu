@@ -200,7 +200,8 @@ __global__ void k_p_ext(Geo<T> G, const T* __restrict__ p, T* __restrict__ pe, B
 
 template <typename T>
 static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t st) {
-  if (G.dim == 3 && getenv("SFB_GRAD_MARCH")) {
+  static const bool grad_march = env_int("SFB_GRAD_MARCH") != 0;
+  if (G.dim == 3 && grad_march) {
     dim3 blk(64, 4);
     const int bx = (G.n[2] + 63) / 64, by = (G.n[1] + 3) / 4;
     const long long bps = (long long)bx * by;
@@ -218,7 +219,11 @@ static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t
   if (G.dim == 3) {
     // 128 x 2 blocks along the contiguous axis (vs the generic 32 x 4 x 2):
     // longer contiguous runs per warp pair, 840^3 fp64 8.18 -> 7.65 ms
-    const int bxk = getenv("SFB_GRAD_BLK") ? atoi(getenv("SFB_GRAD_BLK")) : 128;
+    // SFB_GRAD_BLK: a power of two in [32, 256], else the measured default
+    static const int bxk = [] {
+      const int v = env_int("SFB_GRAD_BLK", 128);
+      return (v >= 32 && v <= 256 && (v & (v - 1)) == 0) ? v : 128;
+    }();
     dim3 blk(bxk, 256 / bxk, 1);
     dim3 grid((B.cnt[2] + blk.x - 1) / blk.x, (B.cnt[1] + blk.y - 1) / blk.y, B.cnt[0]);
     k_grad_sub<T, 3><<<grid, blk, 0, st>>>(G, p, U, B, pe);
@@ -232,7 +237,8 @@ static int launch_grad(const Geo<T>& G, const T* p, MV<T> U, T* pe, cudaStream_t
 
 template <typename T>
 static int launch_div(const Geo<T>& G, CV<T> C, T* out, cudaStream_t st) {
-  if (G.dim == 3 && getenv("SFB_DIV_MARCH")) {
+  static const bool div_march = env_int("SFB_DIV_MARCH") != 0;
+  if (G.dim == 3 && div_march) {
     dim3 blk(64, 4);
     const int bx = (G.n[2] + 63) / 64, by = (G.n[1] + 3) / 4;
     const long long bps = (long long)bx * by;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 #include <vector>
@@ -57,6 +58,16 @@ namespace sfb {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_check(cudaError_t e, const char* what);
+// cudaFuncAttributeMaxDynamicSharedMemorySize for kernel `func` on the
+// current device, set once per (kernel, device) under a mutex (plan.cu):
+// a process may drive several devices, and plans are used from any thread.
+cudaError_t ensure_smem(const void* func, size_t bytes);
+// Tuning knob from the environment, read once (thread-safe static init in the
+// caller): 0 if unset.
+inline int env_int(const char* name, int dflt = 0) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
 
 template <typename T>
 inline const Geo<T>& geo(const sfb_plan* p);

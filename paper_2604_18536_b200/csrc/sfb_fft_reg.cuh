@@ -590,17 +590,20 @@ template <typename T, int A, int B>
 static int reg_launch(const RegCall& c, cudaStream_t st) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
-    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
-    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S2);
-    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
-    cudaFuncSetAttribute(k_rfft_strided<T, A, B, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_S);
-    cudaFuncSetAttribute(k_rfft_r2c<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
-    cudaFuncSetAttribute(k_rfft_c2r<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
-    cudaFuncSetAttribute(k_rfft_r2c_div<T, A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM_R);
-    attr = true;
+  {
+    cudaError_t e = cudaSuccess;
+#define SFB_ATTR(K, B) \
+  if (e == cudaSuccess) e = ensure_smem((const void*)K, (B))
+    SFB_ATTR((k_rfft_strided<T, A, B, 0>), RG::SMEM_S);
+    SFB_ATTR((k_rfft_strided<T, A, B, 1>), RG::SMEM_S);
+    SFB_ATTR((k_rfft_strided<T, A, B, 2>), RG::SMEM_S2);
+    SFB_ATTR((k_rfft_strided<T, A, B, 3>), RG::SMEM_S);
+    SFB_ATTR((k_rfft_strided<T, A, B, 4>), RG::SMEM_S);
+    SFB_ATTR((k_rfft_r2c<T, A, B>), RG::SMEM_R);
+    SFB_ATTR((k_rfft_c2r<T, A, B>), RG::SMEM_R);
+    SFB_ATTR((k_rfft_r2c_div<T, A, B>), RG::SMEM_R);
+#undef SFB_ATTR
+    if (e != cudaSuccess) return -2;
   }
   if (c.kind <= 2 || c.kind == 6 || c.kind == 7) {
     dim3 grid((c.ncol + RG::W - 1) / RG::W, c.nbatch);

@@ -15,9 +15,13 @@ template <typename T>
 struct MV {
   T* c[3];
 };
+// Body force: per-component constants f, or per-DOF fields a (extended
+// arrays, sample_force of a callable, operators.py:241-259); a[c] == NULL
+// means the constant.  Added after diffusion (operators.py:228-235).
 template <typename T>
 struct Force {
   T f[3];
+  const T* a[3];
 };
 template <typename T>
 struct KList {

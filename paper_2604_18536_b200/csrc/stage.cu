@@ -23,7 +23,8 @@ __global__ void __launch_bounds__(256) k_stage_generic(Geo<T> G, StageArgs<T> A,
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     if (!is_udof<T, D>(G, I, a)) continue;
-    const T k = rhs_comp<T, D>(G, A.y, x, I, a, T(0), true, A.diff, A.nu, A.F.f[a]);
+    T k = rhs_comp<T, D>(G, A.y, x, I, a, T(0), true, A.diff, A.nu, A.F.f[a]);
+    if (A.F.a[a]) k += A.F.a[a][x];
     if (A.has_k) A.k_out.c[a][x] = k;
     if (A.has_s) {
       const T base = A.s_from_u0 ? A.u0.c[a][x] : A.s_in.c[a][x];
@@ -153,6 +154,9 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   const bool h0 = G.halo[0] != 0;
   auto load_p = [&](int ip) {
     if constexpr (PROJ) {
+      // slab: planes 0..m+2 = 0..E[0] exist; periodic: wrap1 covers 1-n0..2n0.
+      // Prefetches past that (m == 1 slabs, n0 == 1 grids) are never consumed.
+      if (h0 ? (ip < 0 || ip > G.E[0]) : (ip < 1 - n0 || ip > 2 * n0)) return;
       T* dst = pring + (ip & (kPRing - 1)) * PPS + tid;
       const long long base = (long long)(h0 ? ip : wrap1(ip, n0) - 1) * ps0;
 #pragma unroll
@@ -287,6 +291,11 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
         kv[2] = dof[r][2] ? rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]) : T(0);
       }
       const long long x = x0 + r * rstep;
+      if (A.F.a[0]) {  // per-DOF force fields (sample_force of a callable)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (dof[r][a]) kv[a] += A.F.a[a][x];
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         if (!dof[r][a]) continue;
@@ -323,12 +332,8 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
   constexpr int MINB = (FL & FL_PROJ) ? SFB_STAGE_MINB_PROJ : SFB_STAGE_MINB;
   const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T) + kTJ * sizeof(Coef<T>) +
                       ((FL & FL_PROJ) ? ((size_t)kPRing * (kTJ + 3) * (kTK + 3) + kTJ + kTK + 4) * sizeof(T) : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_stage_march<T, kTJ, kTK, kCPT, FL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem((const void*)k_stage_march<T, kTJ, kTK, kCPT, FL, MINB>, smem))
+    return cuda_check(e, "rk stage: shared-memory attribute");
   const int bx = (G.n[2] + kTK - 1) / kTK, by = (G.n[1] + kTJ - 1) / kTJ;
   const long long bps = (long long)bx * by;
   // split the march into bz chunks so the launch is >= ~30 waves of resident
@@ -339,7 +344,8 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
   long long want = (30LL * 148 * MINB + bps - 1) / bps;
   if (want > G.n[0] / 64) want = G.n[0] / 64;
   if (want < 1) want = 1;
-  if (getenv("SFB_STAGE_BZ")) want = atoi(getenv("SFB_STAGE_BZ"));
+  static const int bz_env = env_int("SFB_STAGE_BZ");
+  if (bz_env > 0) want = bz_env;
   int chunk = (int)((G.n[0] + want - 1) / want);
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;
@@ -352,8 +358,8 @@ template <typename T>
 static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st, bool allow_per = true) {
   // a halo axis 0 (z-slab) has no walls either: every local cell is a DOF, so
   // the branch-free variant applies (its ring reads the exchanged ghost planes)
-  const bool per = allow_per && G.per[0] && G.per[1] && G.per[2] && !G.halo[1] && !G.halo[2] &&
-                   !getenv("SFB_STAGE_NOPER");
+  static const bool noper = env_int("SFB_STAGE_NOPER") != 0;
+  const bool per = allow_per && G.per[0] && G.per[1] && G.per[2] && !G.halo[1] && !G.halo[2] && !noper;
   const int fl = (A.has_k ? FL_K : 0) | (A.has_s ? FL_S : 0) | (A.has_s && A.s_from_u0 ? FL_SU0 : 0) |
                  (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0) | (per ? FL_PER : 0);
   switch (fl) {
@@ -388,7 +394,8 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
     A.s_out.c[c] = on ? (T*)a->s_out[c] : nullptr;
     A.y_next.c[c] = on ? (T*)a->y_next[c] : nullptr;
     A.k_out.c[c] = on ? (T*)a->k_out[c] : nullptr;
-    A.F.f[c] = on ? (T)a->force[c] : T(0);
+    A.F.a[c] = on ? (const T*)a->force_field[c] : nullptr;
+    A.F.f[c] = (on && !A.F.a[c]) ? (T)a->force[c] : T(0);
   }
   A.cb = (T)a->cb;
   A.ca = (T)a->ca;
@@ -401,9 +408,13 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
   A.p_int = (const T*)a->p_int;
   if (A.p_int && !(G.dim == 3 && G.per[0] && G.per[1] && G.per[2] && !G.halo[1] && !G.halo[2]))
     return fail(SFB_ECONFIG, "on-the-fly projection needs a periodic (or z-slab) 3D plan");
+  if ((A.F.a[0] != nullptr) != (G.dim < 2 || A.F.a[1] != nullptr) ||
+      (G.dim == 3 && (A.F.a[0] != nullptr) != (A.F.a[2] != nullptr)))
+    return fail(SFB_EINVAL, "force fields: give all components or none");
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
-  if (G.dim == 3 && (!getenv("SFB_STAGE_GENERIC") || A.p_int)) {
+  static const bool generic = env_int("SFB_STAGE_GENERIC") != 0;
+  if (G.dim == 3 && (!generic || A.p_int)) {
     const int rc = stage_march<T>(G, A, st);
     if (rc >= 0) return rc;
     if (A.p_int) return fail(SFB_ECONFIG, "on-the-fly projection: unsupported stage variant");

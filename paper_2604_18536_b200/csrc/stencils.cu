@@ -96,7 +96,8 @@ struct PlaneSet {
   int size[32];
 };
 
-// mode 0: velocity fill, 1: scalar fill, 2: zero (velocity non-DOFs / scalar ghosts)
+// mode 0: velocity fill, 1: scalar fill, 2: zero velocity non-DOFs
+// (adjoint.py:40-50), 3: zero scalar ghosts (adjoint.py:32-37)
 template <typename T, int D>
 __global__ void k_planes(Geo<T> G, MV<T> U, PlaneSet P, int mode) {
   const int pl = blockIdx.y;
@@ -114,7 +115,7 @@ __global__ void k_planes(Geo<T> G, MV<T> U, PlaneSet P, int mode) {
   }
   T* __restrict__ u = U.c[c];
   const long long x = lin<T, D>(G, I);
-  if (mode == 2) u[x] = T(0);
+  if (mode >= 2) u[x] = T(0);
   else u[x] = ghost_value<T, D>(G, u, c, I, mode == 1);
 }
 
@@ -143,7 +144,7 @@ static PlaneSet make_planes(const Geo<T>& G, int ncomp, bool boundary_faces) {
 
 template <typename T>
 int launch_planes(const Geo<T>& G, MV<T> U, int ncomp, int mode, cudaStream_t st) {
-  PlaneSet P = make_planes(G, ncomp, mode != 1);
+  PlaneSet P = make_planes(G, ncomp, mode == 0 || mode == 2);
   if (P.count == 0) return SFB_OK;
   int mx = 0;
   for (int i = 0; i < P.count; ++i) mx = P.size[i] > mx ? P.size[i] : mx;
@@ -154,6 +155,85 @@ int launch_planes(const Geo<T>& G, MV<T> U, int ncomp, int mode, cudaStream_t st
 }
 template int launch_planes<double>(const Geo<double>&, MV<double>, int, int, cudaStream_t);
 template int launch_planes<float>(const Geo<float>&, MV<float>, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// Adjoint of the ghost fills (adjoint.py:53-111): for one axis a, every
+// position of the other axes' extended plane folds its two ghost entries
+// onto their sources, statement for statement in the reference's order (a
+// thread owns the whole line along a, so n == 1 aliasing is exact).  The
+// host walks the axes in reverse, one launch per axis, as the reference
+// does; blockIdx.y is the component (comp < 0: the scalar rules).
+// ---------------------------------------------------------------------------
+template <typename T, int D>
+__global__ void k_fold(Geo<T> G, MV<T> U, int axis, int scalar) {
+  const int c = blockIdx.y;
+  int sz = 1;
+#pragma unroll
+  for (int b = 0; b < D; ++b)
+    if (b != axis) sz *= G.E[b];
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= sz) return;
+  int I[3] = {0, 0, 0};
+  int rem = pos;
+#pragma unroll
+  for (int b = D - 1; b >= 0; --b) {
+    if (b == axis) continue;
+    I[b] = rem % G.E[b];
+    rem /= G.E[b];
+  }
+  T* __restrict__ u = U.c[c];
+  const int n = G.n[axis];
+  const long long st = G.s[axis];
+  const long long x0 = lin<T, D>(G, I);  // I[axis] == 0
+  T* g_lo = u + x0;
+  T* g_hi = u + x0 + (long long)(n + 1) * st;
+  auto at = [&](int i) -> T& { return u[x0 + (long long)i * st]; };
+  if (G.per[axis]) {
+    at(n) += *g_lo;
+    at(1) += *g_hi;
+    *g_lo = T(0);
+    *g_hi = T(0);
+    return;
+  }
+  if (scalar) {
+    at(1) += *g_lo;
+    at(n) += *g_hi;
+    *g_lo = T(0);
+    *g_hi = T(0);
+    return;
+  }
+  const bool normal = c == axis;
+  if (!normal) {
+    if (G.bc_lo[axis] == SFB_BC_DIRICHLET) at(1) -= *g_lo;
+    else if (G.bc_lo[axis] == SFB_BC_SYMMETRIC) at(1) += *g_lo;
+  }
+  *g_lo = T(0);
+  if (G.bc_hi[axis] == SFB_BC_DIRICHLET || G.bc_hi[axis] == SFB_BC_SYMMETRIC) {
+    if (normal) {
+      at(n - 1) -= *g_hi;
+      at(n) = T(0);
+    } else if (G.bc_hi[axis] == SFB_BC_DIRICHLET) {
+      at(n) -= *g_hi;
+    } else {
+      at(n) += *g_hi;
+    }
+  }
+  *g_hi = T(0);
+}
+
+template <typename T>
+int launch_fold(const Geo<T>& G, MV<T> U, int ncomp, bool scalar, cudaStream_t st) {
+  for (int a = G.dim - 1; a >= 0; --a) {
+    if (G.halo[a]) continue;  // slab ghost planes belong to the neighbouring rank
+    int sz = 1;
+    for (int b = 0; b < G.dim; ++b)
+      if (b != a) sz *= G.E[b];
+    dim3 grid((sz + 255) / 256, ncomp);
+    SFB_DISPATCH_DIM(G.dim, D, (k_fold<T, D><<<grid, 256, 0, st>>>(G, U, a, scalar ? 1 : 0)));
+    SFB_LAUNCH_CHECK("fold ghosts");
+  }
+  return SFB_OK;
+}
 
 // ---------------------------------------------------------------------------
 // divergence (operators.py:108-122): whole extended output, ghosts zero
@@ -202,6 +282,7 @@ __global__ void k_rhs(Geo<T> G, CV<T> U, MV<T> O, Box B, T nu, Force<T> F, int f
     if (is_udof<T, D>(G, I, a)) {
       T v = accum ? o[x] : T(0);
       v = rhs_comp<T, D>(G, U, x, I, a, v, conv, diff, nu, F.f[a]);
+      if (F.a[a]) v += F.a[a][x];
       o[x] = v;
     } else if (!accum) {
       o[x] = T(0);
@@ -398,11 +479,14 @@ static bool ptrs_ok(const sfb_plan* p, const void* const* u) {
 }
 
 template <typename T>
-static int do_rhs(sfb_plan* p, const void* const* u, void* const* out, double nu, const double* force, int flags,
-                  cudaStream_t st) {
+static int do_rhs(sfb_plan* p, const void* const* u, void* const* out, double nu, const double* force,
+                  const void* const* field, int flags, cudaStream_t st) {
   const Geo<T>& G = geo<T>(p);
   Force<T> F;
-  for (int a = 0; a < 3; ++a) F.f[a] = (force && a < p->dim) ? (T)force[a] : T(0);
+  for (int a = 0; a < 3; ++a) {
+    F.a[a] = (field && a < p->dim) ? (const T*)field[a] : nullptr;
+    F.f[a] = (force && a < p->dim && !F.a[a]) ? (T)force[a] : T(0);
+  }
   Box B = ext_box(G);
   SFB_DISPATCH_DIM(G.dim, D, (k_rhs<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, cv<T>(p, u), mv<T>(p, out), B, (T)nu, F, flags)));
   SFB_LAUNCH_CHECK("momentum rhs");
@@ -423,6 +507,26 @@ int sfb_fill_ghosts_velocity(sfb_plan* p, void* const* u, void* stream) {
 int sfb_fill_ghosts_scalar(sfb_plan* p, void* f, void* stream) {
   if (!p || !f) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, launch_planes<T>(geo<T>(p), MV<T>{{(T*)f, nullptr, nullptr}}, 1, 1, (cudaStream_t)stream));
+}
+
+int sfb_fold_ghosts_velocity(sfb_plan* p, void* const* u, void* stream) {
+  if (!p || !ptrs_ok(p, u)) return fail(SFB_EINVAL, "null argument");
+  return SFB_TYPED(p, launch_fold<T>(geo<T>(p), mv<T>(p, u), p->dim, false, (cudaStream_t)stream));
+}
+
+int sfb_fold_ghosts_scalar(sfb_plan* p, void* f, void* stream) {
+  if (!p || !f) return fail(SFB_EINVAL, "null argument");
+  return SFB_TYPED(p, launch_fold<T>(geo<T>(p), MV<T>{{(T*)f, nullptr, nullptr}}, 1, true, (cudaStream_t)stream));
+}
+
+int sfb_zero_non_dofs_velocity(sfb_plan* p, void* const* u, void* stream) {
+  if (!p || !ptrs_ok(p, u)) return fail(SFB_EINVAL, "null argument");
+  return SFB_TYPED(p, launch_planes<T>(geo<T>(p), mv<T>(p, u), p->dim, 2, (cudaStream_t)stream));
+}
+
+int sfb_zero_ghosts_scalar(sfb_plan* p, void* f, void* stream) {
+  if (!p || !f) return fail(SFB_EINVAL, "null argument");
+  return SFB_TYPED(p, launch_planes<T>(geo<T>(p), MV<T>{{(T*)f, nullptr, nullptr}}, 1, 3, (cudaStream_t)stream));
 }
 
 int sfb_divergence(sfb_plan* p, const void* const* u, void* out, void* stream) {
@@ -451,20 +555,21 @@ int sfb_pressure_gradient(sfb_plan* p, const void* pf, void* const* out, void* s
 
 int sfb_convection(sfb_plan* p, const void* const* u, void* const* out, int accumulate, void* stream) {
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
-  return SFB_TYPED(p, do_rhs<T>(p, u, out, 0.0, nullptr, 1 | (accumulate ? 4 : 0), (cudaStream_t)stream));
+  return SFB_TYPED(p, do_rhs<T>(p, u, out, 0.0, nullptr, nullptr, 1 | (accumulate ? 4 : 0), (cudaStream_t)stream));
 }
 
 int sfb_diffusion(sfb_plan* p, const void* const* u, double nu, void* const* out, int accumulate, void* stream) {
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
   if (nu < 0) return fail(SFB_EINVAL, "viscosity must be nonnegative");
-  return SFB_TYPED(p, do_rhs<T>(p, u, out, nu, nullptr, 2 | (accumulate ? 4 : 0), (cudaStream_t)stream));
+  return SFB_TYPED(p, do_rhs<T>(p, u, out, nu, nullptr, nullptr, 2 | (accumulate ? 4 : 0), (cudaStream_t)stream));
 }
 
-int sfb_momentum_rhs(sfb_plan* p, const void* const* u, double nu, const double* force, void* const* out, void* stream) {
+int sfb_momentum_rhs(sfb_plan* p, const void* const* u, double nu, const double* force, const void* const* force_field,
+                     void* const* out, void* stream) {
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
   if (nu < 0) return fail(SFB_EINVAL, "viscosity must be nonnegative");
   int flags = 1 | (nu != 0.0 ? 2 : 0);
-  return SFB_TYPED(p, do_rhs<T>(p, u, out, nu, force, flags, (cudaStream_t)stream));
+  return SFB_TYPED(p, do_rhs<T>(p, u, out, nu, force, force_field, flags, (cudaStream_t)stream));
 }
 
 int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, const void* const* k,

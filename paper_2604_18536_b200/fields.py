@@ -32,9 +32,12 @@ def _as_device(grid, arr):
 class ScalarField:
     """Volume-centred scalar with ghost layer (fields.py:16-30)."""
 
-    def __init__(self, grid, data=None):
+    def __init__(self, grid, data=None, empty=False):
         self.grid = grid
-        self.data = alloc.zeros(grid.ext_shape, grid.dtype) if data is None else _as_device(grid, data)
+        if data is None:
+            self.data = (alloc.empty if empty else alloc.zeros)(grid.ext_shape, grid.dtype)
+        else:
+            self.data = _as_device(grid, data)
 
     @property
     def interior(self):

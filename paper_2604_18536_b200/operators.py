@@ -81,16 +81,53 @@ def convection(u, out=None, scratch=None, accumulate=False):
     return out
 
 
+def _is_constant(f):
+    return np.isscalar(f) or (isinstance(f, np.ndarray) and f.ndim == 0) or (
+        isinstance(f, torch.Tensor) and f.dim() == 0)
+
+
 def constant_force(grid, force):
-    """Per-component constants for the fused kernels, or None."""
+    """Per-component constants for the fused kernels (0.0 for components
+    given as fields), or None."""
     if force is None:
         return None
-    vals = []
-    for f in force:
-        if not np.isscalar(f) and not (isinstance(f, np.ndarray) and f.ndim == 0):
-            raise ConfigurationError("only constant body forces are supported on the GPU path")
-        vals.append(float(grid.dtype.type(f)))
-    return vals
+    return [float(grid.dtype.type(float(f))) if _is_constant(f) else 0.0 for f in force]
+
+
+def force_fields(grid, force):
+    """Per-DOF force components as extended device arrays (zero off the DOFs),
+    or None when every component is a constant.  Accepts the reference's
+    sampled arrays (DOF-shaped, operators.py:249-258), extended arrays, or
+    tensors of either shape; constants in a mixed list become constant
+    fields.  Cached on the list object for repeated stage launches."""
+    if force is None or all(_is_constant(f) for f in force):
+        return None
+    cached = getattr(force, "_sfb_fields", None) if isinstance(force, ForceList) else None
+    if cached is not None:
+        return cached
+    out = []
+    for a in range(grid.dim):
+        f = force[a]
+        full = alloc.zeros(grid.ext_shape, grid.dtype)
+        sl = grid.u_slices(a)
+        if _is_constant(f):
+            full[sl] = float(grid.dtype.type(float(f)))
+        else:
+            t = f if isinstance(f, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(f, dtype=grid.dtype)))
+            t = t.to(device=full.device, dtype=full.dtype)
+            if tuple(t.shape) == tuple(grid.ext_shape):
+                full[sl] = t[sl]
+            else:
+                full[sl] = t
+        out.append(full)
+    if isinstance(force, ForceList):
+        force._sfb_fields = out
+    return out
+
+
+class ForceList(list):
+    """sample_force's result: a list (as the reference returns) that caches
+    its device fields."""
 
 
 def momentum_rhs(u, nu, force=None, closure=None, t=0.0, out=None, scratch=None):
@@ -105,18 +142,28 @@ def momentum_rhs(u, nu, force=None, closure=None, t=0.0, out=None, scratch=None)
     fp = None
     if fv is not None:
         fp = (N.ctypes.c_double * 3)(*(fv + [0.0] * (3 - len(fv))))
-    N.call("sfb_momentum_rhs", _plan(grid), N.ptr3(u.u), float(nu), fp, N.ptr3(out.u), stream_ptr())
+    ff = force_fields(grid, force)
+    ffp = N.ctypes.byref(N.ptr3(ff)) if ff is not None else None
+    N.call("sfb_momentum_rhs", _plan(grid), N.ptr3(u.u), float(nu), fp, ffp, N.ptr3(out.u), stream_ptr())
     if closure is not None:
         closure.add_rhs(u, out, scratch)
     return out
 
 
 def sample_force(grid, force):
-    """operators.py:241-259 (constant vectors; callables are rejected)."""
+    """operators.py:241-259: None, a d-vector of constants, or a callable
+    ``f(component, *coords)`` sampled once at the velocity points (the
+    reference's broadcast and dtype cast, kept on the host as DOF-shaped
+    arrays; the stage kernels read them as device fields)."""
     if force is None:
         return None
     if callable(force):
-        raise ConfigurationError("spatially varying (callable) forces are not supported on the GPU path")
+        out = ForceList()
+        for a in range(grid.dim):
+            coords = [grid.broadcast(c, g) for g, c in enumerate(grid.face_coords(a))]
+            full = np.broadcast_to(force(a, *coords), grid.ext_shape)
+            out.append(np.array(full[grid.u_slices(a)], dtype=grid.dtype))
+        return out
     return [grid.dtype.type(f) for f in force]
 
 

@@ -114,14 +114,6 @@ class ChannelPoissonSolver(_GpuSolver):
         super().__init__(grid, bcs)
 
 
-class DirectPoissonSolver(ChannelPoissonSolver):
-    """``solver="direct"`` on the GPU path: the same augmented zero-mean
-    system (poisson.py:203-229), solved exactly by separation of variables on
-    separable channel grids; other layouts raise ConfigurationError."""
-
-    kind = "direct"
-
-
 class CGPoissonSolver(_GpuSolver):
     """Matrix-free conjugate gradient on the weighted operator
     (poisson.py:232-308): b = -W (rhs - wmean), CG on -W L with the weighted
@@ -163,6 +155,61 @@ class CGPoissonSolver(_GpuSolver):
             b = self.residual_history[0] if self.residual_history else 1.0
             failed.residual = self.residual_history[-1] / b if b else None
             failed.iterations = self.max_iter
+
+    def solve_interior(self, rhs, out):
+        try:
+            super().solve_interior(rhs, out)
+        except ConvergenceError as e:
+            self._after_solve(failed=e)
+            raise
+        self._after_solve()
+
+
+def _periodic_uniform(grid):
+    return all(grid.periodic) and grid.uniform
+
+
+class DirectPoissonSolver(_GpuSolver):
+    """``solver="direct"`` (poisson.py:203-229): the augmented system
+    [[W L, w], [w^T, 0]] -- L p = rhs - wmean with the weighted zero-mean
+    gauge w^T p = 0 -- on any grid, as the reference's sparse LU is.  The GPU
+    path picks the exact solver for the layout:
+
+    * separable channel (periodic uniform x/z, walls on y, 3D): FFT(x,z) x
+      batched tridiagonal(y), exact (``backend == "fft-tridiag"``);
+    * all-periodic uniform grids: the spectral solve -- on uniform grids W is
+      constant, so rhs - wmean is rhs - mean and w^T p = 0 is the zero-mean
+      gauge of the FFT diagonalisation (``backend == "spectral"``);
+    * anything else (stretching along a periodic axis, walls on other axes,
+      symmetric sides, 2D channels): the matrix-free CG on the same weighted
+      operator and gauge, run to a relative residual of 1e-12 (fp64) /
+      1e-6 (fp32) with up to 10000 iterations (``backend == "cg"``); a solve
+      that does not get there raises ConvergenceError instead of returning a
+      less accurate pressure.
+    """
+
+    kind = "direct"
+    tolerance = 1e-12
+
+    def __init__(self, grid, bcs):
+        if _separable_channel(grid):
+            self.backend, self._native_kind = "fft-tridiag", N.SFB_SOLVER_CHANNEL
+        elif _periodic_uniform(grid):
+            self.backend, self._native_kind = "spectral", N.SFB_SOLVER_SPECTRAL
+        else:
+            self.backend, self._native_kind = "cg", N.SFB_SOLVER_CG
+        super().__init__(grid, bcs)
+        if self.backend == "cg":
+            self.tol = 1e-12 if np.dtype(grid.dtype) == np.float64 else 1e-6
+            self.max_iter = 10000
+            N.call("sfb_cg_configure", self.handle, self.tol, self.max_iter)
+            self.residual_history = []
+
+    def _after_solve(self, failed=None):
+        if self.backend == "cg":
+            CGPoissonSolver._after_solve(self, failed)
+        else:
+            self.iterations = 1
 
     def solve_interior(self, rhs, out):
         try:

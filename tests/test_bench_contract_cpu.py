@@ -37,3 +37,23 @@ def test_reference_arm_other_ranks_silent():
     r = _run({"RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def test_gpus_flag_self_launches_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun launches 2 ranks itself (the
+    reference arm needs no GPU, so the launch path is checked here)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "3", "--ref-n", "12"], capture_output=True, text=True,
+                       env=env, cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_gpus_flag_mismatch_fails_loudly():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--steps", "1"],
+                       capture_output=True, text=True, env=dict(os.environ, WORLD_SIZE="2", RANK="0"), cwd=ROOT,
+                       timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

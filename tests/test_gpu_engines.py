@@ -55,9 +55,9 @@ def _solve(P, shape, dtype, monkeypatch, stockham):
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_register_fft_solve_vs_oracle_and_stockham(P, shape, dtype, monkeypatch):
     got, ref = _solve(P, shape, dtype, monkeypatch, stockham=False)
-    assert rel(got, ref) <= (1e-12 if dtype == np.float64 else 2e-5)
+    assert rel(got, ref) <= (1e-12 if dtype == np.float64 else 1e-5)
     old, _ = _solve(P, shape, dtype, monkeypatch, stockham=True)
-    assert rel(got, old) <= (1e-13 if dtype == np.float64 else 2e-5)
+    assert rel(got, old) <= (1e-13 if dtype == np.float64 else 1e-5)
 
 
 def _rk4(P, n, dtype, monkeypatch, env):
@@ -93,7 +93,7 @@ def test_fused_projection_paths(P, n, dtype, monkeypatch):
     for u, p, ref_u, ref_p in runs:
         for a in range(3):
             assert rel(u[a], ref_u[a]) <= t, a
-        assert rel(p, ref_p) <= 10 * t
+        assert rel(p, ref_p) <= t
     for a in range(3):
         assert rel(runs[0][0][a], runs[2][0][a]) <= t
 
@@ -105,4 +105,4 @@ def test_rk4_step_at_256_cubed_vs_oracle(P, monkeypatch):
     u, p, ref_u, ref_p = _rk4(P, (256, 256, 256), np.float64, monkeypatch, ())
     for a in range(3):
         assert rel(u[a], ref_u[a]) <= 1e-12, a
-    assert rel(p, ref_p) <= 1e-11
+    assert rel(p, ref_p) <= 1e-12

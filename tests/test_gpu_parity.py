@@ -132,7 +132,7 @@ def test_spectral_projection_and_steps_golden(P, name):
     got = u.numpy()
     for a in range(3):
         assert rel(got[a], c[f"uproj{a}"]) <= t
-    assert rel(pp.numpy(), c["pproj"]) <= t * 10
+    assert rel(pp.numpy(), c["pproj"]) <= t
     dt = float(c["dt"])
     for tag, tab, meth in (("rk4", P.RK4, "rk4"), ("ssp33", P.SSP33, "ssp33"), ("wray3", P.WRAY3, "wray3")):
         setup.method, setup.tableau = meth, tab
@@ -144,7 +144,7 @@ def test_spectral_projection_and_steps_golden(P, name):
         got = st.u.numpy()
         for a in range(3):
             assert rel(got[a], c[f"{tag}_u{a}"]) <= t, (tag, a)
-        assert rel(st.pressure.numpy(), c[f"{tag}_p"]) <= t * 10, tag
+        assert rel(st.pressure.numpy(), c[f"{tag}_p"]) <= t, tag
 
 
 @pytest.mark.parametrize("shape", [(6, 10, 14), (20, 12, 30), (42, 8, 16), (64, 64, 64), (7, 9, 5),
@@ -177,7 +177,7 @@ def test_taylor_green_2d_rk4_golden(P):
     got = st.u.numpy()
     for a in range(2):
         assert rel(got[a], c[f"u{a}"]) <= 1e-12
-    assert rel(st.pressure.numpy(), c["p"]) <= 1e-11
+    assert rel(st.pressure.numpy(), c["p"]) <= 1e-12
 
 
 def test_taylor_green_2d_64_analytic_decay(P):
@@ -204,14 +204,14 @@ def test_channel_golden_direct_solver(P):
     bcs = P.BoundarySpec.channel()
     setup = P.Setup(pg, bcs, nu=float(c["nu"]), force=(1.0, 0.0, 0.0), solver="direct", method="rk4")
     sol = setup.solver.solve(P.ScalarField(pg, c["rhs"]))
-    assert rel(sol.numpy()[pg.p_slices()], c["sol"][pg.p_slices()]) <= 1e-11
+    assert rel(sol.numpy()[pg.p_slices()], c["sol"][pg.p_slices()]) <= 1e-12
     u = vel(P, pg, [c[f"u{a}"] for a in range(3)])
     P.fill_ghosts_velocity(u, bcs)
     pp = P.project_into(u, setup.solver, bcs)
     got = u.numpy()
     for a in range(3):
         assert rel(got[a], c[f"uproj{a}"]) <= 1e-12
-    assert rel(pp.numpy(), c["pproj"]) <= 1e-11
+    assert rel(pp.numpy(), c["pproj"]) <= 1e-12
     for tag, tab, meth in (("rk4", P.RK4, "rk4"), ("ssp33", P.SSP33, "ssp33")):
         setup.method, setup.tableau = meth, tab
         st = setup.new_state(u0=vel(P, pg, [c[f"uproj{a}"] for a in range(3)]))
@@ -219,10 +219,10 @@ def test_channel_golden_direct_solver(P):
         got = st.u.numpy()
         for a in range(3):
             assert rel(got[a], c[f"{tag}_u{a}"]) <= 1e-12, (tag, a)
-        assert rel(st.pressure.numpy(), c[f"{tag}_p"]) <= 1e-10
+        assert rel(st.pressure.numpy(), c[f"{tag}_p"]) <= 1e-12
 
 
-@pytest.mark.parametrize("shape", [(32, 48, 16), (64, 48, 32)])
+@pytest.mark.parametrize("shape", [(32, 48, 16), (64, 48, 32), (128, 64, 64)])
 def test_channel_step_vs_oracle(P, shape):
     """BASELINE config 4 (reduced): stretched channel, RK4 step vs the
     FFT x tridiagonal oracle."""
@@ -245,7 +245,7 @@ def test_channel_step_vs_oracle(P, shape):
     got = st.u.numpy()
     for a in range(3):
         assert rel(got[a], ru[a]) <= 1e-12
-    assert rel(st.pressure.numpy(), rp) <= 1e-10
+    assert rel(st.pressure.numpy(), rp) <= 1e-12
 
 
 # ------------------------------------------------------------------ 3D configs
@@ -294,7 +294,7 @@ def test_isotropic_rk4_step_vs_oracle(P, dtype):
     t = tol(dtype)
     for a in range(3):
         assert rel(got[a], ru[a]) <= t
-    assert rel(st.pressure.numpy(), rp) <= t * 10
+    assert rel(st.pressure.numpy(), rp) <= t
     ke_ref = O.kinetic_energy(og, ru)
     assert abs(P.kinetic_energy(st.u) - ke_ref) <= t * ke_ref
 
@@ -345,7 +345,7 @@ def test_pullbacks_match_reference_golden(P, name):
     for a in range(d):
         assert rel(dp[a], c[f"divpb{a}"]) <= t
         assert rel(fp[a], c[f"diffpb{a}"]) <= t
-        assert rel(cp[a], c[f"convpb{a}"]) <= t * 10
+        assert rel(cp[a], c[f"convpb{a}"]) <= t
 
 
 def test_project_pullback_and_unrolled_gradient_golden(P):
@@ -363,12 +363,15 @@ def test_project_pullback_and_unrolled_gradient_golden(P):
             assert rel(gr[a], c[f"grad{n}_{a}"]) <= 1e-12
 
 
+@pytest.mark.parametrize("n", [32, 128])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_unrolled_gradient_vs_oracle_32(P, dtype):
-    """BASELINE config 3 VJP (reduced to 32^3): RK4 unrolled gradient of KE."""
+def test_unrolled_gradient_vs_oracle(P, dtype, n):
+    """BASELINE config 3 VJP (32^3 and 128^3; 512^3 in
+    profiles/r2/parity_vjp_512.json): RK4 unrolled gradient of KE, tape +
+    reverse sweep, against the oracle's restatement of adjoint.py:425-444."""
     from paper_2604_18536_b200 import cases
 
-    pg = cases.periodic_box(32, dtype=dtype)
+    pg = cases.periodic_box(n, dtype=dtype)
     og = O.OGrid([ax.boundaries for ax in pg.axes], (True,) * 3, dtype)
     bcs = P.BoundarySpec.all_periodic(3)
     setup = P.Setup(pg, bcs, nu=1 / 1600, solver="spectral", method="rk4")
@@ -377,7 +380,7 @@ def test_unrolled_gradient_vs_oracle_32(P, dtype):
     gr = P.unrolled_gradient(P.KineticEnergyLoss(), u0d, 1, 2e-3, setup).numpy()
     ref = O.unrolled_gradient_ke(og, O.periodic_bcs(3), O.SpectralSolve(og), u0, 1, 2e-3, O.RK4, 1 / 1600)
     for a in range(3):
-        assert rel(gr[a], ref[a]) <= tol(dtype) * 10
+        assert rel(gr[a], ref[a]) <= tol(dtype)
 
 
 def test_fd_identity_unrolled_gradient(P):
