@@ -89,6 +89,11 @@ typedef struct sfb_stage_args {
    * operators.py:241-259): extended arrays, one per component (all or none);
    * replaces force[] and is added after diffusion (operators.py:228-235). */
   const void* force_field[3];
+  /* Optional (NULL = off), stage 0 of a step whose state carries the previous
+   * step's deferred projection: y == u0 unprojected, p_int its pressure; the
+   * kernel takes the projected u0 from shared memory for the combines and
+   * writes it here once (timestep.py:208-210 fused into the next stage 0). */
+  void* u0_out[3];
 } sfb_stage_args;
 
 int sfb_abi_version(void);
@@ -156,6 +161,10 @@ int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream);
  * pressure, valid until the solver's next use.  Feed it to the next
  * sfb_rk_stage (sfb_stage_args.p_int), which applies u - G p on the fly. */
 int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, void* stream);
+/* Second half of sfb_project after sfb_project_solve: u -= G p with the
+ * pressure still in the solver buffer, velocity ghost fill, optional extended
+ * pressure (the deferred last projection of run_steps, poisson.py:333-341). */
+int sfb_project_finish(sfb_solver* s, void* const* u, void* p_ext, void* stream);
 /* Number of kernels (ours) launched by sfb_project (mode 0: without, 1: with
  * the extended pressure), sfb_project_solve (2) or sfb_slab_r2c (3). */
 int sfb_project_launches(const sfb_solver* s, int with_pressure);

@@ -51,6 +51,7 @@ class StageArgs(ctypes.Structure):
         ("force", ctypes.c_double * 3),
         ("p_int", vp),
         ("force_field", VP3),
+        ("u0_out", VP3),
     ]
 
 
@@ -87,6 +88,7 @@ _SIGS = {
     "sfb_project": [vp, VP3, vp, vp],
     "sfb_project_solve": [vp, VP3, ctypes.POINTER(vp), vp],
     "sfb_project_launches": [vp, ctypes.c_int],
+    "sfb_project_finish": [vp, VP3, vp, vp],
     "sfb_slab_solver_create": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
     "sfb_slab_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
                          ctypes.POINTER(vp), ctypes.POINTER(vp)],
@@ -185,6 +187,8 @@ def call(name, *args):
         launches += k
         return
     k = KERNELS_PER_CALL.get(name, 0)
+    if name == "sfb_project_finish":
+        k = 2 + (args[2] is not None and args[2] != 0)
     if name in ("sfb_rfftn", "sfb_irfftn"):
         # engine passes (0 on the cuFFT path) + irfftn's normalisation kernel
         k = _FFT_PASSES.get(args[0], 0) + (name == "sfb_irfftn")

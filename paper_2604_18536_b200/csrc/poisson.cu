@@ -717,6 +717,25 @@ int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, v
   return rc;
 }
 
+int sfb_project_finish(sfb_solver* s, void* const* u, void* p_ext, void* stream) {
+  if (!s || !u) return fail(SFB_EINVAL, "null argument");
+  if (s->slab) return fail(SFB_ECONFIG, "sfb_project_finish: slab solvers use sfb_slab_correct");
+  for (int a = 0; a < s->plan->dim; ++a)
+    if (!u[a]) return fail(SFB_EINVAL, "null velocity component");
+  return SFB_TYPED(s->plan, ([&]() {
+    sfb_plan* p = s->plan;
+    const Geo<T>& G = geo<T>(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    MV<T> U;
+    for (int a = 0; a < 3; ++a) U.c[a] = a < p->dim ? (T*)u[a] : nullptr;
+    int rc;
+    if ((rc = launch_grad<T>(G, (T*)s->rbuf, U, (T*)p_ext, st))) return rc;
+    if ((rc = launch_planes<T>(G, U, p->dim, 0, st))) return rc;
+    if (p_ext && (rc = launch_planes<T>(G, MV<T>{{(T*)p_ext, nullptr, nullptr}}, 1, 1, st))) return rc;
+    return (int)SFB_OK;
+  })());
+}
+
 int sfb_project_launches(const sfb_solver* s, int mode) {
   if (!s) return 0;
   const bool fused = s->plan->dtype == SFB_F64 ? divfused<double>(s) : divfused<float>(s);

@@ -9,6 +9,7 @@ template <typename T>
 struct StageArgs {
   CV<T> y, u0, s_in;
   MV<T> s_out, y_next, k_out;
+  MV<T> u0_out;    // FL_U0P: the projected stage-0 state (u0 == y) is written here
   T cb, ca, nu;
   Force<T> F;
   const T* p_int;  // FL_PROJ: contiguous interior pressure; y is projected on the fly
@@ -52,7 +53,11 @@ __device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
 // bit 16: y is unprojected, y - G p is formed in shared memory (all-periodic 3D)
 // bit 32: every axis periodic (every interior cell is a DOF of every component):
 // branch-free stencil evaluation, stores predicated on the tile bounds only
-enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16, FL_PER = 32 };
+// bit 64 (with FL_PROJ, u0 == y): u0 is the stage state itself, projected in
+// shared memory -- the combines take it from the ring centre and it is
+// written once to u0_out (the deferred last projection of the previous step,
+// timestep.py:208-210 fused into the next step's first stage)
+enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16, FL_PER = 32, FL_U0P = 64 };
 
 
 

@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   typedef RingGeom<TJ, TK> RG;
   constexpr bool PROJ = (FL & FL_PROJ) != 0;
   constexpr bool PER = (FL & FL_PER) != 0;
+  constexpr bool U0P = (FL & FL_U0P) != 0;
+  static_assert(!U0P || PROJ, "FL_U0P needs the on-the-fly projection");
   constexpr int NTH = TJ / CPT * TK;                // threads per CTA
   constexpr int NE = 3 * RG::PS;                    // values per plane slot
   constexpr int NQ = (NE + NTH - 1) / NTH;          // fill copies per thread
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
         b0[r][a] = T(0);
         bs[r][a] = T(0);
         if (dof[r][a]) {
-          if ((FL & FL_NEXT) || ((FL & FL_S) && (FL & FL_SU0))) b0[r][a] = A.u0.c[a][x];
+          if (!U0P && ((FL & FL_NEXT) || ((FL & FL_S) && (FL & FL_SU0)))) b0[r][a] = A.u0.c[a][x];
           if ((FL & FL_S) && !(FL & FL_SU0)) bs[r][a] = A.s_in.c[a][x];
         }
       }
@@ -296,9 +298,14 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
         for (int a = 0; a < 3; ++a)
           if (dof[r][a]) kv[a] += A.F.a[a][x];
       }
+      if constexpr (U0P) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) b0[r][a] = P[1][a * RG::PS];  // projected y at the centre
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         if (!dof[r][a]) continue;
+        if (U0P) A.u0_out.c[a][x] = b0[r][a];
         if (FL & FL_K) A.k_out.c[a][x] = kv[a];
         if (FL & FL_S) A.s_out.c[a][x] = ((FL & FL_SU0) ? b0[r][a] : bs[r][a]) + kv[a] * A.cb;
         if (FL & FL_NEXT) A.y_next.c[a][x] = b0[r][a] + kv[a] * A.ca;
@@ -361,8 +368,13 @@ static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st, 
   static const bool noper = env_int("SFB_STAGE_NOPER") != 0;
   const bool per = allow_per && G.per[0] && G.per[1] && G.per[2] && !G.halo[1] && !G.halo[2] && !noper;
   const int fl = (A.has_k ? FL_K : 0) | (A.has_s ? FL_S : 0) | (A.has_s && A.s_from_u0 ? FL_SU0 : 0) |
-                 (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0) | (per ? FL_PER : 0);
+                 (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0) | (per ? FL_PER : 0) |
+                 (A.u0_out.c[0] ? FL_U0P : 0);
   switch (fl) {
+    case FL_PER | FL_S | FL_SU0 | FL_NEXT | FL_PROJ | FL_U0P:
+      return stage_march_launch<T, FL_PER | FL_S | FL_SU0 | FL_NEXT | FL_PROJ | FL_U0P>(G, A, st);
+    case FL_S | FL_SU0 | FL_NEXT | FL_PROJ | FL_U0P:
+      return stage_march_launch<T, FL_S | FL_SU0 | FL_NEXT | FL_PROJ | FL_U0P>(G, A, st);
     case FL_PER | FL_S | FL_NEXT | FL_PROJ: return stage_march_launch<T, FL_PER | FL_S | FL_NEXT | FL_PROJ>(G, A, st);
     case FL_PER | FL_S | FL_PROJ: return stage_march_launch<T, FL_PER | FL_S | FL_PROJ>(G, A, st);
     case FL_PER | FL_S | FL_SU0 | FL_NEXT: return stage_march_launch<T, FL_PER | FL_S | FL_SU0 | FL_NEXT>(G, A, st);
@@ -394,6 +406,7 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
     A.s_out.c[c] = on ? (T*)a->s_out[c] : nullptr;
     A.y_next.c[c] = on ? (T*)a->y_next[c] : nullptr;
     A.k_out.c[c] = on ? (T*)a->k_out[c] : nullptr;
+    A.u0_out.c[c] = on ? (T*)a->u0_out[c] : nullptr;
     A.F.a[c] = on ? (const T*)a->force_field[c] : nullptr;
     A.F.f[c] = (on && !A.F.a[c]) ? (T)a->force[c] : T(0);
   }
@@ -412,6 +425,13 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
       (G.dim == 3 && (A.F.a[0] != nullptr) != (A.F.a[2] != nullptr)))
     return fail(SFB_EINVAL, "force fields: give all components or none");
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
+  if (A.u0_out.c[0]) {
+    if (!A.p_int || a->u0[0] != a->y[0] || !A.has_s || !A.s_from_u0 || A.has_k)
+      return fail(SFB_EINVAL, "u0_out: stage 0 of a deferred projection only (p_int set, u0 == y, s from u0)");
+    for (int c = 0; c < G.dim; ++c)
+      if (A.u0_out.c[c] == (const T*)a->y[c] || A.u0_out.c[c] == A.s_out.c[c] || A.u0_out.c[c] == A.y_next.c[c])
+        return fail(SFB_EINVAL, "u0_out must not alias y, s_out or y_next");
+  }
   if (A.has_s && A.s_from_u0 && !a->u0[0]) return fail(SFB_EINVAL, "s_out requires s_in or u0");
   static const bool generic = env_int("SFB_STAGE_GENERIC") != 0;
   if (G.dim == 3 && (!generic || A.p_int)) {

@@ -106,3 +106,53 @@ def test_rk4_step_at_256_cubed_vs_oracle(P, monkeypatch):
     for a in range(3):
         assert rel(u[a], ref_u[a]) <= 1e-12, a
     assert rel(p, ref_p) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_run_steps_deferred_last_projection(P, dtype):
+    """run_steps with a fixed dt leaves each step's last projection to the
+    next step's first stage kernel (u0 - G p formed in shared memory and
+    written once): the trajectory equals rk_step called step by step and the
+    oracle; observers and the returned state see fully projected fields."""
+    n = (40, 36, 48)
+    bounds = [O.uniform_bounds(0.0, 1.0 + 0.3 * a, m) for a, m in enumerate(n)]
+    pg, og = grids(P, bounds, (True,) * 3, dtype)
+    rng = np.random.default_rng(9)
+    u0 = random_vel(og, rng)
+    O.fill_velocity(og, O.periodic_bcs(3), u0)
+    solve = O.SpectralSolve(og)
+    O.project_into(og, O.periodic_bcs(3), solve, u0)
+    setup = P.Setup(pg, P.BoundarySpec.all_periodic(3), nu=0.02, force=(0.3, 0.0, -0.1), solver="spectral",
+                    method="rk4")
+    dt, K = 2e-3, 4
+    st_a = setup.new_state(u0=vel(P, pg, u0))
+    for _ in range(K):
+        P.rk_step(st_a, dt, P.RK4, setup.solver, setup)
+    seen = []
+
+    def obs(s):
+        seen.append((s.step, [c.clone() for c in s.u.u], s.pressure.data.clone()))
+
+    st_b = setup.new_state(u0=vel(P, pg, u0))
+    P.run_steps(setup, K, dt=dt, state=st_b, project_initial=False, observers=[obs], observer_cadence=3)
+    assert st_b._pending is None
+    ru = [x.copy() for x in u0]
+    t = tol(dtype)
+    for k in range(K):
+        ru, rp = O.rk_step(og, O.periodic_bcs(3), solve, ru, dt, O.RK4, 0.02, (0.3, 0.0, -0.1))
+        if k == 2:
+            assert seen and seen[0][0] == 3
+            for a in range(3):
+                assert rel(seen[0][1][a].cpu().numpy(), ru[a]) <= t
+            assert rel(seen[0][2].cpu().numpy(), rp) <= t
+    ga, gb = st_a.u.numpy(), st_b.u.numpy()
+    for a in range(3):
+        assert rel(gb[a], ga[a]) <= t
+        assert rel(gb[a], ru[a]) <= t
+    assert rel(st_b.pressure.numpy(), rp) <= t
+    assert rel(st_b.pressure.numpy(), st_a.pressure.numpy()) <= t
+    assert float(P.divergence(st_b.u).data.abs().max()) < (1e-10 if dtype == np.float64 else 1e-3)
+    # simulate with a fixed step defers too; adaptive dt never does
+    st_c = P.simulate(setup, K * dt, dt=dt, u0=vel(P, pg, u0), project_initial=False)
+    for a in range(3):
+        assert rel(st_c.u.numpy()[a], ga[a]) <= t
