@@ -76,6 +76,9 @@ class ChannelSolve:
         piv[0, 0] = 1.0
         cprime[:, 0] = up[1] / piv
         d[:, 0] = rh[:, 0] / piv
+        # the (0, 0) column of the sweep is singular and overflows harmlessly:
+        # that mode is replaced by the bordered solve below
+        err = np.seterr(over="ignore", invalid="ignore")
         for jj in range(1, n1):
             jext = jj + 1
             piv = di[jext] + shift - lo[jext] * cprime[:, jj - 1]
@@ -86,6 +89,7 @@ class ChannelSolve:
         x[:, n1 - 1] = d[:, n1 - 1]
         for jj in range(n1 - 2, -1, -1):
             x[:, jj] = d[:, jj] - cprime[:, jj] * x[:, jj + 1]
+        np.seterr(**err)
         # (0, 0): bordered system [[L_y, 1], [dx^T, 0]]
         a_mat = np.zeros((n1 + 1, n1 + 1))
         for jj in range(n1):
