@@ -382,6 +382,8 @@ int cg_setup(sfb_solver* s) {
     if ((rc = cuda_check(cudaMalloc(b, esz * total), "cudaMalloc(cg)"))) return rc;
   if ((rc = cuda_check(cudaMalloc(&s->cg_part, sizeof(double) * 2 * s->cg_nb), "cudaMalloc(cg part)"))) return rc;
   if ((rc = cuda_check(cudaMalloc(&s->cg_dsc, sizeof(double) * S_N), "cudaMalloc(cg scalars)"))) return rc;
+  // every slot defined before the first host read (compute-sanitizer initcheck)
+  if ((rc = cuda_check(cudaMemset(s->cg_dsc, 0, sizeof(double) * S_N), "cudaMemset(cg scalars)"))) return rc;
   if ((rc = cuda_check(cudaMallocHost(&s->cg_hsc, sizeof(double) * S_N), "cudaMallocHost(cg)"))) return rc;
   // total pressure volume (poisson.py:158, np.sum of the weights)
   double wtot = 0.0;

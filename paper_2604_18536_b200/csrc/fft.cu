@@ -419,7 +419,8 @@ static int launch_strided(typename CX<T>::t* data, const FftLen& P, int W, long 
 }
 
 template <typename T>
-static int launch_r2c(FftSolve& F, const T* rbuf, typename CX<T>::t* cbuf, long long rows, cudaStream_t st) {
+static int launch_r2c(FftSolve& F, const T* rbuf, typename CX<T>::t* cbuf, long long rows, cudaStream_t st,
+                      bool tiled = false) {
   typedef typename CX<T>::t C;
   const int nlast = F.n[F.dim - 1], M = nlast / 2, nh = M + 1;
   if (F.reg_half) {
@@ -430,6 +431,8 @@ static int launch_r2c(FftSolve& F, const T* rbuf, typename CX<T>::t* cbuf, long 
     c.rows = rows;
     c.in_row = nlast;
     c.out_row = nh;
+    c.tlog = tiled ? F.tlog : 0;
+    c.ks = F.tks;
     c.twL = F.tw_half;
     c.twN = F.tw_full;
     return reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
@@ -441,7 +444,8 @@ static int launch_r2c(FftSolve& F, const T* rbuf, typename CX<T>::t* cbuf, long 
 }
 
 template <typename T>
-static int launch_c2r(FftSolve& F, const typename CX<T>::t* cbuf, T* rbuf, long long rows, cudaStream_t st) {
+static int launch_c2r(FftSolve& F, const typename CX<T>::t* cbuf, T* rbuf, long long rows, cudaStream_t st,
+                      bool tiled = false) {
   typedef typename CX<T>::t C;
   const int nlast = F.n[F.dim - 1], M = nlast / 2, nh = M + 1;
   if (F.reg_half) {
@@ -452,6 +456,8 @@ static int launch_c2r(FftSolve& F, const typename CX<T>::t* cbuf, T* rbuf, long 
     c.rows = rows;
     c.in_row = nh;
     c.out_row = nlast;
+    c.tlog = tiled ? F.tlog : 0;
+    c.ks = F.tks;
     c.twL = F.tw_half;
     c.twN = F.tw_full;
     return reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
@@ -483,6 +489,10 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
   const int M = nlast / 2;
   const int nh = M + 1;
   const long long rows = F.total / nlast;
+  // tiled spectrum (every pass in the register engine, r2c_epilogue): the
+  // R2C writes it, the strided passes run on contiguous column blocks, the
+  // C2R reads it
+  const bool tiled = F.tlog > 0 && dim == 3 && (!G || fft_divfuse_ok(F, *G));
   // 1. R2C along the contiguous axis (optionally of the divergence of u)
   if (G && fft_divfuse_ok(F, *G)) {
     RegCall c{};
@@ -490,6 +500,8 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
     c.out = cbuf;
     c.rows = rows;
     c.out_row = nh;
+    c.tlog = tiled ? F.tlog : 0;
+    c.ks = F.tks;
     c.twL = F.tw_half;
     c.twN = F.tw_full;
     c.geo = G;
@@ -506,10 +518,29 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
                                                                             (const C*)F.tw_full, nh)));
     SFB_LAUNCH_CHECK("fft r2c (fused divergence)");
   } else {
-    int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st);
+    int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st, tiled);
     if (rc) return rc;
   }
   ScaleArgs none{};
+  if (tiled) {
+    const int n0 = F.n[0], n1 = F.n[1], tw = 1 << F.tlog, nblk = (nh + tw - 1) / tw;
+    int rc;
+    // 2. axis 1 forward: batch (block, k0) = one contiguous (n1, tw) array
+    if ((rc = launch_strided<T, 0>(cbuf, F.ax[1], 0, tw, tw, (long long)n1 * tw, nblk * n0, (const C*)F.tw_ax[1],
+                                   none, st, nullptr, SFB_REG(F, 1))))
+      return rc;
+    // 3. axis 0 forward + scale + inverse: batch = block, columns (k1, w) contiguous
+    ScaleArgs sc = F.sc;
+    sc.tlog = F.tlog;
+    if ((rc = launch_strided<T, 2>(cbuf, F.ax[0], 0, (long long)n1 * tw, n1 * tw, F.tks, nblk, (const C*)F.tw_ax[0],
+                                   sc, st, nullptr, SFB_REG(F, 0))))
+      return rc;
+    // 4. axis 1 inverse
+    if ((rc = launch_strided<T, 1>(cbuf, F.ax[1], 0, tw, tw, (long long)n1 * tw, nblk * n0, (const C*)F.tw_ax[1],
+                                   none, st, nullptr, SFB_REG(F, 1))))
+      return rc;
+    return launch_c2r<T>(F, cbuf, rbuf, rows, st, true);
+  }
   if (dim == 3) {
     const int n0 = F.n[0], n1 = F.n[1];
     // 2. axis 1 forward: S = nh, columns k2 < nh, batch over k0

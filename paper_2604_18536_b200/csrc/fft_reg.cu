@@ -26,6 +26,13 @@ bool reg_factor(int L, RegLen& R) {
   return false;
 }
 
+// column width W of the strided kernels of length L (RegGeo<C, A, B>::W)
+int reg_strided_w(int L, bool f64) {
+  const size_t csz = f64 ? 16 : 8;
+  const int w0 = (int)((f64 ? SFB_REG_SEG : SFB_REG_SEG_F32) / csz);
+  return (size_t)L * w0 * csz <= 112 * 1024 ? w0 : w0 / 2;
+}
+
 int fft_reg_init() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(SFB_ECUDA, "cudaGetDevice");

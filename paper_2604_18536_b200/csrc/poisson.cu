@@ -562,7 +562,22 @@ static int setup_fft(sfb_solver* s) {
   F.sc.zero_ok = 1;
   fft_reg_assign(F);
   F.enabled = true;
-  if (dim == 3 && !getenv("SFB_NO_TMA")) {
+  // tiled spectrum when every pass runs in the register engine (fft.cu)
+  F.tlog = 0;
+  if (dim == 3 && F.reg_half && F.reg_ax[0] && F.reg_ax[1] && !getenv("SFB_FFT_NATURAL")) {
+    const int w1 = reg_strided_w(p->n[1], f64);
+    const int tw = env_int("SFB_FFT_TILE", w1);
+    int lg = 0;
+    while ((1 << lg) < tw) ++lg;
+    // the row kernels' tiled walk (sfb_fft_reg.cuh kTileIt) covers blocks of
+    // 4 or 8 columns, at most one block per thread group of a row
+    const int tt = F.reg_a_half > F.reg_b_half ? F.reg_a_half : F.reg_b_half;
+    if ((1 << lg) == tw && (tw == 4 || tw == 8) && tw <= tt && tw % w1 == 0) {
+      F.tlog = lg;
+      F.tks = (long long)p->n[0] * p->n[1] * tw;
+    }
+  }
+  if (dim == 3 && !getenv("SFB_NO_TMA") && !F.tlog) {
     const int n0 = p->n[0], n1 = p->n[1];
     const long long nh = nlast / 2 + 1;
     // axis-1 pass: box over (nh complex columns, n1 rows, n0 batch); axis-0: (n1*nh, n0)
@@ -628,7 +643,14 @@ int sfb_solver_create(sfb_plan* p, int kind, sfb_solver** out) {
   int rc;
   std::vector<double> host[3];
   if ((rc = cuda_check(cudaMalloc(&s->rbuf, esz * p->int_count), "cudaMalloc(rbuf)"))) goto bad;
-  if ((rc = cuda_check(cudaMalloc(&s->cbuf, 2 * esz * ncomplex), "cudaMalloc(cbuf)"))) goto bad;
+  // room for the tiled spectrum (fft.cu): nh padded to a multiple of the
+  // widest column block (8); zeroed once so the padding columns the axis-0
+  // pass transforms are finite
+  {
+    const long long cpad = kind == SFB_SOLVER_SPECTRAL ? p->int_count / p->n[dlast] * ((nh + 7) / 8 * 8) : ncomplex;
+    if ((rc = cuda_check(cudaMalloc(&s->cbuf, 2 * esz * cpad), "cudaMalloc(cbuf)"))) goto bad;
+    if ((rc = cuda_check(cudaMemset(s->cbuf, 0, 2 * esz * cpad), "cudaMemset(cbuf)"))) goto bad;
+  }
   // eigenvalue tables lam_a[k] = (2 cos(2 pi k / n) - 2) / h^2 (poisson.py:180-186)
   for (int a = 0; a < 3; ++a) {
     int n = a < p->dim ? p->n[a] : 1;

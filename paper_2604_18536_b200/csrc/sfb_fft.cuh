@@ -21,6 +21,8 @@ struct ScaleArgs {
   const double *l0, *l1, *l2; // per-axis eigenvalue tables (fp64)
   double invN;                // 1 / (n0 n1 n2): the irfftn normalisation
   int zero_ok;                // this chunk holds the k = 0 mode (zeroed)
+  int tlog;                   // > 0: tiled spectrum (fft.cu): batch = k2 block of 2^tlog
+                              // columns, column = k1 * 2^tlog + k2 % 2^tlog
 };
 
 // TMA description of one strided pass: a (2W x Lb [x batch]) box over the
@@ -46,11 +48,17 @@ struct FftSolve {
   // register-resident engine (sfb_fft_reg.cuh) per pass, when instantiated
   int reg_half = 0, reg_ax[3] = {0, 0, 0};  // 0 = Stockham engine, else L
   int reg_a_half = 0, reg_b_half = 0, reg_a[3] = {0, 0, 0}, reg_b[3] = {0, 0, 0};
+  // tiled half spectrum of the 3D solve (r2c_epilogue in sfb_fft_reg.cuh):
+  // blocks of 2^tlog columns, block stride tks; 0 = natural layout
+  int tlog = 0;
+  long long tks = 0;
 };
 
 bool fft_factor(int L, FftLen& P);
 // choose the register engine for every pass whose length is instantiated
 void fft_reg_assign(FftSolve& F);
+// column width of the register engine's strided kernels for length L (fft_reg.cu)
+int reg_strided_w(int L, bool f64);
 int fft_upload_twiddles(int L, bool f64, void** dev);
 int fft_upload_pass_twiddles(FftLen& P, bool f64, void** dev);
 // Spectral solve in place on rbuf.  When G/u are given, the right-hand side

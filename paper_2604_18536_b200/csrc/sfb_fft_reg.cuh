@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
                                   MODE == 2 ? RegGeo<typename CX<T>::t, A, B>::MINB_S2 : RegGeo<typename CX<T>::t, A, B>::MINB_S)
     k_rfft_strided(const typename CX<T>::t* __restrict__ in, typename CX<T>::t* __restrict__ data, long long S,
                    int ncol, long long bin, long long bstride, RowSplit mp, const typename CX<T>::t* __restrict__ twL,
-                   ScaleArgs sc) {
+                   ScaleArgs sc, int swap) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
   constexpr int W = RG::W, XS = RG::XS;
@@ -245,10 +245,12 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
   C* twlo = buf + B * XS;
   C* twhi = twlo + 32;
   const int w = threadIdx.x % W, t = threadIdx.x / W;
-  const int col = blockIdx.x * W + w;
+  // grid: (column blocks, batches), or swapped when the batches exceed grid.y
+  const int cblk = swap ? blockIdx.y : blockIdx.x, bat = swap ? blockIdx.x : blockIdx.y;
+  const int col = cblk * W + w;
   const bool ok = col < ncol;
-  C* base = data + (long long)blockIdx.y * bstride + (ok ? col : 0);
-  const C* ibase = in + (long long)blockIdx.y * bin + (ok ? col : 0);
+  C* base = data + (long long)bat * bstride + (ok ? col : 0);
+  const C* ibase = in + (long long)bat * bin + (ok ? col : 0);
   constexpr bool INV1 = MODE == 1 || MODE == 4;
   const long long gs = (long long)B * S;
   auto mapped = [&](int r) -> long long { return (long long)(r / mp.c) * mp.sq + (long long)(r % mp.c) * mp.s; };
@@ -292,13 +294,20 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
       // eigenvalue scaling (poisson.py:179-199): lam in fp64, cast to T
       double lc = 0.0, l2v = 0.0;
       if (sc.dim == 3) {
-        const int c1 = col / sc.nh, c2 = col - c1 * sc.nh;
+        int c1, c2;
+        if (sc.tlog > 0) {  // tiled spectrum: batch = k2 block; padding columns clamp (never read back)
+          c1 = col >> sc.tlog;
+          c2 = min((bat << sc.tlog) + (col & ((1 << sc.tlog) - 1)), sc.nh - 1);
+        } else {
+          c1 = col / sc.nh;
+          c2 = col - c1 * sc.nh;
+        }
         lc = ok ? sc.l1[c1] : 0.0;
         l2v = ok ? sc.l2[c2] : 0.0;
       } else {
         lc = ok ? sc.l1[col] : 0.0;
       }
-      const bool zmode = col == 0 && blockIdx.y == 0 && sc.zero_ok;
+      const bool zmode = col == 0 && bat == 0 && sc.zero_ok;
 #pragma unroll
       for (int k2 = 0; k2 < B; ++k2) {
         const int m = k1 + A * k2;
@@ -346,10 +355,71 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
 // ---------------------------------------------------------------------------
 // contiguous-axis real transforms, M = A*B complex points per row (N = 2M reals)
 // ---------------------------------------------------------------------------
+// loads per thread of the tiled C2R staging: blocks of tw >= 4 columns, RP
+// rows per CTA, NT_R = RP * TT threads walking TT / tw blocks at a time
+// (tw <= TT; fft.cu falls back to the natural layout otherwise)
+template <int M, int TT>
+constexpr int kTileIt = ((M + 4) / 4 + TT / 4 - 1) / (TT / 4) > ((M + 8) / 8 + TT / 8 - 1) / (TT / 8 > 0 ? TT / 8 : 1)
+                            ? ((M + 4) / 4 + TT / 4 - 1) / (TT / 4)
+                            : ((M + 8) / 8 + TT / 8 - 1) / (TT / 8 > 0 ? TT / 8 : 1);
+
+// Tiled half spectrum (single-GPU spectral solve, fft.cu): element (row, k) of
+// the natural (rows, M+1) layout sits at (k >> tlog) * ks + row * 2^tlog +
+// (k & (2^tlog - 1)) -- blocks of 2^tlog columns, each block a contiguous
+// (rows, 2^tlog) array.  The strided passes then read contiguous 2^tlog-wide
+// column blocks (axis 1: one whole block per CTA; axis 0: rows of the block
+// 64 bytes x n1 apart instead of a 64-byte segment per plane, 5.7 MB apart).
+// tlog <= 0: natural layout.
+//
+// R2C epilogue: X[k] = E[k] + w^k O[k], E = (Z[k] + conj Z[M-k]) / 2,
+// O = (Z[k] - conj Z[M-k]) / (2i), from the CTA's rows in shared memory (row
+// r at r * ROWBUF).  Tiled stores run over (block, row, w) with w fastest, so
+// a warp writes the CTA's consecutive rows of one block contiguously.
+template <typename T, int A, int B>
+__device__ __forceinline__ void r2c_epilogue(const typename CX<T>::t* __restrict__ sbuf, typename CX<T>::t* __restrict__ out,
+                                             long long row0, long long rows, long long out_row,
+                                             const typename CX<T>::t* __restrict__ twN, int tlog, long long ks) {
+  typedef typename CX<T>::t C;
+  typedef RegGeo<C, A, B> RG;
+  constexpr int M = A * B, TT = RG::TT;
+  auto val = [&](const C* buf, int k) -> C {
+    const C zk = buf[k == M ? 0 : k];
+    const C zc = buf[k == 0 ? 0 : M - k];
+    C e, od;
+    e.x = T(0.5) * (zk.x + zc.x);
+    e.y = T(0.5) * (zk.y - zc.y);
+    od.x = T(0.5) * (zk.y + zc.y);
+    od.y = -T(0.5) * (zk.x - zc.x);
+    const C w = __ldg(twN + k);
+    return cadd(e, cmul(w, od));
+  };
+  if (tlog > 0) {
+    // a thread owns one (row, w) slot of every block it walks (see k_rfft_c2r)
+    const int tw = 1 << tlog, nslot = RG::RP << tlog, ng = RG::NT_R / nslot, nblk = (M + tw) >> tlog;
+    const int slot = threadIdx.x % nslot, g = threadIdx.x / nslot;
+    const int r = slot >> tlog, w = slot & (tw - 1);
+    const long long row = row0 + r;
+    if (g >= ng || row >= rows) return;
+    C* dst = out + row * tw + w;
+    const C* sb = sbuf + r * RG::ROWBUF;
+    for (int K = g; K < nblk; K += ng) {
+      const int k = (K << tlog) + w;
+      if (k <= M) __stcs(dst + K * ks, val(sb, k));
+    }
+    return;
+  }
+  const int r = threadIdx.x / TT, t = threadIdx.x % TT;
+  const long long row = row0 + r;
+  if (row >= rows) return;
+  C* o = out + row * out_row;
+  for (int k = t; k <= M; k += TT) __stcs(o + k, val(sbuf + r * RG::ROWBUF, k));
+}
+
 template <typename T, int A, int B>
 __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_ROW_MINB))
     k_rfft_r2c(const T* __restrict__ in, typename CX<T>::t* __restrict__ out, long long rows, long long in_row,
-               long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
+               long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN,
+               int tlog, long long ks) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
   constexpr int M = A * B, TT = RG::TT, AP = RG::AP;
@@ -386,20 +456,8 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW
     for (int k2 = 0; k2 < B; ++k2) buf[t + A * k2] = v[k2];
   }
   __syncthreads();
-  if (!okr) return;
-  C* o = out + row * out_row;
-  // X[k] = E[k] + w^k O[k],  E = (Z[k] + conj Z[M-k]) / 2,  O = (Z[k] - conj Z[M-k]) / (2i)
-  for (int k = t; k <= M; k += TT) {
-    const C zk = buf[k == M ? 0 : k];
-    const C zc = buf[k == 0 ? 0 : M - k];
-    C e, od;
-    e.x = T(0.5) * (zk.x + zc.x);
-    e.y = T(0.5) * (zk.y - zc.y);
-    od.x = T(0.5) * (zk.y + zc.y);
-    od.y = -T(0.5) * (zk.x - zc.x);
-    const C w = __ldg(twN + k);
-    __stcs(o + k, cadd(e, cmul(w, od)));
-  }
+  r2c_epilogue<T, A, B>(reinterpret_cast<const C*>(smem_raw), out, (long long)blockIdx.x * RG::RP, rows, out_row, twN,
+                        tlog, ks);
 }
 
 // R2C of the projection right-hand side computed on the fly: the real input
@@ -422,7 +480,8 @@ __device__ __forceinline__ T div_at(const Geo<T>& G, const T* __restrict__ u0, c
 template <typename T, int A, int B>
 __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_R2CDIV_MINB))
     k_rfft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, long long rows, long long out_row,
-                   const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
+                   const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN, int tlog,
+                   long long ks) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
   constexpr int M = A * B, TT = RG::TT, AP = RG::AP;
@@ -472,25 +531,15 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW
     for (int k2 = 0; k2 < B; ++k2) buf[t + A * k2] = v[k2];
   }
   __syncthreads();
-  if (!okr) return;
-  C* o = out + row * out_row;
-  for (int k = t; k <= M; k += TT) {
-    const C zk = buf[k == M ? 0 : k];
-    const C zc = buf[k == 0 ? 0 : M - k];
-    C e, od;
-    e.x = T(0.5) * (zk.x + zc.x);
-    e.y = T(0.5) * (zk.y - zc.y);
-    od.x = T(0.5) * (zk.y + zc.y);
-    od.y = -T(0.5) * (zk.x - zc.x);
-    const C w = __ldg(twN + k);
-    __stcs(o + k, cadd(e, cmul(w, od)));
-  }
+  r2c_epilogue<T, A, B>(reinterpret_cast<const C*>(smem_raw), out, (long long)blockIdx.x * RG::RP, rows, out_row, twN,
+                        tlog, ks);
 }
 
 template <typename T, int A, int B>
 __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_ROW_MINB))
     k_rfft_c2r(const typename CX<T>::t* __restrict__ in, T* __restrict__ out, long long rows, long long in_row,
-               long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN) {
+               long long out_row, const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN,
+               int tlog, long long ks) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
   constexpr int M = A * B, TT = RG::TT, AP = RG::AP;
@@ -499,10 +548,37 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW
   const long long row = (long long)blockIdx.x * RG::RP + r;
   const bool okr = row < rows;
   C* buf = reinterpret_cast<C*>(smem_raw) + r * RG::ROWBUF;
+  const C* X = in + (okr ? row : 0) * in_row;
+  if (tlog > 0) {
+    // tiled spectrum (see r2c_epilogue): stage the CTA's rows through shared
+    // memory, each block's rows read contiguously
+    // a thread owns one (row, w) slot of every block it walks (the CTA's
+    // rows of one block are contiguous): no per-element index division, and
+    // all of its loads are issued before the first shared store
+    const int tw = 1 << tlog, nslot = RG::RP << tlog, ng = RG::NT_R / nslot, nblk = (M + tw) >> tlog;
+    const int slot = threadIdx.x % nslot, g = threadIdx.x / nslot;
+    const int rr = slot >> tlog, w = slot & (tw - 1);
+    const long long rowt = (long long)blockIdx.x * RG::RP + rr;
+    const bool okt = g < ng && rowt < rows;
+    const C* src = in + rowt * tw + w;
+    C* sb = reinterpret_cast<C*>(smem_raw) + rr * RG::ROWBUF + w;
+    C tmp[kTileIt<M, TT>];
+#pragma unroll
+    for (int q = 0; q < kTileIt<M, TT>; ++q) {
+      const int K = g + q * ng, k = (K << tlog) + w;
+      tmp[q] = okt && K < nblk && k <= M ? __ldcs(src + K * ks) : czero<C>();
+    }
+#pragma unroll
+    for (int q = 0; q < kTileIt<M, TT>; ++q) {
+      const int K = g + q * ng;
+      if (okt && K < nblk && (K << tlog) + w <= M) sb[K << tlog] = tmp[q];
+    }
+    __syncthreads();
+    X = buf;
+  }
+  C v[A];
   if (t < B) {
     const int n2 = t;
-    const C* X = in + (okr ? row : 0) * in_row;
-    C v[A];
     // Z[k] = (X[k] + conj X[M-k]) + i (X[k] - conj X[M-k]) exp(+2 pi i k / N)
 #pragma unroll
     for (int n1 = 0; n1 < A; ++n1) {
@@ -524,6 +600,10 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW
       }
       v[n1] = z;
     }
+  }
+  if (tlog > 0) __syncthreads();  // every staged row read before the exchange overwrites it
+  if (t < B) {
+    const int n2 = t;
     rdft<C, A, true>(v);
 #pragma unroll
     for (int k1 = 0; k1 < A; ++k1) {
@@ -570,6 +650,8 @@ struct RegCall {
   ScaleArgs sc;
   const void* geo;     // kind 5: host Geo<T> of the velocity plan
   const void* u[3];    // kind 5: extended velocity components
+  int tlog;            // kinds 3-5: tiled spectrum (r2c_epilogue), 0 = natural
+  long long ks;        //   its block stride
 };
 
 static int reg_upload_tables() {
@@ -606,7 +688,9 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     if (e != cudaSuccess) return -2;
   }
   if (c.kind <= 2 || c.kind == 6 || c.kind == 7) {
-    dim3 grid((c.ncol + RG::W - 1) / RG::W, c.nbatch);
+    const unsigned nblk = (unsigned)((c.ncol + RG::W - 1) / RG::W);
+    const int swap = c.nbatch > 65535;  // grid.y limit: batches on x
+    const dim3 grid = swap ? dim3(c.nbatch, nblk) : dim3(nblk, c.nbatch);
     C* d = (C*)c.out;
     const C* src = c.in ? (const C*)c.in : d;
     const long long bin = c.in ? c.bstride_in : c.bstride;
@@ -614,7 +698,7 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     const C* tw = (const C*)c.twL;
 #define SFB_STRIDED(M)                                                                                     \
   k_rfft_strided<T, A, B, M><<<grid, RG::NT_S, M == 2 ? RG::SMEM_S2 : RG::SMEM_S, st>>>(src, d, c.S, c.ncol, bin, c.bstride, mp, tw, \
-                                                                 c.sc)
+                                                                 c.sc, swap)
     switch (c.kind) {
       case 0: SFB_STRIDED(0); break;
       case 1: SFB_STRIDED(1); break;
@@ -627,15 +711,15 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     const unsigned nb = (unsigned)((c.rows + RG::RP - 1) / RG::RP);
     if (c.kind == 3)
       k_rfft_r2c<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>((const T*)c.in, (C*)c.out, c.rows, c.in_row, c.out_row,
-                                                          (const C*)c.twL, (const C*)c.twN);
+                                                          (const C*)c.twL, (const C*)c.twN, c.tlog, c.ks);
     else if (c.kind == 4)
       k_rfft_c2r<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>((const C*)c.in, (T*)c.out, c.rows, c.in_row, c.out_row,
-                                                          (const C*)c.twL, (const C*)c.twN);
+                                                          (const C*)c.twL, (const C*)c.twN, c.tlog, c.ks);
     else {
       CV<T> U;
       for (int a = 0; a < 3; ++a) U.c[a] = (const T*)c.u[a];
       k_rfft_r2c_div<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>(*(const Geo<T>*)c.geo, U, (C*)c.out, c.rows, c.out_row,
-                                                              (const C*)c.twL, (const C*)c.twN);
+                                                              (const C*)c.twL, (const C*)c.twN, c.tlog, c.ks);
     }
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;

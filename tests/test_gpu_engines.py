@@ -60,6 +60,20 @@ def test_register_fft_solve_vs_oracle_and_stockham(P, shape, dtype, monkeypatch)
     assert rel(got, old) <= (1e-13 if dtype == np.float64 else 1e-5)
 
 
+@pytest.mark.parametrize("shape", [(840, 6, 8), (6, 840, 40), (96, 64, 512), (48, 40, 32), (20, 24, 420)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_tiled_spectrum_bitwise_natural(P, shape, dtype, monkeypatch):
+    """The 3D solve's tiled half spectrum (column blocks, fft.cu) runs the
+    same per-column arithmetic as the natural layout: bitwise-equal pressure,
+    including ragged last blocks (n2/2+1 not a multiple of the block width)."""
+    monkeypatch.delenv("SFB_FFT_NATURAL", raising=False)
+    tiled, ref = _solve(P, shape, dtype, monkeypatch, stockham=False)
+    monkeypatch.setenv("SFB_FFT_NATURAL", "1")
+    nat, _ = _solve(P, shape, dtype, monkeypatch, stockham=False)
+    assert np.array_equal(tiled, nat)
+    assert rel(tiled, ref) <= (1e-12 if dtype == np.float64 else 1e-5)
+
+
 def _rk4(P, n, dtype, monkeypatch, env):
     for k in ("SFB_NO_PROJFUSE", "SFB_NO_DIVFUSE"):
         monkeypatch.delenv(k, raising=False)
