@@ -16,56 +16,9 @@
 #include "sfb_fft.cuh"
 #include "sfb_fft_dev.cuh"
 #include "sfb_kernels.cuh"
+#include "sfb_tma.cuh"
 
 namespace sfb {
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arm(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
-  const unsigned a = smem_u32(bar);
-  unsigned ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(phase)
-        : "memory");
-  }
-}
-
-__device__ __forceinline__ void tma_load(const CUtensorMap* tm, int rank, void* dst, unsigned long long* bar, int c0,
-                                         int c1, int c2) {
-  const unsigned long long tp = reinterpret_cast<unsigned long long>(tm);
-  if (rank == 3)
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
-            "r"(smem_u32(dst)),
-        "l"(tp), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-  else
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(tp), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_store(const CUtensorMap* tm, int rank, const void* src, int c0, int c1, int c2) {
-  const unsigned long long tp = reinterpret_cast<unsigned long long>(tm);
-  if (rank == 3)
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(tp), "r"(c0),
-                 "r"(c1), "r"(c2), "r"(smem_u32(src))
-                 : "memory");
-  else
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(tp), "r"(c0),
-                 "r"(c1), "r"(smem_u32(src))
-                 : "memory");
-}
 
 struct TmaTile {
   int rank;   // 3: (2W, rows, batch) map; 2: (2W, rows) map
@@ -177,15 +130,15 @@ __global__ void __launch_bounds__(NT, 1) k_fft_tma(const __grid_constant__ CUten
 // ---------------------------------------------------------------------------
 // host side: tensor maps and launches
 // ---------------------------------------------------------------------------
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-  }
+      return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -196,7 +149,7 @@ static int tma_w(bool f64) { return f64 ? 4 : 8; }
 // (2W x rows [x batch]) box over a complex array viewed as doubles/floats
 int fft_tma_make(FftTma& M, void* base, bool f64, int rank, long long inner_complex, long long rows,
                  long long batch, int L) {
-  PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encode_fn();
   if (!enc) return fail(SFB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int W = tma_w(f64);
   const size_t esz = f64 ? 8 : 4;

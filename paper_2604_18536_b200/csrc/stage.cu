@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "sfb_stage.cuh"
+#include "sfb_tma.cuh"
 
 namespace sfb {
 
@@ -46,6 +47,16 @@ __global__ void __launch_bounds__(256) k_stage_generic(Geo<T> G, StageArgs<T> A,
 template <int TJ, int TK>
 struct RingGeom {
   static constexpr int PW = TK + 2, PH = TJ + 2, PS = PW * PH, NT = TJ * TK;
+  // component stride inside a plane slot, padded so each component's TMA box
+  // lands 128-byte aligned
+  static constexpr int CS = (PS + 15) / 16 * 16;
+};
+
+// TMA descriptors of the three stage-state components: (TK+2) x (TJ+2) x 1
+// boxes over the extended array (fp64, even row pitch); ok = 0 -> cp.async fill
+struct alignas(64) StageMaps {
+  CUtensorMap y[3];
+  int ok;
 };
 
 // Momentum RHS of component A at the thread's cell from the smem ring, same
@@ -54,7 +65,7 @@ struct RingGeom {
 template <typename T, int A, int TJ, int TK>
 __device__ __forceinline__ T rhs_ring(const T* const (&P)[3], const Coef<T> (&C)[3], bool diff, T nu, T fa) {
   typedef RingGeom<TJ, TK> RG;
-  auto Y = [&](int c, int di, int dj, int dk) -> T { return P[1 + di][c * RG::PS + dj * RG::PW + dk]; };
+  auto Y = [&](int c, int di, int dj, int dk) -> T { return P[1 + di][c * RG::CS + dj * RG::PW + dk]; };
   const T uc = Y(A, 0, 0, 0);
   T up[3], um[3];
   up[0] = Y(A, 1, 0, 0);
@@ -97,20 +108,22 @@ constexpr int kRing = 5;   // planes i-1, i, i+1 in use, i+2 landing, i+3 issued
 constexpr int kPRing = 4;  // FL_PROJ: pressure planes, slot = plane & 3
 
 template <typename T, int TJ, int TK, int CPT, int FL, int MINB>
-__global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, StageArgs<T> A, int chunk) {
+__global__ void __launch_bounds__(TJ / CPT * TK, MINB)
+    k_stage_march(Geo<T> G, StageArgs<T> A, int chunk, const __grid_constant__ StageMaps SM) {
   typedef RingGeom<TJ, TK> RG;
   constexpr bool PROJ = (FL & FL_PROJ) != 0;
   constexpr bool PER = (FL & FL_PER) != 0;
   constexpr bool U0P = (FL & FL_U0P) != 0;
   static_assert(!U0P || PROJ, "FL_U0P needs the on-the-fly projection");
   constexpr int NTH = TJ / CPT * TK;                // threads per CTA
-  constexpr int NE = 3 * RG::PS;                    // values per plane slot
+  constexpr int NE = 3 * RG::CS;                    // values per plane slot (padded components)
   constexpr int NQ = (NE + NTH - 1) / NTH;          // fill copies per thread
   constexpr int RS = TJ / CPT;                      // row stride between a thread's cells
   constexpr int PPW = TK + 3, PPS = (TJ + 3) * PPW; // FL_PROJ pressure slot (j0-1 .. j0+TJ+1)
   constexpr int NQP = PROJ ? (PPS + NTH - 1) / NTH : 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw);         // [kRing][3][PS]
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);         // [kRing][3][CS]
+  __shared__ __align__(8) unsigned long long ybar[kRing];  // TMA completion of each plane slot
   Coef<T>* cj = reinterpret_cast<Coef<T>*>(ring + kRing * NE);  // axis-1 coefficients of the tile rows
   T* pring = reinterpret_cast<T*>(cj + TJ);         // FL_PROJ: [kPRing][PPS]
   const int tk = threadIdx.x, tq = threadIdx.y, tid = tq * TK + tk;
@@ -126,12 +139,12 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int e = tid + q * NTH;
-    const int c = e / RG::PS;
-    const int r = e - c * RG::PS;
+    const int c = e / RG::CS;
+    const int r = e - c * RG::CS;
     const int jj = r / RG::PW;
     const int kk = r - jj * RG::PW;
     int gj = j0 - 1 + jj, gk = k0 - 1 + kk;
-    fok[q] = e < NE && gj < G.E[1] && gk < G.E[2];
+    fok[q] = e < NE && r < RG::PS && gj < G.E[1] && gk < G.E[2];
     if (PROJ) {
       gj = wrap1(gj, n1);
       gk = wrap1(gk, n2);
@@ -154,6 +167,25 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   // slab (halo axis 0): y ghost planes exchanged, pressure planes 0..m+2 stored
   // (sfb_slab_buffers p_slab); otherwise periodic wrap into the n0 planes
   const bool h0 = G.halo[0] != 0;
+  // y planes by TMA (one thread, three boxes per plane, mbarrier completion)
+  // unless the tile's halo wraps around a periodic edge of an unprojected
+  // stage state (FL_PROJ: its ghosts are never filled) -- those edge tiles
+  // keep the per-element wrapped cp.async fill
+  const bool tma = SM.ok && (!PROJ || (blockIdx.x > 0 && k0 + TK <= n2 && blockIdx.y > 0 && j0 + TJ <= n1));
+  unsigned yph = 0, ypend = 0;  // per-slot barrier parity / loads in flight (tracked by every thread)
+  if (tma && tid == 0) {
+#pragma unroll
+    for (int b = 0; b < kRing; ++b) mbar_init(&ybar[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto ywait = [&](int slot) {
+    if (tma && ((ypend >> slot) & 1)) {
+      mbar_wait(&ybar[slot], (yph >> slot) & 1);
+      yph ^= 1u << slot;
+      ypend &= ~(1u << slot);
+    }
+  };
   auto load_p = [&](int ip) {
     if constexpr (PROJ) {
       // slab: planes 0..m+2 = 0..E[0] exist; periodic: wrap1 covers 1-n0..2n0.
@@ -168,11 +200,22 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
   };
   auto load_plane = [&](int ip, int slot, bool with_p = true) {
     if (ip < 0 || ip >= G.E[0]) return;
-    T* dst = ring + slot * NE + tid;
-    const long long base = (long long)(PROJ && !h0 ? wrap1(ip, n0) : ip) * s0;
+    const int pl = PROJ && !h0 ? wrap1(ip, n0) : ip;
+    if (tma) {
+      ypend |= 1u << slot;
+      if (tid == 0) {
+        T* dst = ring + slot * NE;
+        mbar_arm(&ybar[slot], 3u * RG::PS * (unsigned)sizeof(T));
 #pragma unroll
-    for (int q = 0; q < NQ; ++q)
-      if (q < NQ - 1 || tid + q * NTH < NE) cp_async_val(dst + q * NTH, fsrc[q] + (fok[q] ? base : 0), fok[q]);
+        for (int c = 0; c < 3; ++c) tma_load(&SM.y[c], 3, dst + c * RG::CS, &ybar[slot], k0 - 1, j0 - 1, pl);
+      }
+    } else {
+      T* dst = ring + slot * NE + tid;
+      const long long base = (long long)pl * s0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < NQ - 1 || tid + q * NTH < NE) cp_async_val(dst + q * NTH, fsrc[q] + (fok[q] ? base : 0), fok[q]);
+    }
     if (with_p) load_p(ip + 1);  // the pressure plane this y plane's projection needs besides its own
   };
   // y -= G p on one freshly landed plane slot (poisson.py:334-339 arithmetic).
@@ -207,8 +250,8 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
           const int po = jj * PPW + kk;
           const T p0 = pc[po];
           ys[r] -= (pn[po] - p0) * r0;
-          ys[RG::PS + r] -= (pc[po + PPW] - p0) * rdj[jj];
-          ys[2 * RG::PS + r] -= (pc[po + 1] - p0) * rdk[kk];
+          ys[RG::CS + r] -= (pc[po + PPW] - p0) * rdj[jj];
+          ys[2 * RG::CS + r] -= (pc[po + 1] - p0) * rdk[kk];
         }
       }
     }
@@ -258,14 +301,22 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
       }
     }
     C[0] = coef_at(G, 0, i);
-    if (PROJ && i == ib + 1) cp_wait<0>();
-    else cp_wait<1>();
-    __syncthreads();
     int sl_l = sl_m + 4;
     if (sl_l >= kRing) sl_l -= kRing;
     int s1i = sl_m + 1, s2i = sl_m + 2;
     if (s1i >= kRing) s1i -= kRing;
     if (s2i >= kRing) s2i -= kRing;
+    if (i == ib) {
+      ywait(sl_m);
+      ywait(s1i);
+    }
+    ywait(s2i);
+    if (PROJ && i == ib + 1) cp_wait<0>();
+    else cp_wait<1>();
+    // this thread's generic-proxy accesses of the slot refilled below (read by
+    // the stencil, rewritten by the projection) ordered before the TMA overwrite
+    if (tma) fence_proxy_async_smem();
+    __syncthreads();
     if constexpr (PROJ) {
       if (i == ib) {
         project_plane(i - 1, sl_m);
@@ -300,7 +351,7 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
       }
       if constexpr (U0P) {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) b0[r][a] = P[1][a * RG::PS];  // projected y at the centre
+        for (int a = 0; a < 3; ++a) b0[r][a] = P[1][a * RG::CS];  // projected y at the centre
       }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -314,6 +365,9 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
     sl_m = s1i;
   }
   cp_wait<0>();
+  // no TMA write may still target this CTA's shared memory when it exits
+#pragma unroll
+  for (int b = 0; b < kRing; ++b) ywait(b);
 }
 
 #ifndef SFB_STAGE_TJ
@@ -327,6 +381,31 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB) k_stage_march(Geo<T> G, S
 #endif
 constexpr int kTJ = SFB_STAGE_TJ, kTK = SFB_STAGE_TK, kCPT = SFB_STAGE_CPT;
 
+// TMA maps of the stage state y (fp64 only: a (TK+2)-wide fp32 box row is not
+// a multiple of 16 bytes); SM.ok = 0 keeps the cp.async fill
+template <typename T>
+static void stage_maps(const Geo<T>& G, const StageArgs<T>& A, StageMaps& SM) {
+  SM.ok = 0;
+  static const bool off = env_int("SFB_STAGE_NOTMA") != 0;
+  if (sizeof(T) != 8 || off || G.dim != 3) return;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encode_fn();
+  if (!enc) return;
+  const size_t esz = sizeof(T);
+  if ((G.s[1] * esz) % 16 || (G.s[0] * esz) % 16) return;
+  cuuint64_t dims[3] = {(cuuint64_t)G.E[2], (cuuint64_t)G.E[1], (cuuint64_t)G.E[0]};
+  cuuint64_t strides[2] = {(cuuint64_t)(G.s[1] * esz), (cuuint64_t)(G.s[0] * esz)};
+  cuuint32_t box[3] = {(cuuint32_t)(kTK + 2), (cuuint32_t)(kTJ + 2), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  for (int c = 0; c < 3; ++c) {
+    if (!A.y.c[c] || ((uintptr_t)A.y.c[c] % 16)) return;
+    if (enc(&SM.y[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A.y.c[c], dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return;
+  }
+  SM.ok = 1;
+}
+
 template <typename T, int FL>
 static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
   typedef RingGeom<kTJ, kTK> RG;
@@ -337,7 +416,7 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
 #define SFB_STAGE_MINB_PROJ 3
 #endif
   constexpr int MINB = (FL & FL_PROJ) ? SFB_STAGE_MINB_PROJ : SFB_STAGE_MINB;
-  const size_t smem = (size_t)kRing * 3 * RG::PS * sizeof(T) + kTJ * sizeof(Coef<T>) +
+  const size_t smem = (size_t)kRing * 3 * RG::CS * sizeof(T) + kTJ * sizeof(Coef<T>) +
                       ((FL & FL_PROJ) ? ((size_t)kPRing * (kTJ + 3) * (kTK + 3) + kTJ + kTK + 4) * sizeof(T) : 0);
   if (cudaError_t e = ensure_smem((const void*)k_stage_march<T, kTJ, kTK, kCPT, FL, MINB>, smem))
     return cuda_check(e, "rk stage: shared-memory attribute");
@@ -356,7 +435,16 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
   int chunk = (int)((G.n[0] + want - 1) / want);
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;
-  k_stage_march<T, kTJ, kTK, kCPT, FL, MINB><<<dim3(bx, by, bz), dim3(kTK, kTJ / kCPT), smem, st>>>(G, A, chunk);
+  // TMA fill for the stages whose running sum is carried in s (FL_PROJ
+  // without FL_SU0: stages 1-3).  Stage 0 (s formed from u0) measured slower
+  // with it (840^3: FL46 11.3 -> 13.0 ms, FL126 18.5 -> 20.9 ms; more DRAM
+  // re-reads and long-scoreboard stalls), stages 1-2 / 3 faster (17.8 -> 16.3,
+  // 13.8 -> 12.8 ms; profiles/r2/stage_tma)
+  StageMaps SM;
+  SM.ok = 0;
+  static const bool tma_all = env_int("SFB_STAGE_TMA_ALL") != 0;
+  if (tma_all || ((FL & FL_PROJ) && !(FL & FL_SU0))) stage_maps<T>(G, A, SM);
+  k_stage_march<T, kTJ, kTK, kCPT, FL, MINB><<<dim3(bx, by, bz), dim3(kTK, kTJ / kCPT), smem, st>>>(G, A, chunk, SM);
   SFB_LAUNCH_CHECK("rk stage (march)");
   return SFB_OK;
 }
