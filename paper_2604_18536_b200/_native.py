@@ -10,7 +10,8 @@ import os
 from .errors import ConfigurationError, ConvergenceError, NumericalError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstagflow_b200.so")
+# SFB_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("SFB_LIB") or os.path.join(HERE, "libstagflow_b200.so")
 
 SFB_OK, SFB_EINVAL, SFB_ECONFIG, SFB_ENUMERIC, SFB_ECUDA, SFB_ECONVERGE = range(6)
 SFB_F64, SFB_F32 = 0, 1

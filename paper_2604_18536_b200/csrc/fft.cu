@@ -492,7 +492,9 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
   // tiled spectrum (every pass in the register engine, r2c_epilogue): the
   // R2C writes it, the strided passes run on contiguous column blocks, the
   // C2R reads it
-  const bool tiled = F.tlog > 0 && dim == 3 && (!G || fft_divfuse_ok(F, *G));
+  // hybrid: natural rows, the strided passes on a tiled copy (F.tbuf)
+  const bool hybrid = F.tlog > 0 && dim == 3 && F.tbuf;
+  const bool tiled = F.tlog > 0 && dim == 3 && !F.tbuf && (!G || fft_divfuse_ok(F, *G));
   // 1. R2C along the contiguous axis (optionally of the divergence of u)
   if (G && fft_divfuse_ok(F, *G)) {
     RegCall c{};
@@ -522,6 +524,45 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
     if (rc) return rc;
   }
   ScaleArgs none{};
+  if (hybrid) {
+    const int n0 = F.n[0], n1 = F.n[1], tw = 1 << F.tlog, nblk = (nh + tw - 1) / tw;
+    C* tb = (C*)F.tbuf;
+    int rc;
+    // 2. axis 1 forward, natural -> tiled: each CTA reads 4-column segments of
+    //    one plane and writes one contiguous (n1, tw) block
+    RegCall c{};
+    c.kind = 0;
+    c.in = cbuf;
+    c.out = tb;
+    c.S_in = nh;
+    c.bstride_in = (long long)n1 * nh;
+    c.cbs_in = tw;
+    c.S = tw;
+    c.bstride = (long long)n1 * tw;
+    c.cbs_out = F.tks;
+    c.ncol = nh;
+    c.nbatch = n0;
+    c.twL = F.tw_ax[1];
+    if ((rc = reg_run<T>(SFB_REG(F, 1), c, st))) return rc;
+    // 3. axis 0 forward + scale + inverse in place on the tiled copy
+    ScaleArgs sc = F.sc;
+    sc.tlog = F.tlog;
+    if ((rc = launch_strided<T, 2>(tb, F.ax[0], 0, (long long)n1 * tw, n1 * tw, F.tks, nblk, (const C*)F.tw_ax[0],
+                                   sc, st, nullptr, SFB_REG(F, 0))))
+      return rc;
+    // 4. axis 1 inverse, tiled -> natural
+    c.kind = 1;
+    c.in = tb;
+    c.out = cbuf;
+    c.S_in = tw;
+    c.bstride_in = (long long)n1 * tw;
+    c.cbs_in = F.tks;
+    c.S = nh;
+    c.bstride = (long long)n1 * nh;
+    c.cbs_out = tw;
+    if ((rc = reg_run<T>(SFB_REG(F, 1), c, st))) return rc;
+    return launch_c2r<T>(F, cbuf, rbuf, rows, st);
+  }
   if (tiled) {
     const int n0 = F.n[0], n1 = F.n[1], tw = 1 << F.tlog, nblk = (nh + tw - 1) / tw;
     int rc;

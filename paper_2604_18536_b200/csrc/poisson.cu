@@ -575,6 +575,16 @@ static int setup_fft(sfb_solver* s) {
     if ((1 << lg) == tw && (tw == 4 || tw == 8) && tw <= tt && tw % w1 == 0) {
       F.tlog = lg;
       F.tks = (long long)p->n[0] * p->n[1] * tw;
+      // hybrid (default, axis-1 kernel width only): a separate tiled copy;
+      // SFB_FFT_TILED_ROWS=1 tiles the row passes' spectrum too (measured
+      // slower: the row kernels lose more than the copy costs)
+      if (tw == w1 && !getenv("SFB_FFT_TILED_ROWS")) {
+        const long long nblk = (p->n[2] / 2 + 1 + tw - 1) / tw;
+        const size_t bytes = (f64 ? 16 : 8) * (size_t)nblk * F.tks;
+        if ((rc = cuda_check(cudaMalloc(&s->tbuf, bytes), "cudaMalloc(tiled spectrum)"))) return rc;
+        if ((rc = cuda_check(cudaMemset(s->tbuf, 0, bytes), "cudaMemset(tiled spectrum)"))) return rc;
+        F.tbuf = s->tbuf;
+      }
     }
   }
   if (dim == 3 && !getenv("SFB_NO_TMA") && !F.tlog) {

@@ -52,6 +52,10 @@ struct FftSolve {
   // blocks of 2^tlog columns, block stride tks; 0 = natural layout
   int tlog = 0;
   long long tks = 0;
+  // hybrid layout (default): the row passes keep the natural spectrum, the
+  // axis-1 passes copy it to / from this tiled buffer, the axis-0 pass runs
+  // on it in place (solver-owned; null = all passes on the tiled cbuf)
+  void* tbuf = nullptr;
 };
 
 bool fft_factor(int L, FftLen& P);

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
                                   MODE == 2 ? RegGeo<typename CX<T>::t, A, B>::MINB_S2 : RegGeo<typename CX<T>::t, A, B>::MINB_S)
     k_rfft_strided(const typename CX<T>::t* __restrict__ in, typename CX<T>::t* __restrict__ data, long long S,
                    int ncol, long long bin, long long bstride, RowSplit mp, const typename CX<T>::t* __restrict__ twL,
-                   ScaleArgs sc, int swap) {
+                   ScaleArgs sc, int swap, long long S_in, long long cbs_in, long long cbs_out) {
   typedef typename CX<T>::t C;
   typedef RegGeo<C, A, B> RG;
   constexpr int W = RG::W, XS = RG::XS;
@@ -249,8 +249,10 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
   const int cblk = swap ? blockIdx.y : blockIdx.x, bat = swap ? blockIdx.x : blockIdx.y;
   const int col = cblk * W + w;
   const bool ok = col < ncol;
-  C* base = data + (long long)bat * bstride + (ok ? col : 0);
-  const C* ibase = in + (long long)bat * bin + (ok ? col : 0);
+  // column block cblk at cblk * cbs (natural layout: cbs = W, i.e. column
+  // col; tiled spectrum: the block stride); input rows S_in apart, output S
+  C* base = data + (long long)bat * bstride + (ok ? cblk * cbs_out + w : 0);
+  const C* ibase = in + (long long)bat * bin + (ok ? cblk * cbs_in + w : 0);
   constexpr bool INV1 = MODE == 1 || MODE == 4;
   const long long gs = (long long)B * S;
   auto mapped = [&](int r) -> long long { return (long long)(r / mp.c) * mp.sq + (long long)(r % mp.c) * mp.s; };
@@ -261,9 +263,10 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_S,
 #pragma unroll
       for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(ibase + mapped(B * n1 + t)) : czero<C>();
     } else {
-      const C* g = ibase + (long long)t * S;
+      const C* g = ibase + (long long)t * S_in;
+      const long long gsi = (long long)B * S_in;
 #pragma unroll
-      for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(g + n1 * gs) : czero<C>();
+      for (int n1 = 0; n1 < A; ++n1) v[n1] = ok ? __ldcs(g + n1 * gsi) : czero<C>();
     }
   }
   tw_fill(twlo, twhi, twL, A * B);
@@ -648,6 +651,7 @@ struct RegCall {
   const void* twL;  // plain table exp(-2 pi i m / L), m < L
   const void* twN;  // real trick: exp(-2 pi i k / 2L), k <= L
   ScaleArgs sc;
+  long long S_in, cbs_in, cbs_out;  // strided kinds: input row stride, column-block strides (0 = natural)
   const void* geo;     // kind 5: host Geo<T> of the velocity plan
   const void* u[3];    // kind 5: extended velocity components
   int tlog;            // kinds 3-5: tiled spectrum (r2c_epilogue), 0 = natural
@@ -695,10 +699,11 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     const C* src = c.in ? (const C*)c.in : d;
     const long long bin = c.in ? c.bstride_in : c.bstride;
     const RowSplit mp{c.map_c > 0 ? c.map_c : 1, c.map_sq, c.map_s};
+    const long long sin = c.S_in ? c.S_in : c.S, cbi = c.cbs_in ? c.cbs_in : RG::W, cbo = c.cbs_out ? c.cbs_out : RG::W;
     const C* tw = (const C*)c.twL;
 #define SFB_STRIDED(M)                                                                                     \
   k_rfft_strided<T, A, B, M><<<grid, RG::NT_S, M == 2 ? RG::SMEM_S2 : RG::SMEM_S, st>>>(src, d, c.S, c.ncol, bin, c.bstride, mp, tw, \
-                                                                 c.sc, swap)
+                                                                 c.sc, swap, sin, cbi, cbo)
     switch (c.kind) {
       case 0: SFB_STRIDED(0); break;
       case 1: SFB_STRIDED(1); break;
