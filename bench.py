@@ -258,7 +258,7 @@ def run_ours(args):
 
         ic = "isotropic random-phase IC"
     else:
-        from paper_2604_18536_b200.distributed import Comm, CudaSlabBackend, SlabGrid, SlabLayout, SlabSimulation
+        from paper_2604_18536_b200.distributed import CudaSlabBackend, SlabGrid, SlabLayout, SlabSimulation, make_comm
 
         gshape = WEAK_LADDER.get(world) if args.n == 840 else (args.n * world, args.n, args.n)
         if gshape is None:
@@ -268,7 +268,7 @@ def run_ours(args):
         lay = SlabLayout(gshape[0], rank, world)
         sg = SlabGrid(gg, lay)
         be = CudaSlabBackend(sg, 1 / 1600, None)
-        sim = SlabSimulation(be, Comm(lay, group=dist.group.WORLD if world > 1 else None))
+        sim = SlabSimulation(be, make_comm(lay, group=dist.group.WORLD if world > 1 else None))
         st = sim.new_state(_slab_tgv(sg, P))
         sim.proj.project(st.u)
         local_cells = lay.m * gshape[1] * gshape[2]
@@ -358,6 +358,12 @@ def run_ours(args):
     e2e_ms = float(t.item())
     field_bytes = int(np.prod(ext)) * np.dtype(dtype).itemsize
     ke_after = ke()
+    # device memory in use per rank (cudaMemGetInfo), max over ranks
+    free_b, total_b = torch.cuda.mem_get_info()
+    mem = torch.tensor([float(total_b - free_b)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(mem, op=dist.ReduceOp.MAX)
+    hbm_used_gb = float(mem.item()) / 1e9
 
     if rank == 0:
         peak, peak_kind = _peaks()
@@ -382,7 +388,8 @@ def run_ours(args):
             "config": {"workload": wl, "grid": list(gshape), "method": "rk4", "solver": "spectral",
                        "nu": 1 / 1600, "dt": dt,
                        "l2": "inputs larger than L2 (each field >= 4.7 GB at 840^3 per GPU); no flush needed",
-                       "parallelism": f"z-slab x{world}" if slab else "single GPU"},
+                       "parallelism": f"z-slab x{world}" if slab else "single GPU",
+                       **({"comm": type(sim.comm).__name__} if slab else {})},
             "e2e": {"value": total_cells / (e2e_ms * 1e-3), "unit": "cell-updates/s",
                     "h2d_bytes_per_step": 3 * field_bytes * world, "d2h_bytes_per_step": 3 * field_bytes * world,
                     "steps": e2e_steps,
@@ -397,6 +404,7 @@ def run_ours(args):
             "step_roofline": {"algorithmic_bytes_per_cell": bpc, "achieved": step_gbs, "peak": peak,
                               "frac": step_gbs / peak},
             "gpu_launches": launches,
+            "hbm_gb": {"used_max_over_ranks": hbm_used_gb, "total_per_gpu": total_b / 1e9},
             "clocks": clocks.summary(),
             "ke_after": ke_after,
         }

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SFB_ABI_VERSION 4
+#define SFB_ABI_VERSION 5
 
 enum { SFB_OK = 0, SFB_EINVAL = 1, SFB_ECONFIG = 2, SFB_ENUMERIC = 3, SFB_ECUDA = 4, SFB_ECONVERGE = 5 };
 enum { SFB_F64 = 0, SFB_F32 = 1 };
@@ -220,6 +220,30 @@ int sfb_slab_axis1(sfb_solver* s, int chunk, int nchunks, int inverse, void* str
 int sfb_slab_axis0(sfb_solver* s, int chunk, int nchunks, void* stream);
 int sfb_slab_c2r(sfb_solver* s, void* stream);
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream);
+
+/* NCCL communicator of the slab decomposition (SURVEY 8(b) comm_create,
+ * 8(e)).  No reference counterpart (the reference is single-process; the
+ * paper's outlook).  Rank 0 calls sfb_comm_unique_id and
+ * the caller broadcasts the 128 id bytes; every rank then calls
+ * sfb_comm_create on its device.  NCCL is dlopen'ed (libnccl.so.2, the copy
+ * already loaded by the process).  All operations are enqueued on `stream`
+ * (no host synchronisation); with one rank they are device copies. */
+typedef struct sfb_comm sfb_comm;
+int sfb_comm_unique_id(void* id128);
+int sfb_comm_create(const void* id128, int nranks, int rank, sfb_comm** out);
+int sfb_comm_destroy(sfb_comm* c);
+int sfb_comm_rank(const sfb_comm* c);
+/* send `bytes` to peer_send and receive `bytes` from peer_recv (one group;
+ * a null buffer skips that side) */
+int sfb_comm_sendrecv(sfb_comm* c, const void* send, int peer_send, void* recv, int peer_recv, size_t bytes,
+                      void* stream);
+/* axis-0 ghost planes of nf extended slab fields with m local planes:
+ * plane 0 <- prev's plane m, plane m+1 <- next's plane 1 */
+int sfb_comm_halo(sfb_comm* c, void* const* fields, int nf, size_t plane_bytes, int m, void* stream);
+/* equal-split all-to-all (block q of send to rank q) */
+int sfb_comm_alltoall(sfb_comm* c, const void* send, void* recv, size_t bytes_per_peer, void* stream);
+/* in-place device all-reduce of fp64 values: op 0 sum, 1 min, 2 max */
+int sfb_comm_allreduce_f64(sfb_comm* c, double* buf, size_t count, int op, void* stream);
 
 /* Adjoints of the ghost fills (adjoint.py:53-111): accumulate every ghost
  * entry onto its source and zero the ghosts, axes in reverse order, for the

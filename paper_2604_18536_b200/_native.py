@@ -18,7 +18,7 @@ SFB_F64, SFB_F32 = 0, 1
 SFB_BC_PERIODIC, SFB_BC_DIRICHLET, SFB_BC_SYMMETRIC, SFB_BC_HALO = 0, 1, 2, 3
 SFB_SOLVER_SPECTRAL, SFB_SOLVER_CHANNEL, SFB_SOLVER_CG = 0, 1, 2
 SFB_NTAB = 10
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 vp = ctypes.c_void_p
 VP3 = vp * 3
@@ -99,6 +99,14 @@ _SIGS = {
     "sfb_slab_axis0": [vp, ctypes.c_int, ctypes.c_int, vp],
     "sfb_slab_c2r": [vp, vp],
     "sfb_slab_correct": [vp, VP3, vp, vp],
+    "sfb_comm_unique_id": [vp],
+    "sfb_comm_create": [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
+    "sfb_comm_destroy": [vp],
+    "sfb_comm_rank": [vp],
+    "sfb_comm_sendrecv": [vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_size_t, vp],
+    "sfb_comm_halo": [vp, VP3, ctypes.c_int, ctypes.c_size_t, ctypes.c_int, vp],
+    "sfb_comm_alltoall": [vp, vp, vp, ctypes.c_size_t, vp],
+    "sfb_comm_allreduce_f64": [vp, vp, ctypes.c_size_t, ctypes.c_int, vp],
     "sfb_fold_ghosts_velocity": [vp, VP3, vp],
     "sfb_fold_ghosts_scalar": [vp, vp, vp],
     "sfb_zero_non_dofs_velocity": [vp, VP3, vp],

@@ -38,11 +38,14 @@ def build(force=False, verbose=False, jobs=None):
     objs = []
     procs = []
     os.makedirs(os.path.join(CSRC, "build"), exist_ok=True)
+    # nccl.h of the NCCL PyTorch loads (comm.cu dlopens libnccl.so.2 at run time)
+    nccl_inc = [f for d in glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia", "nccl",
+                                                  "include")) for f in ("-I", d)][:2]
     for src in sources():
         obj = os.path.join(CSRC, "build", os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         extra = os.environ.get("SFB_NVCC_FLAGS", "").split()
-        cmd = [nvcc, *ARCH, *FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", obj]
+        cmd = [nvcc, *ARCH, *FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"), *nccl_inc, "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -58,7 +61,7 @@ def build(force=False, verbose=False, jobs=None):
         raise RuntimeError(f"nvcc failed:\n{msg}")
     torch_cufft = glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia", "cufft", "lib"))
     rpaths = [os.path.join(CUDA, "lib64")] + torch_cufft
-    link = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-L", os.path.join(CUDA, "lib64"), "-lcufft"]
+    link = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-L", os.path.join(CUDA, "lib64"), "-lcufft", "-ldl"]
     for r in rpaths:
         link += ["-Xlinker", "-rpath=" + r]
     subprocess.run(link, check=True)

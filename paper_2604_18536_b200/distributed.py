@@ -164,6 +164,115 @@ class Comm:
         return float(t.item())
 
 
+class _Event:
+    """Handle of an exchange enqueued on the communicator's stream: wait()
+    orders the caller's current stream after it."""
+
+    def __init__(self, ev):
+        self.ev = ev
+
+    def wait(self):
+        torch.cuda.current_stream().wait_event(self.ev)
+        return True
+
+
+class NcclComm:
+    """The same operations as ``Comm`` through the library's own NCCL
+    communicator (``sfb_comm_*`` in the C ABI): the halo planes of all
+    fields in one NCCL group on the compute stream, the transposes'
+    all-to-alls on a dedicated stream (ordered by CUDA events, so they
+    overlap the next chunk's kernels), device-side fp64 all-reduces.  The
+    128-byte NCCL id is broadcast over ``group`` (any torch.distributed
+    backend); with one rank everything is a device copy."""
+
+    def __init__(self, layout, group=None):
+        import os
+
+        # NCCL prints its version banner to stdout at the first init unless
+        # told otherwise; keep stdout for the caller (bench.py's JSON line)
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
+        self.layout = layout
+        id_buf = (ctypes.c_ubyte * 128)()
+        if layout.rank == 0:
+            N.call("sfb_comm_unique_id", ctypes.cast(id_buf, ctypes.c_void_p))
+        if layout.size > 1:
+            t = torch.tensor(list(id_buf), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=0, group=group)
+            for i, b in enumerate(t.cpu().tolist()):
+                id_buf[i] = b
+        h = ctypes.c_void_p()
+        N.call("sfb_comm_create", ctypes.cast(id_buf, ctypes.c_void_p), layout.size, layout.rank, ctypes.byref(h))
+        self.handle = h
+        self.stream = torch.cuda.Stream()
+        self._red = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                N.lib.sfb_comm_destroy(h)
+            except Exception:  # pragma: no cover
+                pass
+
+    @staticmethod
+    def _sp(stream=None):
+        return ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+
+    def halo(self, tensors):
+        m = self.layout.m
+        t0 = tensors[0]
+        ptrs = (ctypes.c_void_p * 3)(*[t.data_ptr() for t in tensors] + [None] * (3 - len(tensors)))
+        N.call("sfb_comm_halo", self.handle, ptrs, len(tensors), t0[0].numel() * t0.element_size(), m, self._sp())
+
+    def _sendrecv(self, send, dst, recv, src):
+        N.call("sfb_comm_sendrecv", self.handle, send.data_ptr(), dst, recv.data_ptr(), src,
+               send.numel() * send.element_size(), self._sp())
+
+    def plane_from_next(self, send_plane, recv_plane):
+        lay = self.layout
+        self._sendrecv(send_plane, lay.prev, recv_plane, lay.next)
+
+    def plane_from_prev(self, send_plane, recv_plane):
+        lay = self.layout
+        self._sendrecv(send_plane, lay.next, recv_plane, lay.prev)
+
+    def all_to_all(self, out, inp):
+        self.all_to_all_async(out, inp).wait()
+
+    def all_to_all_async(self, out, inp):
+        cur = torch.cuda.current_stream()
+        self.stream.wait_stream(cur)
+        N.call("sfb_comm_alltoall", self.handle, inp.data_ptr(), out.data_ptr(),
+               inp.numel() * inp.element_size() // self.layout.size, self._sp(self.stream))
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        return _Event(ev)
+
+    def allreduce_device(self, t, op="sum"):
+        """In-place all-reduce of an fp64 CUDA tensor, no host round trip."""
+        N.call("sfb_comm_allreduce_f64", self.handle, t.data_ptr(), t.numel(), {"sum": 0, "min": 1, "max": 2}[op],
+               self._sp())
+        return t
+
+    def allreduce(self, value, op="sum"):
+        if self.layout.size == 1:
+            return value
+        self._red.fill_(value)
+        return float(self.allreduce_device(self._red, op).item())
+
+
+def make_comm(layout, group=None):
+    """The slab communicator of a CUDA run: the library's NCCL communicator
+    (``SFB_COMM=torch`` keeps torch.distributed's)."""
+    import os
+
+    if os.environ.get("SFB_COMM", "nccl") == "torch":
+        return Comm(layout, group=group)
+    return NcclComm(layout, group=group)
+
+
 # ---------------------------------------------------------------------------
 # CUDA backend (C ABI)
 # ---------------------------------------------------------------------------
