@@ -94,6 +94,10 @@ typedef struct sfb_stage_args {
    * kernel takes the projected u0 from shared memory for the combines and
    * writes it here once (timestep.py:208-210 fused into the next stage 0). */
   void* u0_out[3];
+  /* Optional (NULL = off): per-DOF closure term of the stage state (the
+   * eddy-stress divergence, les.py:343-414, from sfb_eddy_stress_divergence),
+   * added after the force (operators.py:236-237); extended arrays. */
+  const void* closure_term[3];
 } sfb_stage_args;
 
 int sfb_abi_version(void);
@@ -220,6 +224,14 @@ int sfb_slab_axis1(sfb_solver* s, int chunk, int nchunks, int inverse, void* str
 int sfb_slab_axis0(sfb_solver* s, int chunk, int nchunks, void* stream);
 int sfb_slab_c2r(sfb_solver* s, void* stream);
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream);
+
+/* Pullback of the Smagorinsky closure term (les.py:343-414 with
+ * les.py:90-100's nu_t) on a periodic 3D grid: out += (dE/du)^T vbar, through
+ * the resolved gradients and through nu_t.  u, nut and vbar need filled
+ * (periodic) ghosts; scratch holds 16 extended scalars.  No reference
+ * counterpart: its tape leaves closures out (adjoint.py:374); SURVEY 8(f2). */
+int sfb_closure_pullback(sfb_plan* plan, int kind, double c, const void* const* u, const void* nut,
+                         const void* const* vbar, void* const* out, void* scratch, void* stream);
 
 /* NCCL communicator of the slab decomposition (SURVEY 8(b) comm_create,
  * 8(e)).  No reference counterpart (the reference is single-process; the

@@ -294,3 +294,93 @@ def eddy_stress_divergence(g, u, nut, out=None):
                 lo[b] = slice(0, -1)
                 out[a][sl] += (flux[tuple(hi)] - flux[tuple(lo)]) / g.col(g.dx[b], b, sl[b])
     return out
+
+
+# ---------------------------------------------------------------------------
+# Adjoint of the Smagorinsky closure term (no reference counterpart: the
+# reference's tape leaves closures out, adjoint.py:374).  Checker for
+# csrc/les.cu k_cpb1-3; pinned by the FD identity in
+# tests/test_oracle_les_adjoint.py (the reference's checks.py:72-126 protocol).
+# ---------------------------------------------------------------------------
+def smagorinsky_pullback(g, u, vbar, c=None, scratch_out=None):
+    """(dE/du)^T vbar for E(u) = eddy_stress_divergence(u, nu_t(u, smagorinsky))
+    on a periodic 3D grid, through the resolved gradients and through nu_t;
+    interior result on velocity-shaped extended arrays (ghosts zero)."""
+    from .stagflow_np import fill_velocity, periodic_bcs
+
+    c = float(MODEL_CONSTANTS["smagorinsky"] if c is None else c)
+    assert g.dim == 3 and all(g.periodic)
+    bcs = periodic_bcs(3)
+    u = [x.copy() for x in u]
+    fill_velocity(g, bcs, u)
+    eb = [x.copy() for x in vbar]
+    fill_velocity(g, bcs, eb)
+    nut = np.zeros(g.ext_shape, dtype=g.dtype)
+    nut[g.pdof()] = nu_t(g, u, "smagorinsky", c=c)
+    fill_like_pressure(g, nut)
+    shape = g.shape
+    sl = tuple(slice(1, n + 1) for n in shape)
+    idx = [np.arange(1, n + 1) for n in shape]
+
+    def sh(*offs):  # interior slice shifted by (axis, offset) pairs
+        s = list(sl)
+        for a, o in zip(offs[::2], offs[1::2]):
+            s[a] = slice(1 + o, shape[a] + 1 + o)
+        return tuple(s)
+
+    def tab(table, a, i):
+        r = [1, 1, 1]
+        r[a] = -1
+        return (1.0 / table[a][i]).reshape(r)
+
+    pairs = [(0, 1), (0, 2), (1, 2)]
+    scr = np.zeros((16,) + g.ext_shape, dtype=g.dtype)
+    nud = 0.0
+    for a in range(3):
+        # centre fluxes 2 nu_t A_aa: cotangent Fbar, then gbar = 2 nu Fbar
+        fb = eb[a][sh(a, -1)] * tab(g.du, a, idx[a] - 1) - eb[a][sl] * tab(g.du, a, idx[a])
+        ga = (u[a][sl] - u[a][sh(a, -1)]) * tab(g.dx, a, idx[a])
+        scr[a][sl] = 2.0 * nut[sl] * fb
+        nud = nud + 2.0 * ga * fb
+    scr[6][sl] = nud
+    for p, (a, b) in enumerate(pairs):
+        # corner fluxes 2 nu_t S_ab (shared by E_a along b and E_b along a)
+        fcb = (eb[a][sl] * tab(g.dx, b, idx[b]) - eb[a][sh(b, 1)] * tab(g.dx, b, idx[b] + 1)) + (
+            eb[b][sl] * tab(g.dx, a, idx[a]) - eb[b][sh(a, 1)] * tab(g.dx, a, idx[a] + 1))
+        sab = (u[a][sh(b, 1)] - u[a][sl]) * tab(g.du, b, idx[b]) + (u[b][sh(a, 1)] - u[b][sl]) * tab(g.du, a, idx[a])
+        nc = 0.25 * ((nut[sl] + nut[sh(a, 1)]) + (nut[sh(b, 1)] + nut[sh(a, 1, b, 1)]))
+        scr[3 + p][sl] = fcb * nc
+        scr[7 + p][sl] = fcb * sab
+    for f in range(10):
+        fill_like_pressure(g, scr[f])
+    nub = scr[6][sl].copy()
+    for p, (a, b) in enumerate(pairs):
+        w = scr[7 + p]
+        nub += 0.25 * ((w[sl] + w[sh(a, -1)]) + (w[sh(b, -1)] + w[sh(a, -1, b, -1)]))
+    A = gradient_tensor(g, u)
+    S = 0.5 * (A + np.swapaxes(A, -1, -2))
+    mag = np.sqrt(np.maximum(2.0 * np.einsum("...ij,...ij->...", S, S), 0.0))
+    cd2 = (c * filter_width(g)) ** 2
+    f = np.where(mag > 0, nub * cd2 * 2.0 / np.where(mag > 0, mag, 1.0), 0.0)
+    for k, (i, j) in enumerate([(0, 0), (1, 1), (2, 2), (0, 1), (0, 2), (1, 2)]):
+        scr[10 + k][sl] = f * S[..., i, j]
+    for k in range(10, 16):
+        fill_like_pressure(g, scr[k])
+    out = g.zeros_vel()
+    for i in range(3):
+        v = (scr[i][sl] + scr[10 + i][sl]) * tab(g.dx, i, idx[i]) - (
+            scr[i][sh(i, 1)] + scr[10 + i][sh(i, 1)]) * tab(g.dx, i, idx[i] + 1)
+        for o in range(3):
+            if o == i:
+                continue
+            pr = min(i, o) + max(i, o) - 1
+            sb = scr[3 + pr]
+            v = v + sb[sh(o, -1)] * tab(g.du, o, idx[o] - 1) - sb[sl] * tab(g.du, o, idx[o])
+            ab = scr[13 + pr]
+            lo = (ab[sl] + ab[sh(i, 1)]) + (ab[sh(o, -1)] + ab[sh(i, 1, o, -1)])
+            hi = (ab[sl] + ab[sh(i, 1)]) + (ab[sh(o, 1)] + ab[sh(i, 1, o, 1)])
+            v = v + 0.25 * (lo * tab(g.du, o, idx[o] - 1) - hi * tab(g.du, o, idx[o]))
+        out[i][sl] = v
+    if scratch_out is not None:
+        scratch_out.append(scr)
+    return out

@@ -53,6 +53,7 @@ class StageArgs(ctypes.Structure):
         ("p_int", vp),
         ("force_field", VP3),
         ("u0_out", VP3),
+        ("closure_term", VP3),
     ]
 
 
@@ -77,6 +78,7 @@ _SIGS = {
     "sfb_solver_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
     "sfb_closure_nut": [vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, VP3, vp, vp],
     "sfb_eddy_stress_divergence": [vp, VP3, vp, VP3, ctypes.c_int, vp],
+    "sfb_closure_pullback": [vp, ctypes.c_int, ctypes.c_double, VP3, vp, VP3, VP3, vp, vp],
     "sfb_scalar_minmax": [vp, vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), vp],
     "sfb_plane_sums": [vp, ctypes.c_int, VP3, ctypes.c_int, vp, vp],
     "sfb_sub_plane_mean": [vp, ctypes.c_int, VP3, vp, vp],

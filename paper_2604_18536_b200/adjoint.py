@@ -196,11 +196,22 @@ def _axpy_into(grid, dst, src, coef):
     N.call("sfb_combine", _plan(grid), N.ptr3(dst.u), N.ptr3(dst.u), 1, karr, carr, stream_ptr())
 
 
-def step_forward_tape(u0, dt, tableau, solver, setup):
+class _ClosureScratch:
+    closure_term = None
+    nut = None
+
+
+def step_forward_tape(u0, dt, tableau, solver, setup, include_closure=False):
     """adjoint.py:352-384: one projected RK step recording the stage states.
-    Uses the same stage kernels as rk_step."""
-    from .timestep import _combine, _stage
+    Uses the same stage kernels as rk_step.  ``include_closure``: the stage
+    RHS carries the setup's closure term like rk_step's (the reference's tape
+    omits closures, adjoint.py:374)."""
+    from .timestep import _closure_term, _combine, _stage
     from .poisson import project_into
+    from .les import active as active_closure
+
+    closure = setup.closure if include_closure and active_closure(setup.closure) else None
+    cs = _ClosureScratch()
 
     bcs = setup.bcs
     grid = u0.grid
@@ -220,14 +231,15 @@ def step_forward_tape(u0, dt, tableau, solver, setup):
             nxt = j + 1 < s
             yn = VelocityField(grid, empty=True) if nxt else None
             b = tableau.b[j]
+            ct = _closure_term(closure, cur, cs) if closure is not None else None
             _stage(setup, cur, u0=u0, s_in=acc if started else None, s_out=acc if b != 0.0 else None,
-                   y_next=yn, cb=dt * b, ca=dt * (tableau.a[j + 1][j] if nxt else 0.0))
+                   y_next=yn, cb=dt * b, ca=dt * (tableau.a[j + 1][j] if nxt else 0.0), closure_term=ct)
             started = started or b != 0.0
             if nxt:
                 _project_quiet(yn, solver, bcs)
                 cur = yn
         project_into(acc, solver, bcs)
-        return acc, (stages, dt, tableau)
+        return acc, (stages, dt, tableau, closure)
     ks = []
     for j in range(s):
         if j == 0:
@@ -239,13 +251,14 @@ def step_forward_tape(u0, dt, tableau, solver, setup):
             project_into(yj, solver, bcs)
         stages.append(yj)
         kj = VelocityField(grid, empty=True)
-        _stage(setup, yj, k_out=kj)
+        ct = _closure_term(closure, yj, cs) if closure is not None else None
+        _stage(setup, yj, k_out=kj, closure_term=ct)
         ks.append(kj)
     u1 = VelocityField(grid, empty=True)
     terms = [(ks[l], dt * tableau.b[l]) for l in range(s) if tableau.b[l] != 0.0]
     _combine(grid, u1, u0, [k for k, _ in terms], [c for _, c in terms])
     project_into(u1, solver, bcs)
-    return u1, (stages, dt, tableau)
+    return u1, (stages, dt, tableau, closure)
 
 
 def _combine_into(grid, dst, terms):
@@ -278,8 +291,17 @@ def step_backward(tape, ubar, solver, setup):
     kbar_j = dt*b_j*ybar + dt*a_{j+1,j}*ybar_{j+1} (one combine kernel, no
     zero-initialised accumulators), and ``g0 += ybar_j`` is fused into the
     projection pullback; the generic path follows the reference loop."""
-    stages, dt, tableau = tape
+    stages, dt, tableau = tape[:3]
+    closure = tape[3] if len(tape) > 3 else None
     bcs = setup.bcs
+
+    def _closure_pb(kb, j, out):
+        # the closure's share of the stage RHS pullback (out += dE/du^T kb)
+        if closure is not None:
+            from .les import closure_pullback
+
+            closure_pullback(closure, stages[j], kb, out=out, accumulate=True)
+
     grid = stages[0].grid
     s = tableau.stages
     ybar = project_pullback(ubar, solver, bcs)
@@ -301,8 +323,10 @@ def step_backward(tape, ubar, solver, setup):
             _combine_into(grid, kb, terms)
             if j == 0:
                 rhs_pullback(kb, stages[0], setup.nu, bcs, out=g0, accumulate=True)
+                _closure_pb(kb, 0, g0)
                 continue
             rhs_pullback(kb, stages[j], setup.nu, bcs, out=fb)
+            _closure_pb(kb, j, fb)
             yj = spare
             _project_pullback_into(fb, solver, bcs, out=yj, acc=g0)
             spare = ynext if ynext is not None else VelocityField(grid, empty=True)
@@ -318,6 +342,7 @@ def step_backward(tape, ubar, solver, setup):
         if kbars[j] is None:
             continue
         fb = rhs_pullback(kbars[j], stages[j], setup.nu, bcs)
+        _closure_pb(kbars[j], j, fb)
         if j == 0:
             _axpy_into(grid, g0, fb, 1.0)
             continue
@@ -332,15 +357,18 @@ def step_backward(tape, ubar, solver, setup):
     return g0
 
 
-def unrolled_gradient(loss, u0, n_steps, dt, setup):
-    """adjoint.py:425-444"""
+def unrolled_gradient(loss, u0, n_steps, dt, setup, include_closure=False):
+    """adjoint.py:425-444.  ``include_closure=True`` differentiates through
+    the setup's closure too (forward stages with the closure term, its
+    pullback in the reverse sweep: a-posteriori closure training); the
+    default follows the reference, whose tape omits closures."""
     _require_periodic(setup.bcs)
     tableau = setup.tableau
     solver = setup.solver
     u = u0.copy()
     tapes = []
     for _ in range(n_steps):
-        u, tape = step_forward_tape(u, dt, tableau, solver, setup)
+        u, tape = step_forward_tape(u, dt, tableau, solver, setup, include_closure=include_closure)
         tapes.append(tape)
     ubar = loss.gradient(u)
     for tape in reversed(tapes):

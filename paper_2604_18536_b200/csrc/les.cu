@@ -383,6 +383,165 @@ static int closure_nut_run(sfb_plan* p, int kind, double c, double pexp, const v
   return SFB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Pullback of the Smagorinsky closure term E(u) = div(2 nu_t(u) S(u)) on a
+// periodic 3D grid: out += (dE/du)^T Ebar, both through the resolved
+// gradients (nu_t fixed) and through nu_t = (c Delta)^2 |S|.  The reference's
+// tape leaves closures out (adjoint.py:374); this is the a-posteriori
+// training extension.  Three gather passes over intermediate
+// cell fields (periodic ghosts filled between them, so every stencil reach
+// is a plain +-1 read), no atomics: the result is deterministic.
+//   K1 (cell c): centre flux cotangents Fbar_a = Ebar_a[c-e_a]/du_a[c_a-1]
+//       - Ebar_a[c]/du_a[c_a] -> gbar_a = 2 nu Fbar_a, nud = sum 2 g_a Fbar_a;
+//       corner (a<b) cotangents Fcbar from E_a and E_b -> sbar = Fcbar nc,
+//       W = Fcbar sab (for the four nu_t of the corner average)
+//   K2 (cell c): nubar = nud + 1/4 sum_pairs W over the corners touching c;
+//       Abar_ij = nubar (c Delta)^2 2 S_ij / |S| (symmetric, 6 fields)
+//   K3 (velocity DOF J): the transposes of the centre / corner differences
+//       and of grad_tensor, gathered from gbar, sbar, Abar
+// scratch layout (extended scalars): 0-2 gbar, 3-5 sbar (pairs 01, 02, 12),
+// 6 nud, 7-9 W, 10-15 Abar (00, 11, 22, 01, 02, 12)
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int pair_a(int p) { return p < 2 ? 0 : 1; }  // pairs (0,1) (0,2) (1,2)
+__host__ __device__ constexpr int pair_b(int p) { return p == 0 ? 1 : 2; }
+__host__ __device__ constexpr int pair_of(int a, int b) { return a + b - 1; }  // (0,1)->0 (0,2)->1 (1,2)->2
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_cpb1(Geo<T> G, CV<T> U, const T* __restrict__ nut, CV<T> Eb,
+                                              T* __restrict__ scr, long long fs, Box B) {
+  int I[3];
+  if (!box_coords<3>(B, I)) return;
+  const long long x = lin<T, 3>(G, I);
+  T nud = T(0);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const long long sa = G.s[a];
+    const T fb = Eb.c[a][x - sa] * tab(G, a, T_RDU, I[a] - 1) - Eb.c[a][x] * tab(G, a, T_RDU, I[a]);
+    const T g = (U.c[a][x] - U.c[a][x - sa]) * tab(G, a, T_RDX, I[a]);
+    scr[a * fs + x] = T(2) * nut[x] * fb;
+    nud += T(2) * g * fb;
+  }
+  scr[6 * fs + x] = nud;
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const int a = pair_a(p), b = pair_b(p);
+    const long long sa = G.s[a], sb = G.s[b];
+    const T fcb = (Eb.c[a][x] * tab(G, b, T_RDX, I[b]) - Eb.c[a][x + sb] * tab(G, b, T_RDX, I[b] + 1)) +
+                  (Eb.c[b][x] * tab(G, a, T_RDX, I[a]) - Eb.c[b][x + sa] * tab(G, a, T_RDX, I[a] + 1));
+    const T sab = (U.c[a][x + sb] - U.c[a][x]) * tab(G, b, T_RDU, I[b]) +
+                  (U.c[b][x + sa] - U.c[b][x]) * tab(G, a, T_RDU, I[a]);
+    const T nc = T(0.25) * ((nut[x] + nut[x + sa]) + (nut[x + sb] + nut[x + sa + sb]));
+    scr[(3 + p) * fs + x] = fcb * nc;
+    scr[(7 + p) * fs + x] = fcb * sab;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_cpb2(Geo<T> G, CV<T> U, T c, T* __restrict__ scr, long long fs, Box B) {
+  int I[3];
+  if (!box_coords<3>(B, I)) return;
+  const long long x = lin<T, 3>(G, I);
+  T nub = scr[6 * fs + x];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const long long sa = G.s[pair_a(p)], sb = G.s[pair_b(p)];
+    const T* W = scr + (7 + p) * fs;
+    nub += T(0.25) * ((W[x] + W[x - sa]) + (W[x - sb] + W[x - sa - sb]));
+  }
+  T A[3][3];
+  grad_tensor<T, 3>(G, U, I, x, A);
+  T S[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) S[i][j] = T(0.5) * (A[i][j] + A[j][i]);
+  T q = T(0);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) q += S[i][j] * S[j][i];
+  const T mag = sqrt(fmax(T(2) * q, T(0)));  // |S| = sqrt(-4 qs), qs = -q/2 (k_nut)
+  T prod = T(1);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) prod = prod * tab(G, a, T_DX, I[a]);
+  const T delta = cbrt(prod);
+  const T cd2 = (c * delta) * (c * delta);
+  // d|S|/dA_ij = 2 S_ij / |S| (zero where |S| = 0: the subgradient the
+  // forward's max(., 0) takes)
+  const T f = mag > T(0) ? nub * cd2 * T(2) / mag : T(0);
+  scr[10 * fs + x] = f * S[0][0];
+  scr[11 * fs + x] = f * S[1][1];
+  scr[12 * fs + x] = f * S[2][2];
+  scr[13 * fs + x] = f * S[0][1];
+  scr[14 * fs + x] = f * S[0][2];
+  scr[15 * fs + x] = f * S[1][2];
+}
+
+template <typename T>
+__device__ __forceinline__ int abar_slot(int i, int j) {
+  return i == j ? 10 + i : 13 + pair_of(i < j ? i : j, i < j ? j : i);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_cpb3(Geo<T> G, const T* __restrict__ scr, long long fs, MV<T> out, Box B) {
+  int I[3];
+  if (!box_coords<3>(B, I)) return;
+  const long long x = lin<T, 3>(G, I);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const long long si = G.s[i];
+    // centre differences: eddy flux gradients and grad_tensor's diagonal
+    const T* gb = scr + i * fs;
+    const T* Ad = scr + (10 + i) * fs;
+    T v = (gb[x] + Ad[x]) * tab(G, i, T_RDX, I[i]) - (gb[x + si] + Ad[x + si]) * tab(G, i, T_RDX, I[i] + 1);
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (o == i) continue;
+      const long long so = G.s[o];
+      // corner strain 2 S_io of the eddy fluxes
+      const T* sb = scr + (3 + pair_of(i < o ? i : o, i < o ? o : i)) * fs;
+      v += sb[x - so] * tab(G, o, T_RDU, I[o] - 1) - sb[x] * tab(G, o, T_RDU, I[o]);
+      // grad_tensor's four-corner average of du_i / dx_o
+      const T* Ab = scr + abar_slot<T>(i, o) * fs;
+      const T lo = (Ab[x] + Ab[x + si]) + (Ab[x - so] + Ab[x + si - so]);
+      const T hi = (Ab[x] + Ab[x + si]) + (Ab[x + so] + Ab[x + si + so]);
+      v += T(0.25) * (lo * tab(G, o, T_RDU, I[o] - 1) - hi * tab(G, o, T_RDU, I[o]));
+    }
+    out.c[i][x] += v;
+  }
+}
+
+template <typename T>
+static int closure_pullback_run(sfb_plan* p, double c, const void* const* u, const void* nut, const void* const* vbar,
+                                void* const* out, void* scratch, cudaStream_t st) {
+  const Geo<T>& G = geo<T>(p);
+  CV<T> U, Eb;
+  MV<T> O;
+  for (int a = 0; a < 3; ++a) {
+    U.c[a] = (const T*)u[a];
+    Eb.c[a] = (const T*)vbar[a];
+    O.c[a] = (T*)out[a];
+  }
+  T* scr = (T*)scratch;
+  const long long fs = p->ext_count;
+  Box B = int_box(G);
+  k_cpb1<T><<<box_grid(3, B), box_block(3), 0, st>>>(G, U, (const T*)nut, Eb, scr, fs, B);
+  SFB_LAUNCH_CHECK("closure pullback 1");
+  for (int f = 0; f < 10; f += 3)
+    if (int rc = launch_planes<T>(G, MV<T>{{scr + f * fs, f + 1 < 10 ? scr + (f + 1) * fs : nullptr,
+                                              f + 2 < 10 ? scr + (f + 2) * fs : nullptr}},
+                                  f + 3 <= 10 ? 3 : 10 - f, 1, st))
+      return rc;
+  k_cpb2<T><<<box_grid(3, B), box_block(3), 0, st>>>(G, U, (T)c, scr, fs, B);
+  SFB_LAUNCH_CHECK("closure pullback 2");
+  for (int f = 10; f < 16; f += 3)
+    if (int rc = launch_planes<T>(G, MV<T>{{scr + f * fs, scr + (f + 1) * fs, scr + (f + 2) * fs}}, 3, 1, st))
+      return rc;
+  k_cpb3<T><<<box_grid(3, B), box_block(3), 0, st>>>(G, scr, fs, O, B);
+  SFB_LAUNCH_CHECK("closure pullback 3");
+  return SFB_OK;
+}
+
 }  // namespace sfb
 
 using namespace sfb;
@@ -421,6 +580,16 @@ int sfb_eddy_stress_divergence(sfb_plan* p, const void* const* u, const void* nu
     SFB_LAUNCH_CHECK("eddy stress divergence");
     return SFB_OK;
   }()));
+}
+
+int sfb_closure_pullback(sfb_plan* p, int kind, double c, const void* const* u, const void* nut,
+                         const void* const* vbar, void* const* out, void* scratch, void* stream) {
+  if (!p || !u || !nut || !vbar || !out || !scratch) return fail(SFB_EINVAL, "null argument");
+  if (kind != LES_SMAG) return fail(SFB_ECONFIG, "closure pullback: Smagorinsky only");
+  if (p->dim != 3 || !p->all_periodic) return fail(SFB_ECONFIG, "closure pullback: periodic 3D grids only");
+  for (int a = 0; a < 3; ++a)
+    if (!u[a] || !vbar[a] || !out[a]) return fail(SFB_EINVAL, "null velocity component");
+  return SFB_TYPED(p, closure_pullback_run<T>(p, c, u, nut, vbar, out, scratch, (cudaStream_t)stream));
 }
 
 int sfb_scalar_minmax(sfb_plan* p, const void* f, double* mn, double* mx, void* stream) {

@@ -22,6 +22,7 @@ template <typename T>
 struct Force {
   T f[3];
   const T* a[3];
+  const T* c[3];  // closure term (stage kernels): added after the force
 };
 template <typename T>
 struct KList {

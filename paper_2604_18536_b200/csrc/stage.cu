@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256) k_stage_generic(Geo<T> G, StageArgs<T> A,
     if (!is_udof<T, D>(G, I, a)) continue;
     T k = rhs_comp<T, D>(G, A.y, x, I, a, T(0), true, A.diff, A.nu, A.F.f[a]);
     if (A.F.a[a]) k += A.F.a[a][x];
+    if (A.F.c[a]) k += A.F.c[a][x];  // operators.py:236-237
     if (A.has_k) A.k_out.c[a][x] = k;
     if (A.has_s) {
       const T base = A.s_from_u0 ? A.u0.c[a][x] : A.s_in.c[a][x];
@@ -344,7 +345,16 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB)
         kv[2] = dof[r][2] ? rhs_ring<T, 2, TJ, TK>(P, C, A.diff, A.nu, A.F.f[2]) : T(0);
       }
       const long long x = x0 + r * rstep;
-      if (A.F.a[0]) {  // per-DOF force fields (sample_force of a callable)
+      if (A.F.c[0]) {  // closure term after the force (operators.py:236-237)
+        if (A.F.a[0]) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            if (dof[r][a]) kv[a] += A.F.a[a][x];
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (dof[r][a]) kv[a] += A.F.c[a][x];
+      } else if (A.F.a[0]) {  // per-DOF force fields (sample_force of a callable)
 #pragma unroll
         for (int a = 0; a < 3; ++a)
           if (dof[r][a]) kv[a] += A.F.a[a][x];
@@ -496,6 +506,7 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
     A.k_out.c[c] = on ? (T*)a->k_out[c] : nullptr;
     A.u0_out.c[c] = on ? (T*)a->u0_out[c] : nullptr;
     A.F.a[c] = on ? (const T*)a->force_field[c] : nullptr;
+    A.F.c[c] = on ? (const T*)a->closure_term[c] : nullptr;
     A.F.f[c] = (on && !A.F.a[c]) ? (T)a->force[c] : T(0);
   }
   A.cb = (T)a->cb;

@@ -485,6 +485,7 @@ static int do_rhs(sfb_plan* p, const void* const* u, void* const* out, double nu
   Force<T> F;
   for (int a = 0; a < 3; ++a) {
     F.a[a] = (field && a < p->dim) ? (const T*)field[a] : nullptr;
+    F.c[a] = nullptr;
     F.f[a] = (force && a < p->dim && !F.a[a]) ? (T)force[a] : T(0);
   }
   Box B = ext_box(G);

@@ -12,6 +12,7 @@ import ctypes
 import numpy as np
 
 from . import _native as N
+from .bcs import BoundarySpec
 from .errors import ConfigurationError
 from .fields import ScalarField, VelocityField
 from .operators import _plan
@@ -83,6 +84,21 @@ class ClosureModel:
                out.data.data_ptr(), stream_ptr())
         return out
 
+    def nu_t_into(self, u, out):
+        """nu_t into an existing scalar field (no allocation)."""
+        if self.filter_rule != "geometric":
+            raise ConfigurationError(f"unknown filter width rule: {self.filter_rule!r}")
+        N.call("sfb_closure_nut", _plan(u.grid), _KIND_CODE[self.kind], self.c, self.p, N.ptr3(u.u),
+               out.data.data_ptr(), stream_ptr())
+        return out
+
+    def rhs_into(self, u, out, nut):
+        """The closure's RHS term alone (out = div 2 nu_t S on the DOFs),
+        with nu_t in the caller's buffer: the fused stage adds it after the
+        force, like add_rhs does onto the assembled RHS."""
+        self.nu_t_into(u, nut)
+        _eddy(u, nut, out, accumulate=False)
+
     def add_rhs(self, u, out, scratch=None):
         if self.kind == "none":
             return
@@ -100,6 +116,35 @@ def _eddy(u, nut, out, accumulate):
     N.call("sfb_fill_ghosts_scalar", plan, nut.data.data_ptr(), stream_ptr())
     N.call("sfb_eddy_stress_divergence", plan, N.ptr3(u.u), nut.data.data_ptr(), N.ptr3(out.u),
            1 if accumulate else 0, stream_ptr())
+
+
+def closure_pullback(closure, u, vbar, out=None, accumulate=False):
+    """VJP of the closure's RHS term u -> div(2 nu_t(u) S(u)) at ``u``:
+    (dE/du)^T vbar, nu_t's dependence on u included (Smagorinsky; periodic
+    3D).  Fills the ghosts of ``u`` and ``vbar`` (periodic images).  The
+    reference has no closure adjoint (its tape omits closures,
+    adjoint.py:374); this is the training extension of SURVEY 8(f2)."""
+    import torch
+
+    from .fields import fill_ghosts_velocity
+
+    if closure.kind != "smagorinsky":
+        raise ConfigurationError("closure pullback: Smagorinsky only")
+    grid = u.grid
+    if out is None:
+        out = VelocityField(grid)
+    elif not accumulate:
+        for c in out.u:
+            c.zero_()
+    bcs = BoundarySpec.all_periodic(grid.dim)
+    fill_ghosts_velocity(u, bcs)
+    fill_ghosts_velocity(vbar, bcs)
+    nut = closure.nu_t_into(u, ScalarField(grid))
+    N.call("sfb_fill_ghosts_scalar", _plan(grid), nut.data.data_ptr(), stream_ptr())
+    scratch = torch.empty((16,) + tuple(u.u[0].shape), dtype=u.u[0].dtype, device=u.u[0].device)
+    N.call("sfb_closure_pullback", _plan(grid), _KIND_CODE[closure.kind], closure.c, N.ptr3(u.u),
+           nut.data.data_ptr(), N.ptr3(vbar.u), N.ptr3(out.u), scratch.data_ptr(), stream_ptr())
+    return out
 
 
 def scalar_max(f):
