@@ -33,6 +33,10 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# stdout carries exactly one JSON line: NCCL's banner / info lines (printed to
+# stdout when the environment sets NCCL_DEBUG=VERSION or INFO) go to stderr
+os.environ["NCCL_DEBUG"] = "WARN"
+os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
 sys.path.insert(0, ROOT)
 
 RK4_BYTES_PER_CELL_F64 = 864
