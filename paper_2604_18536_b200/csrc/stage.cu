@@ -393,7 +393,7 @@ constexpr int kTJ = SFB_STAGE_TJ, kTK = SFB_STAGE_TK, kCPT = SFB_STAGE_CPT;
 
 // TMA maps of the stage state y (fp64 only: a (TK+2)-wide fp32 box row is not
 // a multiple of 16 bytes); SM.ok = 0 keeps the cp.async fill
-template <typename T>
+template <typename T, int TJ>
 static void stage_maps(const Geo<T>& G, const StageArgs<T>& A, StageMaps& SM) {
   SM.ok = 0;
   static const bool off = env_int("SFB_STAGE_NOTMA") != 0;
@@ -404,7 +404,7 @@ static void stage_maps(const Geo<T>& G, const StageArgs<T>& A, StageMaps& SM) {
   if ((G.s[1] * esz) % 16 || (G.s[0] * esz) % 16) return;
   cuuint64_t dims[3] = {(cuuint64_t)G.E[2], (cuuint64_t)G.E[1], (cuuint64_t)G.E[0]};
   cuuint64_t strides[2] = {(cuuint64_t)(G.s[1] * esz), (cuuint64_t)(G.s[0] * esz)};
-  cuuint32_t box[3] = {(cuuint32_t)(kTK + 2), (cuuint32_t)(kTJ + 2), 1};
+  cuuint32_t box[3] = {(cuuint32_t)(kTK + 2), (cuuint32_t)(TJ + 2), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   for (int c = 0; c < 3; ++c) {
     if (!A.y.c[c] || ((uintptr_t)A.y.c[c] % 16)) return;
@@ -418,19 +418,24 @@ static void stage_maps(const Geo<T>& G, const StageArgs<T>& A, StageMaps& SM) {
 
 template <typename T, int FL>
 static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st) {
-  typedef RingGeom<kTJ, kTK> RG;
 #ifndef SFB_STAGE_MINB
 #define SFB_STAGE_MINB 3
 #endif
 #ifndef SFB_STAGE_MINB_PROJ
 #define SFB_STAGE_MINB_PROJ 3
 #endif
-  constexpr int MINB = (FL & FL_PROJ) ? SFB_STAGE_MINB_PROJ : SFB_STAGE_MINB;
-  const size_t smem = (size_t)kRing * 3 * RG::CS * sizeof(T) + kTJ * sizeof(Coef<T>) +
-                      ((FL & FL_PROJ) ? ((size_t)kPRing * (kTJ + 3) * (kTK + 3) + kTJ + kTK + 4) * sizeof(T) : 0);
-  if (cudaError_t e = ensure_smem((const void*)k_stage_march<T, kTJ, kTK, kCPT, FL, MINB>, smem))
+  // the deferred-projection stage 0 (FL_U0P: three field writes, no TMA) runs
+  // 4 x 32 tiles, one cell per thread, 4 CTAs per SM (840^3: 18.1 -> 17.4 ms;
+  // the other variants lost with that tile, profiles/r2/stage_tiles)
+  constexpr bool U0P = (FL & FL_U0P) != 0;
+  constexpr int TJ = U0P ? 4 : kTJ, CPT = U0P ? 1 : kCPT;
+  constexpr int MINB = U0P ? 4 : ((FL & FL_PROJ) ? SFB_STAGE_MINB_PROJ : SFB_STAGE_MINB);
+  typedef RingGeom<TJ, kTK> RG;
+  const size_t smem = (size_t)kRing * 3 * RG::CS * sizeof(T) + TJ * sizeof(Coef<T>) +
+                      ((FL & FL_PROJ) ? ((size_t)kPRing * (TJ + 3) * (kTK + 3) + TJ + kTK + 4) * sizeof(T) : 0);
+  if (cudaError_t e = ensure_smem((const void*)k_stage_march<T, TJ, kTK, CPT, FL, MINB>, smem))
     return cuda_check(e, "rk stage: shared-memory attribute");
-  const int bx = (G.n[2] + kTK - 1) / kTK, by = (G.n[1] + kTJ - 1) / kTJ;
+  const int bx = (G.n[2] + kTK - 1) / kTK, by = (G.n[1] + TJ - 1) / TJ;
   const long long bps = (long long)bx * by;
   // split the march into bz chunks so the launch is >= ~30 waves of resident
   // CTAs: with one chunk (840^3: 2835 CTAs = 6.4 waves of 444) the last
@@ -453,8 +458,8 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
   StageMaps SM;
   SM.ok = 0;
   static const bool tma_all = env_int("SFB_STAGE_TMA_ALL") != 0;
-  if (tma_all || ((FL & FL_PROJ) && !(FL & FL_SU0))) stage_maps<T>(G, A, SM);
-  k_stage_march<T, kTJ, kTK, kCPT, FL, MINB><<<dim3(bx, by, bz), dim3(kTK, kTJ / kCPT), smem, st>>>(G, A, chunk, SM);
+  if (tma_all || ((FL & FL_PROJ) && !(FL & FL_SU0))) stage_maps<T, TJ>(G, A, SM);
+  k_stage_march<T, TJ, kTK, CPT, FL, MINB><<<dim3(bx, by, bz), dim3(kTK, TJ / CPT), smem, st>>>(G, A, chunk, SM);
   SFB_LAUNCH_CHECK("rk stage (march)");
   return SFB_OK;
 }
