@@ -13,4 +13,9 @@ for path in sys.argv[1:]:
             p = ln.split()
             if len(p) >= 2:
                 d[p[0]] = p[1]
-        print(lines[0].strip()[-32:].ljust(34) + "".join(d.get(k, "-")[:9].rjust(10) for k in KEYS))
+        def fmt(v):
+            try:
+                return f"{float(v):.4g}"
+            except ValueError:
+                return v
+        print(lines[0].strip()[-32:].ljust(34) + "".join(fmt(d.get(k, "-")).rjust(10) for k in KEYS))
