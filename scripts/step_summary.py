@@ -1,7 +1,7 @@
 """Per-kernel summary of ONE RK4 step from an ncu launch list of
 `bench.py --steps 2 --warmup 1` (run_steps): the second timed step, which
 starts at the stage-0 launch that applies the previous step's deferred
-projection (k_stage_march with FL 126: PER|S|SU0|NEXT|PROJ|U0P) and ends
+projection (k_stage_march with FL_U0P, FL 120 / 126) and ends
 before the final gradient subtract of run_steps (or the next stage 0)."""
 import subprocess
 import sys
@@ -11,10 +11,18 @@ import parse_launches as PL  # noqa: E402
 
 k = PL.load(sys.argv[1])
 ids = [i for (i, name) in k]
-starts = [i for (i, name) in k if "k_stage_march" in name and ", 126," in name]
+
+
+def fl(name):
+    return int(name.split("k_stage_march<")[1].split(",")[4]) if "k_stage_march<" in name else -1
+
+
+# stage 0 of a step: applies the deferred projection (FL_U0P = 64) or runs on
+# a projected state (no FL_PROJ = 16)
+starts = [i for (i, name) in k if fl(name) >= 0 and fl(name) & 64]
 first = starts[0]
-after = [i for (i, name) in k if i > first and ("k_grad_sub" in name or ("k_stage_march" in name and
-                                                                          (", 46," in name or ", 126," in name)))]
+after = [i for (i, name) in k if i > first and ("k_grad_sub" in name or (fl(name) >= 0 and (fl(name) & 64 or
+                                                                                             not fl(name) & 16)))]
 last = max(i for i in ids if i < after[0])
 print(f"# one RK4 step (launch IDs {first}-{last} of {sys.argv[1]}); ncu --metrics "
       "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
