@@ -176,3 +176,21 @@ def test_solve_transpose_golden(P):
         solver = P.make_solver(str(cc["kind"]), pg, bcs)
         out = P.adjoint.poisson_solve_transpose(P.ScalarField(pg, cc["pbar"]), solver)
         assert rel(out.numpy(), cc["out"]) <= t, tag
+
+
+def test_config_build_setup_channel_rk4(P):
+    """a configuration with the B200 keys (run.device,
+    solver.kind = fft-tridiag, time.method = rk4) builds the channel setup on
+    the device (cli.py:76-110) and steps it."""
+    from paper_2604_18536_b200 import cases
+    from paper_2604_18536_b200.config import build_setup, parse_config
+
+    cfg = parse_config("[run]\nstudy = channel-smoke\ndevice = cuda:0\n[grid]\ndim = 3\nx_n = 16\ny_n = 24\n"
+                       "z_n = 8\ny_kind = tanh\ny_a = 0\ny_b = 2\ny_gamma = 2.0\n[bc]\ny = dirichlet\n"
+                       "[physics]\nnu = 0.0055\nforce = constant\n[solver]\nkind = fft-tridiag\n"
+                       "[time]\nmethod = rk4\ndt = 0.001\n")
+    setup = build_setup(cfg)
+    assert setup.solver.kind == "fft-tridiag" and setup.method == "rk4"
+    st = setup.new_state(u0=cases.channel_ic(setup.grid, 0.0055, seed=1))
+    P.rk_step(st, 1e-3, P.RK4, setup.solver, setup)
+    assert float(P.divergence(st.u).data.abs().max()) < 1e-10
