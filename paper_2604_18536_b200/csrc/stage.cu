@@ -450,15 +450,15 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
   int chunk = (int)((G.n[0] + want - 1) / want);
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;
-  // TMA fill for the stages whose running sum is carried in s (FL_PROJ
-  // without FL_SU0: stages 1-3).  Stage 0 (s formed from u0) measured slower
-  // with it (840^3: FL46 11.3 -> 13.0 ms, FL126 18.5 -> 20.9 ms; more DRAM
-  // re-reads and long-scoreboard stalls), stages 1-2 / 3 faster (17.8 -> 16.3,
-  // 13.8 -> 12.8 ms; profiles/r2/stage_tma)
+  // TMA fill for the on-the-fly-projection stages: stages 1-3 (17.8 -> 16.3,
+  // 13.8 -> 12.8 ms at 840^3) and the deferred stage 0 on its 4 x 32 tiles
+  // (17.4 -> 16.8 ms).  The plain stage 0 of a projected state (FL46) stays
+  // on cp.async: with TMA it re-read more DRAM and stalled longer on 8 x 32
+  // tiles (11.3 -> 13.0 ms; profiles/r2/stage_tma)
   StageMaps SM;
   SM.ok = 0;
   static const bool tma_all = env_int("SFB_STAGE_TMA_ALL") != 0;
-  if (tma_all || ((FL & FL_PROJ) && !(FL & FL_SU0))) stage_maps<T, TJ>(G, A, SM);
+  if (tma_all || ((FL & FL_PROJ) && (!(FL & FL_SU0) || (FL & FL_U0P)))) stage_maps<T, TJ>(G, A, SM);
   k_stage_march<T, TJ, kTK, CPT, FL, MINB><<<dim3(bx, by, bz), dim3(kTK, TJ / CPT), smem, st>>>(G, A, chunk, SM);
   SFB_LAUNCH_CHECK("rk stage (march)");
   return SFB_OK;
