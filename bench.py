@@ -369,6 +369,18 @@ def run_ours(args):
         dist.all_reduce(mem, op=dist.ReduceOp.MAX)
     hbm_used_gb = float(mem.item()) / 1e9
 
+    # other BASELINE configs, measured on the same box by the same run (rank 0
+    # at N=1): the 840^3 fields are released first
+    others = []
+    if world == 1 and not slab and not args.no_extras:
+        del u, host
+        state = setup = None  # noqa: F841 (release the 840^3 registers)
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        others = run_other_configs()
+
     if rank == 0:
         peak, peak_kind = _peaks()
         achieved = st_bytes / (st_ms * 1e-3) / 1e9
@@ -412,11 +424,36 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "ke_after": ke_after,
         }
+        if others:
+            line["other_configs"] = others
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_other_configs():
+    """BASELINE configs 3-4 next to the headline (bench_extra.py cases, CUDA
+    events, median of 5 after 2 warm-ups): 512^3 RK4 step fp64 and fp32, the
+    512^3 RK4 unrolled gradient (tape + reverse sweep), the Re_tau=180
+    channel 512x256x256 RK4 step.  A failing case reports its error."""
+    import gc
+
+    import torch
+
+    import bench_extra as BE
+
+    out = []
+    for name, fn in (("step512", lambda: BE.case_step(512, "f64")), ("step512f32", lambda: BE.case_step(512, "f32")),
+                     ("vjp512", lambda: BE.case_vjp(512)), ("channel", BE.case_channel)):
+        try:
+            out.append(fn())
+        except Exception as exc:  # noqa: BLE001 - reported, the headline line still prints
+            out.append({"case": name, "error": f"{type(exc).__name__}: {exc}"[:200]})
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -430,6 +467,7 @@ def main():
     ap.add_argument("--ref-n", type=int, default=96)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other BASELINE configs (other_configs)")
     ap.add_argument("--slab", action="store_true", help="use the z-slab path even at N=1")
     args = ap.parse_args()
     world = os.environ.get("WORLD_SIZE")
