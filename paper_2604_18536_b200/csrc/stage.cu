@@ -427,9 +427,18 @@ static int stage_march_launch(const Geo<T>& G, const StageArgs<T>& A, cudaStream
   // the deferred-projection stage 0 (FL_U0P: three field writes, no TMA) runs
   // 4 x 32 tiles, one cell per thread, 4 CTAs per SM (840^3: 18.1 -> 17.4 ms;
   // the other variants lost with that tile, profiles/r2/stage_tiles)
+#ifndef SFB_U0P_TJ
+#define SFB_U0P_TJ 4
+#endif
+#ifndef SFB_U0P_CPT
+#define SFB_U0P_CPT 1
+#endif
+#ifndef SFB_U0P_MINB
+#define SFB_U0P_MINB 4
+#endif
   constexpr bool U0P = (FL & FL_U0P) != 0;
-  constexpr int TJ = U0P ? 4 : kTJ, CPT = U0P ? 1 : kCPT;
-  constexpr int MINB = U0P ? 4 : ((FL & FL_PROJ) ? SFB_STAGE_MINB_PROJ : SFB_STAGE_MINB);
+  constexpr int TJ = U0P ? SFB_U0P_TJ : kTJ, CPT = U0P ? SFB_U0P_CPT : kCPT;
+  constexpr int MINB = U0P ? SFB_U0P_MINB : ((FL & FL_PROJ) ? SFB_STAGE_MINB_PROJ : SFB_STAGE_MINB);
   typedef RingGeom<TJ, kTK> RG;
   const size_t smem = (size_t)kRing * 3 * RG::CS * sizeof(T) + TJ * sizeof(Coef<T>) +
                       ((FL & FL_PROJ) ? ((size_t)kPRing * (TJ + 3) * (kTK + 3) + TJ + kTK + 4) * sizeof(T) : 0);
