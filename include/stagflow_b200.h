@@ -268,6 +268,12 @@ int sfb_zero_ghosts_scalar(sfb_plan* plan, void* f, void* stream);
 /* poisson_solve_transpose (adjoint.py:236-250): out = W S W^-1 pbar on the
  * interior of extended scalars (out's ghosts zeroed); any non-slab solver. */
 int sfb_solve_transpose(sfb_solver* s, const void* pbar, void* out, void* stream);
+/* project_pullback (adjoint.py:335-349) of the reverse sweep of a
+ * sub-diagonal tableau: r = P^T vbar is accumulated into acc (g0 += ybar_j)
+ * and only the next stage cotangent kb = c1 ybar + c2 r is stored
+ * (adjoint.py:400-419's combine fused); periodic grids. */
+int sfb_project_pullback_kb(sfb_solver* s, void* const* vbar, void* const* acc, const void* const* ybar, double c1,
+                            double c2, void* const* kb, void* stream);
 
 /* Pullbacks (adjoint.py:114-349), periodic grids. Mutating semantics of the
  * reference are kept: divergence_pullback zeroes pbar's ghosts;

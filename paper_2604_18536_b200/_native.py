@@ -121,6 +121,7 @@ _SIGS = {
     "sfb_rhs_pullback": [vp, VP3, VP3, ctypes.c_double, VP3, ctypes.c_double, ctypes.c_int, vp],
     "sfb_project_pullback": [vp, VP3, VP3, vp],
     "sfb_project_pullback_ex": [vp, VP3, ctypes.POINTER(VP3), ctypes.POINTER(VP3), vp],
+    "sfb_project_pullback_kb": [vp, VP3, VP3, VP3, ctypes.c_double, ctypes.c_double, VP3, vp],
     "sfb_fft_create": [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(vp)],
     "sfb_fft_destroy": [vp],
     "sfb_fft_uses_own": [vp],

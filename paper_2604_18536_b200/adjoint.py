@@ -310,26 +310,40 @@ def step_backward(tape, ubar, solver, setup):
         kb = VelocityField(grid, empty=True)
         fb = VelocityField(grid, empty=True)
         ynext = None
-        spare = VelocityField(grid, empty=True)
+        spare = None
+        kb_ready = False  # kb already holds stage j's cotangent (fused into the projection pullback)
         for j in reversed(range(s)):
-            terms = []
-            if tableau.b[j] != 0.0:
-                terms.append((ybar, dt * tableau.b[j]))
-            if ynext is not None and j + 1 < s and tableau.a[j + 1][j] != 0.0:
-                terms.append((ynext, dt * tableau.a[j + 1][j]))
-            if not terms:
-                ynext = None
-                continue
-            _combine_into(grid, kb, terms)
+            if not kb_ready:
+                terms = []
+                if tableau.b[j] != 0.0:
+                    terms.append((ybar, dt * tableau.b[j]))
+                if ynext is not None and j + 1 < s and tableau.a[j + 1][j] != 0.0:
+                    terms.append((ynext, dt * tableau.a[j + 1][j]))
+                if not terms:
+                    ynext = None
+                    continue
+                _combine_into(grid, kb, terms)
+            kb_ready = False
             if j == 0:
                 rhs_pullback(kb, stages[0], setup.nu, bcs, out=g0, accumulate=True)
                 _closure_pb(kb, 0, g0)
                 continue
             rhs_pullback(kb, stages[j], setup.nu, bcs, out=fb)
             _closure_pb(kb, j, fb)
-            yj = spare
+            c1, c2 = dt * tableau.b[j - 1], dt * tableau.a[j][j - 1]
+            if c1 != 0.0 and c2 != 0.0:
+                # ybar_j = P^T fb goes into g0 and straight into the next
+                # stage cotangent kb = c1 ybar + c2 ybar_j (one kernel, ybar_j
+                # never stored)
+                s_ = _native_solver(solver, bcs)
+                N.call("sfb_project_pullback_kb", s_.handle, N.ptr3(fb.u), N.ptr3(g0.u), N.ptr3(ybar.u), float(c1),
+                       float(c2), N.ptr3(kb.u), stream_ptr())
+                kb_ready = True
+                ynext = None
+                continue
+            yj = spare if spare is not None else VelocityField(grid, empty=True)
             _project_pullback_into(fb, solver, bcs, out=yj, acc=g0)
-            spare = ynext if ynext is not None else VelocityField(grid, empty=True)
+            spare = ynext
             ynext = yj
         return g0
     kbars = [None] * s

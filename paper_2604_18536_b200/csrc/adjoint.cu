@@ -404,9 +404,13 @@ static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int d
   return SFB_OK;
 }
 
-// projection pullback tail: out_a = vbar_a + D^T(w * s)  (adjoint.py:335-349)
+// projection pullback tail: out_a = vbar_a + D^T(w * s)  (adjoint.py:335-349).
+// With Kb (the sub-diagonal reverse sweep): the result r feeds only the next
+// stage cotangent kbar = c1 ybar + c2 r (adjoint.py:400-419, the combine of
+// step_backward fused here) and the g0 accumulation, so r itself is not stored.
 template <typename T, int D>
-__global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T> O, Box B, MV<T> Acc) {
+__global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T> O, Box B, MV<T> Acc, CV<T> Yb,
+                               T c1, T c2, MV<T> Kb) {
   int J[3];
   if (!box_coords<D>(B, J)) return;
   const long long x = lin<T, D>(G, J);
@@ -414,6 +418,10 @@ __global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T
     if (O.c[0]) {
 #pragma unroll
       for (int a = 0; a < D; ++a) O.c[a][x] = T(0);
+    }
+    if (Kb.c[0]) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) Kb.c[a][x] = T(0);
     }
     return;
   }
@@ -434,6 +442,11 @@ __global__ void k_proj_pb_tail(Geo<T> G, const T* __restrict__ s, CV<T> Vb, MV<T
     const T r = Vb.c[a][x] + d;
     if (O.c[0]) O.c[a][x] = r;
     if (Acc.c[0]) Acc.c[a][x] += r;  // g0 += ybar_j (adjoint.py:414-415)
+    if (Kb.c[0]) {
+      T v = Yb.c[a][x] * c1;  // k_combine's order: ybar term, then ybar_j term
+      v += r * c2;
+      Kb.c[a][x] = v;
+    }
   }
 }
 
@@ -491,7 +504,8 @@ static int need_periodic(const sfb_plan* p) {
 }
 
 template <typename T>
-static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, void* const* acc, cudaStream_t st) {
+static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, void* const* acc, cudaStream_t st,
+                      const void* const* ybar = nullptr, double c1 = 0.0, double c2 = 0.0, void* const* kb = nullptr) {
   sfb_plan* p = s->plan;
   const Geo<T>& G = geo<T>(p);
   int rc;
@@ -504,7 +518,10 @@ static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, void* 
   Box E = ext_box(G);
   MV<T> O = out ? mvp<T>(p, out) : MV<T>{{nullptr, nullptr, nullptr}};
   MV<T> Acc = acc ? mvp<T>(p, acc) : MV<T>{{nullptr, nullptr, nullptr}};
-  SFB_DISPATCH_DIM(G.dim, D, (k_proj_pb_tail<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, cvp<T>(p, vbar), O, E, Acc)));
+  MV<T> Kb = kb ? mvp<T>(p, kb) : MV<T>{{nullptr, nullptr, nullptr}};
+  CV<T> Yb = ybar ? cvp<T>(p, ybar) : CV<T>{{nullptr, nullptr, nullptr}};
+  SFB_DISPATCH_DIM(G.dim, D, (k_proj_pb_tail<T, D><<<box_grid(D, E), box_block(D), 0, st>>>(G, rb, cvp<T>(p, vbar), O, E, Acc,
+                                                                                          Yb, (T)c1, (T)c2, Kb)));
   SFB_LAUNCH_CHECK("project pullback: divergence pullback");
   return SFB_OK;
 }
@@ -623,6 +640,16 @@ int sfb_project_pullback_ex(sfb_solver* s, void* const* vbar, void* const* out, 
   if (int rc = need_periodic(s->plan)) return rc;
   return s->plan->dtype == SFB_F64 ? project_pb<double>(s, vbar, out, acc, (cudaStream_t)stream)
                                    : project_pb<float>(s, vbar, out, acc, (cudaStream_t)stream);
+}
+
+int sfb_project_pullback_kb(sfb_solver* s, void* const* vbar, void* const* acc, const void* const* ybar, double c1,
+                            double c2, void* const* kb, void* stream) {
+  if (!s || !okp(s->plan, vbar) || !okp(s->plan, acc) || !okp(s->plan, ybar) || !okp(s->plan, kb))
+    return fail(SFB_EINVAL, "null argument");
+  if (int rc = need_periodic(s->plan)) return rc;
+  return s->plan->dtype == SFB_F64
+             ? project_pb<double>(s, vbar, nullptr, acc, (cudaStream_t)stream, ybar, c1, c2, kb)
+             : project_pb<float>(s, vbar, nullptr, acc, (cudaStream_t)stream, ybar, c1, c2, kb);
 }
 
 }  // extern "C"
