@@ -219,24 +219,35 @@ def step_forward_tape(u0, dt, tableau, solver, setup, include_closure=False):
     fill_ghosts_velocity(u0, bcs)
     stages = []
     if tableau.subdiagonal:
-        # the fused stage kernels of rk_step (bitwise the same primal), each
-        # projected stage state kept in its own buffer for the tape
-        from .timestep import _project_quiet
+        # the fused stage kernels of rk_step, each projected stage state kept
+        # in its own buffer for the tape.  On periodic 3D grids (no closure)
+        # the intermediate projections stop after the solve and the next stage
+        # kernel forms y - G p on the fly, writing the projected y once into
+        # the tape (no gradient-subtract pass); otherwise full projections
+        from .timestep import _fuse_projection, _project_quiet, _project_solve
 
+        fuse = closure is None and _fuse_projection(grid)
         acc = VelocityField(grid, empty=True)
         started = False
         cur = u0
+        p_pending = None
         for j in range(s):
-            stages.append(cur)
+            yrec = VelocityField(grid, empty=True) if p_pending is not None else None
+            stages.append(yrec if yrec is not None else cur)
             nxt = j + 1 < s
             yn = VelocityField(grid, empty=True) if nxt else None
             b = tableau.b[j]
             ct = _closure_term(closure, cur, cs) if closure is not None else None
             _stage(setup, cur, u0=u0, s_in=acc if started else None, s_out=acc if b != 0.0 else None,
-                   y_next=yn, cb=dt * b, ca=dt * (tableau.a[j + 1][j] if nxt else 0.0), closure_term=ct)
+                   y_next=yn, cb=dt * b, ca=dt * (tableau.a[j + 1][j] if nxt else 0.0), closure_term=ct,
+                   p_int=p_pending, u0_out=yrec)
             started = started or b != 0.0
+            p_pending = None
             if nxt:
-                _project_quiet(yn, solver, bcs)
+                if fuse:
+                    p_pending = _project_solve(yn, solver, bcs)
+                else:
+                    _project_quiet(yn, solver, bcs)
                 cur = yn
         project_into(acc, solver, bcs)
         return acc, (stages, dt, tableau, closure)

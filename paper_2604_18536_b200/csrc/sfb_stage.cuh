@@ -57,7 +57,9 @@ __device__ __forceinline__ Coef<T> coef_at(const Geo<T>& G, int axis, int i) {
 // shared memory -- the combines take it from the ring centre and it is
 // written once to u0_out (the deferred last projection of the previous step,
 // timestep.py:208-210 fused into the next step's first stage)
-enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16, FL_PER = 32, FL_U0P = 64 };
+// bit 128 (with FL_PROJ, u0 != y): the projected stage state (ring centre) is
+// written to u0_out -- the VJP tape records it without a gradient-subtract pass
+enum { FL_K = 1, FL_S = 2, FL_SU0 = 4, FL_NEXT = 8, FL_PROJ = 16, FL_PER = 32, FL_U0P = 64, FL_YOUT = 128 };
 
 
 

@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(TJ / CPT * TK, MINB)
       for (int a = 0; a < 3; ++a) {
         if (!dof[r][a]) continue;
         if (U0P) A.u0_out.c[a][x] = b0[r][a];
+        if (FL & FL_YOUT) A.u0_out.c[a][x] = P[1][a * RG::CS];  // projected y at the centre (tape)
         if (FL & FL_K) A.k_out.c[a][x] = kv[a];
         if (FL & FL_S) A.s_out.c[a][x] = ((FL & FL_SU0) ? b0[r][a] : bs[r][a]) + kv[a] * A.cb;
         if (FL & FL_NEXT) A.y_next.c[a][x] = b0[r][a] + kv[a] * A.ca;
@@ -481,8 +482,13 @@ static int stage_march(const Geo<T>& G, const StageArgs<T>& A, cudaStream_t st, 
   const bool per = allow_per && G.per[0] && G.per[1] && G.per[2] && !G.halo[1] && !G.halo[2] && !noper;
   const int fl = (A.has_k ? FL_K : 0) | (A.has_s ? FL_S : 0) | (A.has_s && A.s_from_u0 ? FL_SU0 : 0) |
                  (A.has_next ? FL_NEXT : 0) | (A.p_int ? FL_PROJ : 0) | (per ? FL_PER : 0) |
-                 (A.u0_out.c[0] ? FL_U0P : 0);
+                 (A.u0_out.c[0] && A.u0.c[0] == A.y.c[0] ? FL_U0P : 0) |
+                 (A.u0_out.c[0] && A.u0.c[0] != A.y.c[0] ? FL_YOUT : 0);
   switch (fl) {
+    // VJP tape: stages 1-3 also record the projected stage state
+    case FL_PER | FL_S | FL_NEXT | FL_PROJ | FL_YOUT:
+      return stage_march_launch<T, FL_PER | FL_S | FL_NEXT | FL_PROJ | FL_YOUT>(G, A, st);
+    case FL_PER | FL_S | FL_PROJ | FL_YOUT: return stage_march_launch<T, FL_PER | FL_S | FL_PROJ | FL_YOUT>(G, A, st);
     case FL_PER | FL_S | FL_SU0 | FL_NEXT | FL_PROJ | FL_U0P:
       return stage_march_launch<T, FL_PER | FL_S | FL_SU0 | FL_NEXT | FL_PROJ | FL_U0P>(G, A, st);
     case FL_S | FL_SU0 | FL_NEXT | FL_PROJ | FL_U0P:
@@ -538,7 +544,10 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
       (G.dim == 3 && (A.F.a[0] != nullptr) != (A.F.a[2] != nullptr)))
     return fail(SFB_EINVAL, "force fields: give all components or none");
   if (A.has_next && !a->u0[0]) return fail(SFB_EINVAL, "y_next requires u0");
-  if (A.u0_out.c[0]) {
+  if (A.u0_out.c[0] && a->u0[0] != a->y[0]) {
+    if (!A.p_int || A.has_k)
+      return fail(SFB_EINVAL, "u0_out with u0 != y: the projected stage state of an on-the-fly projection only");
+  } else if (A.u0_out.c[0]) {
     if (!A.p_int || a->u0[0] != a->y[0] || !A.has_s || !A.s_from_u0 || A.has_k)
       return fail(SFB_EINVAL, "u0_out: stage 0 of a deferred projection only (p_int set, u0 == y, s from u0)");
     for (int c = 0; c < G.dim; ++c)
