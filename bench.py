@@ -281,8 +281,9 @@ def run_ours(args):
             sim.rk4_step(st, dt)
 
         def steps(k):
-            for _ in range(k):
-                step()
+            # run_steps on the slab: each step's last projection is finished
+            # by the next step's stage 0
+            sim.run_steps(st, k, dt)
 
         def cur_u():
             return st.u

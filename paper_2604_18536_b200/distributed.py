@@ -330,9 +330,11 @@ class CudaSlabBackend:
     def _sp(self):
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
-    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0, p_slab=None):
+    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0, p_slab=None, u0_out=None):
         a = N.StageArgs()
         a.p_int = None if p_slab is None else p_slab.data_ptr()
+        if u0_out is not None:
+            a.u0_out = N.ptr3(u0_out.u)
         a.y = N.ptr3(y.u)
         a.u0 = N.ptr3(u0.u if u0 is not None else [None] * 3)
         a.s_in = N.ptr3(s_in.u if s_in is not None else [None] * 3)
@@ -347,7 +349,7 @@ class CudaSlabBackend:
         if TS.STAGE_EVENTS is None:
             N.call("sfb_rk_stage", self.plan.handle, ctypes.byref(a), self._sp())
             return
-        nfield = 1 + (s_out is not None) + (y_next is not None)
+        nfield = 1 + (s_out is not None) + (y_next is not None) + (u0_out is not None)
         nfield += (u0 is not None and u0 is not y and (y_next is not None or (s_out is not None and s_in is None)))
         nfield += (s_in is not None and s_out is not None)
         nfield += (1.0 / 3.0) if p_slab is not None else 0.0
@@ -473,6 +475,15 @@ class SlabProjector:
         if p_ext is not None:
             comm.halo([p_ext.data])
 
+    def finish(self, u, p_ext=None):
+        """Complete a projection stopped after project_solve (u -= G p, ghost
+        fills, halo): the tail of ``project``."""
+        b, comm = self.b, self.comm
+        b.correct(u, p_ext)
+        comm.halo(u.u)
+        if p_ext is not None:
+            comm.halo([p_ext.data])
+
     def project_solve(self, u):
         """Projection split at the gradient subtract (timestep._project_solve):
         u keeps its exchanged (unprojected) ghost planes, the slab pressure
@@ -495,6 +506,9 @@ class SlabState:
         self.pressure = p
         self.t = t
         self.step = 0
+        # run_steps: the last projection of the previous step stopped after
+        # its solve (u unprojected, this slab pressure pending)
+        self.pending = None
 
 
 class SlabSimulation:
@@ -513,18 +527,39 @@ class SlabSimulation:
         self.comm.halo(u_local.u)
         return SlabState(u_local, regs, p)
 
-    def rk4_step(self, state, dt):
+    def rk4_step(self, state, dt, defer=False):
+        """One RK4 step.  ``defer`` (run_steps): the step's last projection
+        stops after its solve and the next step's stage 0 applies u - G p
+        while staging u, writing the projected u0 once (timestep.rk_step's
+        deferred form on the slab)."""
         from .timestep import RK4
 
         tab = RK4
-        u0 = state.u
-        acc, y, yn = state.regs
+        p_in = state.pending
+        state.pending = None
+        if p_in is not None:
+            # registers: u* (the unprojected state), u0 (its projection), s, y
+            u_star = state.u
+            u0, acc, y = state.regs
+            yn = None
+        else:
+            u_star = None
+            u0 = state.u
+            acc, y, yn = state.regs
         started = False
-        cur = u0
-        p_pending = None
+        cur = u0 if p_in is None else u_star
+        p_pending = p_in
         for j in range(tab.stages):
             bj = tab.b[j]
             nxt = j + 1 < tab.stages
+            if j == 0 and p_in is not None:
+                self.b.stage(u_star, u0=u_star, s_out=acc, y_next=y, cb=dt * bj, ca=dt * tab.a[1][0],
+                             p_slab=p_in, u0_out=u0)
+                started = True
+                yn = u_star  # u* is free once its projection is in u0
+                p_pending = self.proj.project_solve(y)
+                cur = y
+                continue
             self.b.stage(cur, u0=u0, s_in=acc if started else None, s_out=acc if bj != 0.0 else None,
                          y_next=yn if nxt else None, cb=dt * bj, ca=dt * (tab.a[j + 1][j] if nxt else 0.0),
                          p_slab=p_pending)
@@ -535,12 +570,30 @@ class SlabSimulation:
                 p_pending = self.proj.project_solve(yn)
                 y, yn = yn, y
                 cur = y
-        self.proj.project(acc, p_ext=state.pressure)
+        if defer:
+            state.pending = self.proj.project_solve(acc)
+        else:
+            self.proj.project(acc, p_ext=state.pressure)
         state.regs = [u0, y, yn]
         state.u = acc
         state.t += dt
         state.step += 1
         return state
+
+    def finish(self, state):
+        """Complete a deferred last projection (the state rk4_step returns)."""
+        if state.pending is not None:
+            self.proj.finish(state.u, p_ext=state.pressure)
+            state.pending = None
+        return state
+
+    def run_steps(self, state, nsteps, dt):
+        """timestep.run_steps on the slab: each step's last projection is
+        finished by the next step's first stage kernel; the returned state is
+        fully projected."""
+        for _ in range(nsteps):
+            self.rk4_step(state, dt, defer=True)
+        return self.finish(state)
 
     def kinetic_energy(self, u):
         return self.comm.allreduce(self.b.kinetic_energy_local(u), "sum")

@@ -99,17 +99,21 @@ class CpuSlabBackend:
             ys[a] -= g
         return ys
 
-    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0, p_slab=None):
+    def stage(self, y, u0=None, s_in=None, s_out=None, y_next=None, cb=0.0, ca=0.0, p_slab=None, u0_out=None):
         og = self.og
         yv = self._np(y) if p_slab is None else self._project_copy(y, p_slab)
         k = O.momentum_rhs(og, yv, self.nu, self.force)
         for a in range(3):
             sl = og.udof(a)
+            # u0_out (u0 is y, deferred projection): the combines use projected y
+            u0v = yv[a] if u0_out is not None else (u0.u[a].numpy() if u0 is not None else None)
+            if u0_out is not None:
+                u0_out.u[a].numpy()[sl] = yv[a][sl]
             if s_out is not None:
-                base = (s_in if s_in is not None else u0).u[a].numpy()
+                base = s_in.u[a].numpy() if s_in is not None else u0v
                 s_out.u[a].numpy()[sl] = base[sl] + k[a][sl] * cb
             if y_next is not None:
-                y_next.u[a].numpy()[sl] = u0.u[a].numpy()[sl] + k[a][sl] * ca
+                y_next.u[a].numpy()[sl] = u0v[sl] + k[a][sl] * ca
 
     # -- spectral solve in column chunks (the CUDA backend's interface)
     def max_chunks(self):

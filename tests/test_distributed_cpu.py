@@ -40,7 +40,7 @@ def _global_case():
     return bounds, g, u
 
 
-def _worker(rank, size, port, outdir, nsteps):
+def _worker(rank, size, port, outdir, nsteps, defer=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=size)
@@ -57,8 +57,11 @@ def _worker(rank, size, port, outdir, nsteps):
         for a, arr in enumerate(scatter_field(u, lay)):
             loc.u[a].copy_(torch.from_numpy(arr))
         st = sim.new_state(loc)
-        for _ in range(nsteps):
-            sim.rk4_step(st, DT)
+        if defer:
+            sim.run_steps(st, nsteps, DT)
+        else:
+            for _ in range(nsteps):
+                sim.rk4_step(st, DT)
         ke = sim.kinetic_energy(st.u)
         m = lay.m
         parts = [st.u.u[a][1:m + 1].contiguous() for a in range(3)] + [st.pressure.data[1:m + 1].contiguous()]
@@ -81,11 +84,13 @@ def _worker(rank, size, port, outdir, nsteps):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("nsteps", [1, 2])
-def test_slab_rk4_world2_matches_oracle(nsteps):
+@pytest.mark.parametrize("nsteps,defer", [(1, False), (2, False), (3, True)])
+def test_slab_rk4_world2_matches_oracle(nsteps, defer):
+    """world 2 (gloo): rk4_step, and run_steps with each step's last
+    projection deferred into the next step's stage 0 (u0_out)."""
     size = 2
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(size, _free_port(), d, nsteps), nprocs=size, join=True)
+        mp.spawn(_worker, args=(size, _free_port(), d, nsteps, defer), nprocs=size, join=True)
         z = np.load(os.path.join(d, "out.npz"))
         bounds, g, u = _global_case()
         bcs = O.periodic_bcs(3)

@@ -32,7 +32,7 @@ def _case():
     return bounds, g, u
 
 
-def _run(rank, size, stage_host, nsteps, nccl=False):
+def _run(rank, size, stage_host, nsteps, nccl=False, defer=False):
     import paper_2604_18536_b200 as P
     from paper_2604_18536_b200.distributed import (Comm, CudaSlabBackend, NcclComm, SlabGrid, SlabLayout,
                                                    SlabSimulation, scatter_field)
@@ -47,8 +47,11 @@ def _run(rank, size, stage_host, nsteps, nccl=False):
     for a, arr in enumerate(scatter_field(u, lay)):
         loc.u[a].copy_(torch.from_numpy(arr))
     st = sim.new_state(loc)
-    for _ in range(nsteps):
-        sim.rk4_step(st, DT)
+    if defer:
+        sim.run_steps(st, nsteps, DT)
+    else:
+        for _ in range(nsteps):
+            sim.rk4_step(st, DT)
     torch.cuda.synchronize()
     m = lay.m
     return [st.u.u[a][1:m + 1].cpu() for a in range(3)] + [st.pressure.data[1:m + 1].cpu()], sim.kinetic_energy(st.u)
@@ -86,6 +89,15 @@ def test_slab_p1_nccl_comm_matches_oracle():
     _check([f.numpy() for f in fields], ke, 2)
 
 
+def test_slab_p1_run_steps_deferred_matches_oracle():
+    """run_steps on the slab (NCCL communicator): each step's last projection
+    applied by the next step's stage 0 (FL_U0P on the halo plan)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    fields, ke = _run(0, 1, False, 3, nccl=True, defer=True)
+    _check([f.numpy() for f in fields], ke, 3)
+
+
 def test_nccl_comm_ops_one_rank():
     """sfb_comm_* at one rank: periodic self halo, all-to-all and
     send/recv as device copies on the caller's stream, all-reduce identity."""
@@ -119,13 +131,13 @@ def _free_port():
     return port
 
 
-def _worker(rank, size, port, outdir):
+def _worker(rank, size, port, outdir, defer=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
-        fields, ke = _run(rank, size, True, 2)
+        fields, ke = _run(rank, size, True, 2, defer=defer)
         gathered = []
         for t in fields:
             t = t.contiguous()
@@ -139,10 +151,14 @@ def _worker(rank, size, port, outdir):
         dist.destroy_process_group()
 
 
-def test_slab_p2_cuda_two_processes_matches_oracle():
+@pytest.mark.parametrize("defer", [False, True])
+def test_slab_p2_cuda_two_processes_matches_oracle(defer):
+    """P = 2 on one device (host-staged gloo): rk4_step, and run_steps with
+    the deferred last projection (stage 0 reads the exchanged unprojected
+    ghost planes and the neighbours' pressure planes)."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, _free_port(), d, defer), nprocs=2, join=True)
         z = np.load(os.path.join(d, "out.npz"))
         _check([z[f"f{i}"] for i in range(4)], float(z["ke"]), 2)
