@@ -62,11 +62,18 @@ def test_register_fft_solve_vs_oracle_and_stockham(P, shape, dtype, monkeypatch)
 
 @pytest.mark.parametrize("shape", [(840, 6, 8), (6, 840, 40), (96, 64, 512), (48, 40, 32), (20, 24, 420)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_tiled_spectrum_bitwise_natural(P, shape, dtype, monkeypatch):
-    """The 3D solve's tiled half spectrum (column blocks, fft.cu) runs the
-    same per-column arithmetic as the natural layout: bitwise-equal pressure,
-    including ragged last blocks (n2/2+1 not a multiple of the block width)."""
+@pytest.mark.parametrize("rows_tiled", [False, True])
+def test_tiled_spectrum_bitwise_natural(P, shape, dtype, rows_tiled, monkeypatch):
+    """The 3D solve's tiled half spectrum (column blocks, fft.cu) -- the
+    default hybrid (tiled copy for the strided passes) and the all-tiled
+    variant (SFB_FFT_TILED_ROWS) -- runs the same per-column arithmetic as the
+    natural layout: bitwise-equal pressure, including ragged last blocks
+    (n2/2+1 not a multiple of the block width)."""
     monkeypatch.delenv("SFB_FFT_NATURAL", raising=False)
+    if rows_tiled:
+        monkeypatch.setenv("SFB_FFT_TILED_ROWS", "1")
+    else:
+        monkeypatch.delenv("SFB_FFT_TILED_ROWS", raising=False)
     tiled, ref = _solve(P, shape, dtype, monkeypatch, stockham=False)
     monkeypatch.setenv("SFB_FFT_NATURAL", "1")
     nat, _ = _solve(P, shape, dtype, monkeypatch, stockham=False)
