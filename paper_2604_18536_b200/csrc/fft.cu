@@ -479,6 +479,65 @@ template bool fft_divfuse_ok<float>(const FftSolve&, const Geo<float>&);
 
 #define SFB_REG(F, a) reg_of((F).reg_ax[a], (F).reg_a[a], (F).reg_b[a])
 
+// ---- channel solve (poisson.py:203-229 on separable channel grids): the
+// register engine does the raw FFT(x, z) passes, the batched tridiagonal
+// solve along y (poisson.cu k_tridiag) runs between them on the natural
+// half spectrum (n0, n1, nh)
+template <typename T>
+bool fft_channel_divfuse_ok(const FftSolve& F, const Geo<T>& G) {
+  if (getenv("SFB_NO_DIVFUSE")) return false;
+  return F.reg_half && F.reg_ax[0] && G.dim == 3 && F.dim == 3 && G.per[0] && !G.halo[0] && G.per[2] && !G.halo[2] &&
+         !G.per[1] && F.n[0] == G.n[0] && F.n[1] == G.n[1] && F.n[2] == G.n[2];
+}
+template bool fft_channel_divfuse_ok<double>(const FftSolve&, const Geo<double>&);
+template bool fft_channel_divfuse_ok<float>(const FftSolve&, const Geo<float>&);
+
+template <typename T>
+int fft_channel_forward(FftSolve& F, const T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G,
+                        const void* const* u) {
+  typedef typename CX<T>::t C;
+  C* cbuf = (C*)cbuf_v;
+  const int n0 = F.n[0], n1 = F.n[1], nlast = F.n[2], nh = nlast / 2 + 1;
+  const long long rows = (long long)n0 * n1;
+  if (G) {
+    // R2C along z of the divergence (walls on y resolved inline)
+    RegCall c{};
+    c.kind = 5;
+    c.out = cbuf;
+    c.rows = rows;
+    c.out_row = nh;
+    c.twL = F.tw_half;
+    c.twN = F.tw_full;
+    c.geo = G;
+    c.wall1 = 1;
+    for (int a = 0; a < 3; ++a) c.u[a] = u[a];
+    if (int rc = reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st)) return rc;
+  } else if (int rc = launch_r2c<T>(F, rbuf, cbuf, rows, st)) {
+    return rc;
+  }
+  ScaleArgs none{};
+  return launch_strided<T, 0>(cbuf, F.ax[0], 0, (long long)n1 * nh, n1 * nh, 0, 1, (const C*)F.tw_ax[0], none, st,
+                              nullptr, SFB_REG(F, 0));
+}
+
+template <typename T>
+int fft_channel_inverse(FftSolve& F, void* cbuf_v, T* rbuf, cudaStream_t st) {
+  typedef typename CX<T>::t C;
+  C* cbuf = (C*)cbuf_v;
+  const int n0 = F.n[0], n1 = F.n[1], nh = F.n[2] / 2 + 1;
+  ScaleArgs none{};
+  if (int rc = launch_strided<T, 1>(cbuf, F.ax[0], 0, (long long)n1 * nh, n1 * nh, 0, 1, (const C*)F.tw_ax[0], none,
+                                    st, nullptr, SFB_REG(F, 0)))
+    return rc;
+  return launch_c2r<T>(F, cbuf, rbuf, (long long)n0 * n1, st);
+}
+template int fft_channel_forward<double>(FftSolve&, const double*, void*, cudaStream_t, const Geo<double>*,
+                                         const void* const*);
+template int fft_channel_forward<float>(FftSolve&, const float*, void*, cudaStream_t, const Geo<float>*,
+                                        const void* const*);
+template int fft_channel_inverse<double>(FftSolve&, void*, double*, cudaStream_t);
+template int fft_channel_inverse<float>(FftSolve&, void*, float*, cudaStream_t);
+
 template <typename T>
 int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u) {
   typedef typename CX<T>::t C;

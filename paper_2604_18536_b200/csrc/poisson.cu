@@ -454,11 +454,35 @@ static int exec_inv(sfb_solver* s, T* out, cudaStream_t st) {
 }
 
 template <typename T>
+static int launch_tridiag(sfb_solver* s, cudaStream_t st) {
+  sfb_plan* p = s->plan;
+  const int n0 = p->n[0], n1 = p->n[1], nh = p->n[2] / 2 + 1;
+  dim3 grid((nh + 63) / 64, n0);
+  double2* dd = sizeof(T) == 8 ? (double2*)s->cbuf : s->dscr;
+  k_tridiag<T><<<grid, 64, 0, st>>>((typename CT<T>::type*)s->cbuf, dd, s->cprime, s->up, s->lo, s->di, s->dxy,
+                                    s->lam[0], s->lam[2], n0, n1, nh, 1.0 / ((double)n0 * p->n[2]));
+  SFB_LAUNCH_CHECK("tridiagonal");
+  return SFB_OK;
+}
+
+// channel solve on the register FFT engine: FFT(x, z) -> tridiagonal(y) ->
+// inverse; the divergence of u fused into the R2C when G/u are given
+template <typename T>
+static int channel_fft_solve(sfb_solver* s, T* buf, cudaStream_t st, const Geo<T>* G = nullptr,
+                             const void* const* u = nullptr) {
+  int rc;
+  if ((rc = fft_channel_forward<T>(s->fft, buf, s->cbuf, st, G, u))) return rc;
+  if ((rc = launch_tridiag<T>(s, st))) return rc;
+  return fft_channel_inverse<T>(s->fft, s->cbuf, buf, st);
+}
+
+template <typename T>
 int solve_inplace(sfb_solver* s, T* buf, cudaStream_t st) {
   // buf: contiguous interior rhs in, solution out
   sfb_plan* p = s->plan;
   int rc;
   if (s->kind == SFB_SOLVER_CG) return cg_solve<T>(s, buf, st);
+  if (s->kind == SFB_SOLVER_CHANNEL && s->fft.enabled) return channel_fft_solve<T>(s, buf, st);
   if (s->fft.enabled) return fft_solve_inplace<T>(s->fft, buf, s->cbuf, st);
   if ((rc = exec_fwd<T>(s, buf, st))) return rc;
   if (s->kind == SFB_SOLVER_SPECTRAL) {
@@ -471,13 +495,8 @@ int solve_inplace(sfb_solver* s, T* buf, cudaStream_t st) {
                      (k_spec_scale<T, D><<<nb, 256, 0, st>>>((typename CT<T>::type*)s->cbuf, s->lam[0], s->lam[1],
                                                              s->lam[2], m0, m1, mh, invN)));
     SFB_LAUNCH_CHECK("spectral scale");
-  } else {
-    const int n0 = p->n[0], n1 = p->n[1], nh = p->n[2] / 2 + 1;
-    dim3 grid((nh + 63) / 64, n0);
-    double2* dd = sizeof(T) == 8 ? (double2*)s->cbuf : s->dscr;
-    k_tridiag<T><<<grid, 64, 0, st>>>((typename CT<T>::type*)s->cbuf, dd, s->cprime, s->up, s->lo, s->di, s->dxy,
-                                      s->lam[0], s->lam[2], n0, n1, nh, 1.0 / ((double)n0 * p->n[2]));
-    SFB_LAUNCH_CHECK("tridiagonal");
+  } else if ((rc = launch_tridiag<T>(s, st))) {
+    return rc;
   }
   return exec_inv<T>(s, buf, st);
 }
@@ -486,6 +505,7 @@ template int solve_inplace<float>(sfb_solver*, float*, cudaStream_t);
 
 template <typename T>
 static bool divfused(const sfb_solver* s) {
+  if (s->kind == SFB_SOLVER_CHANNEL) return s->fft.enabled && fft_channel_divfuse_ok<T>(s->fft, geo<T>(s->plan));
   return s->fft.enabled && (fft_divfuse_ok<T>(s->fft, geo<T>(s->plan)) || getenv("SFB_DIVFUSE"));
 }
 
@@ -500,7 +520,11 @@ static int project_solve(sfb_solver* s, const void* const* u, cudaStream_t st) {
   int rc;
   if (divfused<T>(s)) {
     // divergence fused into the first FFT pass
-    if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, u))) return rc;
+    if (s->kind == SFB_SOLVER_CHANNEL) {
+      if ((rc = channel_fft_solve<T>(s, rb, st, &G, u))) return rc;
+    } else if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, u))) {
+      return rc;
+    }
   } else {
     if ((rc = launch_div<T>(G, C, rb, st))) return rc;
     if ((rc = solve_inplace<T>(s, rb, st))) return rc;
@@ -522,6 +546,33 @@ static int project(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t st) 
     // pressure ghosts (fields.py:81-93) from the interior just written
     if ((rc = launch_planes<T>(G, MV<T>{{(T*)p_ext, nullptr, nullptr}}, 1, 1, st))) return rc;
   }
+  return SFB_OK;
+}
+
+// Register-engine FFT(x, z) for the channel solver when the x length and the
+// half z length have an instantiated engine (else cuFFT plans, make_plans)
+static int setup_fft_channel(sfb_solver* s) {
+  sfb_plan* p = s->plan;
+  FftSolve& F = s->fft;
+  const bool f64 = p->dtype == SFB_F64;
+  const int n0 = p->n[0], n2 = p->n[2];
+  if (p->dim != 3 || n2 % 2 != 0) return SFB_OK;
+  FftLen half, ax0;
+  if (!fft_factor(n2 / 2, half) || !fft_factor(n0, ax0)) return SFB_OK;
+  int rc;
+  if ((rc = (f64 ? fft_set_smem_limits<double>() : fft_set_smem_limits<float>()))) return rc;
+  F.dim = 3;
+  for (int a = 0; a < 3; ++a) F.n[a] = p->n[a];
+  F.total = p->int_count;
+  F.half = half;
+  F.ax[0] = ax0;
+  F.ax[1] = ax0;  // unused (the y direction is the tridiagonal solve)
+  if ((rc = fft_upload_pass_twiddles(F.ax[0], f64, &F.tw_ax[0]))) return rc;
+  if ((rc = fft_upload_pass_twiddles(F.half, f64, &F.tw_half))) return rc;
+  if ((rc = fft_upload_twiddles(n2, f64, &F.tw_full))) return rc;
+  fft_reg_assign(F);
+  if (!F.reg_half || !F.reg_ax[0]) return SFB_OK;
+  F.enabled = true;
   return SFB_OK;
 }
 
@@ -676,6 +727,9 @@ int sfb_solver_create(sfb_plan* p, int kind, sfb_solver** out) {
   }
   if (kind == SFB_SOLVER_SPECTRAL && !getenv("SFB_FORCE_CUFFT")) {
     if ((rc = setup_fft(s))) goto bad;
+  }
+  if (kind == SFB_SOLVER_CHANNEL && !getenv("SFB_FORCE_CUFFT")) {
+    if ((rc = setup_fft_channel(s))) goto bad;
   }
   if (!s->fft.enabled && (rc = make_plans(s))) goto bad;
   if (kind == SFB_SOLVER_CHANNEL) {

@@ -78,6 +78,16 @@ template <typename T>
 int fft_forward(FftSolve& F, const T* in, void* out, cudaStream_t st);
 template <typename T>
 int fft_inverse(FftSolve& F, void* in, T* out, cudaStream_t st);
+// channel solve (fft.cu): R2C along z (of the divergence when G/u given,
+// walls on y resolved inline) + forward FFT along x; inverse x + C2R; the
+// tridiagonal solve along y runs between them (poisson.cu)
+template <typename T>
+int fft_channel_forward(FftSolve& F, const T* rbuf, void* cbuf, cudaStream_t st, const Geo<T>* G,
+                        const void* const* u);
+template <typename T>
+int fft_channel_inverse(FftSolve& F, void* cbuf, T* rbuf, cudaStream_t st);
+template <typename T>
+bool fft_channel_divfuse_ok(const FftSolve& F, const Geo<T>& G);
 // the register engine can fuse the divergence of u into the R2C pass
 template <typename T>
 bool fft_divfuse_ok(const FftSolve& F, const Geo<T>& G);

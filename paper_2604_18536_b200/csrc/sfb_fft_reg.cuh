@@ -468,19 +468,29 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW
 // (operators.py:108-122, same operation order as k_div_int), read from the
 // extended velocity arrays; the divergence field never touches HBM.
 // Axes 1 and 2 periodic, axis 0 periodic or a halo axis (slab).
-template <typename T>
+// WALL1 (channel: walls on axis 1): the two axis-1 faces of a wall-adjacent
+// row are resolved inline like k_div_int / k_div_march (the wall face carries
+// the Dirichlet value, zero for a symmetric wall): w1lo -> u_1 below = v1lo,
+// w1hi -> u_1 at the cell's upper face = v1hi
+template <typename T, bool WALL1 = false>
 __device__ __forceinline__ T div_at(const Geo<T>& G, const T* __restrict__ u0, const T* __restrict__ u1,
                                     const T* __restrict__ u2, long long x, long long o0m, long long o1m, T r0, T r1,
-                                    int kk) {
+                                    int kk, bool w1lo = false, bool w1hi = false, T v1lo = T(0), T v1hi = T(0)) {
   const long long xk = x + kk;
   const long long o2m = kk == 1 ? (long long)(G.n[2] - 1) : -1;
   T acc = (__ldg(u0 + xk) - __ldg(u0 + xk + o0m)) * r0;
-  acc += (__ldg(u1 + xk) - __ldg(u1 + xk + o1m)) * r1;
+  if constexpr (WALL1) {
+    const T c1 = w1hi ? v1hi : __ldg(u1 + xk);
+    const T p1 = w1lo ? v1lo : __ldg(u1 + xk + o1m);
+    acc += (c1 - p1) * r1;
+  } else {
+    acc += (__ldg(u1 + xk) - __ldg(u1 + xk + o1m)) * r1;
+  }
   acc += (__ldg(u2 + xk) - __ldg(u2 + xk + o2m)) * tab(G, 2, T_RDX, kk);
   return acc;
 }
 
-template <typename T, int A, int B>
+template <typename T, int A, int B, bool WALL1 = false>
 __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_R2CDIV_MINB))
     k_rfft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, long long rows, long long out_row,
                    const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN, int tlog,
@@ -500,13 +510,16 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW
       const int i = 1 + (int)(row / G.n[1]), j = 1 + (int)(row % G.n[1]);
       const long long x = (long long)i * G.s[0] + (long long)j * G.s[1];
       const long long o0m = (i == 1 && !G.halo[0]) ? (long long)(G.n[0] - 1) * G.s[0] : -G.s[0];
-      const long long o1m = j == 1 ? (long long)(G.n[1] - 1) * G.s[1] : -G.s[1];
+      const long long o1m = (!WALL1 && j == 1) ? (long long)(G.n[1] - 1) * G.s[1] : -G.s[1];
       const T r0 = tab(G, 0, T_RDX, i), r1 = tab(G, 1, T_RDX, j);
+      const bool w1lo = WALL1 && j == 1, w1hi = WALL1 && j == G.n[1];
+      const T v1lo = (WALL1 && G.bc_lo[1] == SFB_BC_DIRICHLET) ? G.vlo[1][1] : T(0);
+      const T v1hi = (WALL1 && G.bc_hi[1] == SFB_BC_DIRICHLET) ? G.vhi[1][1] : T(0);
 #pragma unroll
       for (int n1 = 0; n1 < A; ++n1) {
         const int m = B * n1 + n2;
-        v[n1].x = div_at(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 1);
-        v[n1].y = div_at(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 2);
+        v[n1].x = div_at<T, WALL1>(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 1, w1lo, w1hi, v1lo, v1hi);
+        v[n1].y = div_at<T, WALL1>(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 2, w1lo, w1hi, v1lo, v1hi);
       }
     } else {
 #pragma unroll
@@ -655,6 +668,7 @@ struct RegCall {
   const void* geo;     // kind 5: host Geo<T> of the velocity plan
   const void* u[3];    // kind 5: extended velocity components
   int tlog;            // kinds 3-5: tiled spectrum (r2c_epilogue), 0 = natural
+  int wall1;           // kind 5: walls on axis 1 (channel), resolved inline
   long long ks;        //   its block stride
 };
 
@@ -688,6 +702,7 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     SFB_ATTR((k_rfft_r2c<T, A, B>), RG::SMEM_R);
     SFB_ATTR((k_rfft_c2r<T, A, B>), RG::SMEM_R);
     SFB_ATTR((k_rfft_r2c_div<T, A, B>), RG::SMEM_R);
+    SFB_ATTR((k_rfft_r2c_div<T, A, B, true>), RG::SMEM_R);
 #undef SFB_ATTR
     if (e != cudaSuccess) return -2;
   }
@@ -723,8 +738,14 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     else {
       CV<T> U;
       for (int a = 0; a < 3; ++a) U.c[a] = (const T*)c.u[a];
-      k_rfft_r2c_div<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>(*(const Geo<T>*)c.geo, U, (C*)c.out, c.rows, c.out_row,
-                                                              (const C*)c.twL, (const C*)c.twN, c.tlog, c.ks);
+      if (c.wall1)
+        k_rfft_r2c_div<T, A, B, true><<<nb, RG::NT_R, RG::SMEM_R, st>>>(*(const Geo<T>*)c.geo, U, (C*)c.out, c.rows,
+                                                                      c.out_row, (const C*)c.twL, (const C*)c.twN,
+                                                                      c.tlog, c.ks);
+      else
+        k_rfft_r2c_div<T, A, B><<<nb, RG::NT_R, RG::SMEM_R, st>>>(*(const Geo<T>*)c.geo, U, (C*)c.out, c.rows,
+                                                                c.out_row, (const C*)c.twL, (const C*)c.twN, c.tlog,
+                                                                c.ks);
     }
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
