@@ -512,9 +512,15 @@ static int project_pb(sfb_solver* s, void* const* vbar, void* const* out, void* 
   if ((rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st))) return rc;  // zero_non_dofs(vbar)
   Box B = int_box(G);
   T* rb = (T*)s->rbuf;
-  SFB_DISPATCH_DIM(G.dim, D, (k_grad_pb<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, cvp<T>(p, vbar), rb, B, T(-1), 1, 1)));
-  SFB_LAUNCH_CHECK("project pullback: gradient pullback");
-  if ((rc = solve_inplace<T>(s, rb, st))) return rc;
+  static const bool nofuse = env_int("SFB_NO_PBFUSE") != 0;
+  if (s->kind == SFB_SOLVER_SPECTRAL && s->fft.enabled && fft_divfuse_ok<T>(s->fft, G) && !nofuse) {
+    // -G^T(vbar)/W formed inside the solve's first (R2C) pass
+    if ((rc = fft_solve_inplace<T>(s->fft, rb, s->cbuf, st, &G, (const void* const*)vbar, 1))) return rc;
+  } else {
+    SFB_DISPATCH_DIM(G.dim, D, (k_grad_pb<T, D><<<box_grid(D, B), box_block(D), 0, st>>>(G, cvp<T>(p, vbar), rb, B, T(-1), 1, 1)));
+    SFB_LAUNCH_CHECK("project pullback: gradient pullback");
+    if ((rc = solve_inplace<T>(s, rb, st))) return rc;
+  }
   Box E = ext_box(G);
   MV<T> O = out ? mvp<T>(p, out) : MV<T>{{nullptr, nullptr, nullptr}};
   MV<T> Acc = acc ? mvp<T>(p, acc) : MV<T>{{nullptr, nullptr, nullptr}};

@@ -539,7 +539,8 @@ template int fft_channel_inverse<double>(FftSolve&, void*, double*, cudaStream_t
 template int fft_channel_inverse<float>(FftSolve&, void*, float*, cudaStream_t);
 
 template <typename T>
-int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u) {
+int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const Geo<T>* G, const void* const* u,
+                      int gradt) {
   typedef typename CX<T>::t C;
   C* cbuf = (C*)cbuf_v;
   const size_t csz = sizeof(C);
@@ -563,6 +564,7 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
     c.out_row = nh;
     c.tlog = tiled ? F.tlog : 0;
     c.ks = F.tks;
+    c.gradt = gradt;
     c.twL = F.tw_half;
     c.twN = F.tw_full;
     c.geo = G;
@@ -570,6 +572,7 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
     int rc = reg_run<T>(reg_of(F.reg_half, F.reg_a_half, F.reg_b_half), c, st);
     if (rc) return rc;
   } else if (G) {
+    if (gradt) return fail(SFB_EINVAL, "fused projection-pullback input needs the register R2C");
     size_t sm = 2 * (size_t)M * csz;
     CV<T> U;
     for (int a = 0; a < 3; ++a) U.c[a] = a < dim ? (const T*)u[a] : nullptr;
@@ -666,8 +669,10 @@ int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf_v, cudaStream_t st, const
   // 5. C2R along the contiguous axis
   return launch_c2r<T>(F, cbuf, rbuf, rows, st);
 }
-template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*);
-template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*);
+template int fft_solve_inplace<double>(FftSolve&, double*, void*, cudaStream_t, const Geo<double>*, const void* const*,
+                                       int);
+template int fft_solve_inplace<float>(FftSolve&, float*, void*, cudaStream_t, const Geo<float>*, const void* const*,
+                                      int);
 
 // Standalone unnormalised real transforms (the `transforms.rfftn/irfftn`
 // plugin, transforms.py:9-12): R2C along the contiguous axis, then forward

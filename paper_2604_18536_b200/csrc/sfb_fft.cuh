@@ -67,9 +67,10 @@ int fft_upload_twiddles(int L, bool f64, void** dev);
 int fft_upload_pass_twiddles(FftLen& P, bool f64, void** dev);
 // Spectral solve in place on rbuf.  When G/u are given, the right-hand side
 // is the divergence of u, computed inside the first (R2C) pass.
+// gradt: the right-hand side is -G^T(u)/W instead (the projection pullback)
 template <typename T>
 int fft_solve_inplace(FftSolve& F, T* rbuf, void* cbuf, cudaStream_t st, const Geo<T>* G = nullptr,
-                      const void* const* u = nullptr);
+                      const void* const* u = nullptr, int gradt = 0);
 template <typename T>
 int fft_set_smem_limits();
 // unnormalised real transforms of a contiguous array (fft.cu): forward

@@ -490,7 +490,25 @@ __device__ __forceinline__ T div_at(const Geo<T>& G, const T* __restrict__ u0, c
   return acc;
 }
 
-template <typename T, int A, int B, bool WALL1 = false>
+// GT: the input of the projection pullback's solve instead of a divergence,
+// -G^T(v) / W at the pressure point (adjoint.cu k_grad_pb with sign -1 and
+// the 1/W weight, periodic axes), same operation order
+template <typename T>
+__device__ __forceinline__ T gradT_at(const Geo<T>& G, const T* __restrict__ v0, const T* __restrict__ v1,
+                                      const T* __restrict__ v2, long long x, long long o0m, long long o1m, T q0m, T q0,
+                                      T q1m, T q1, T rw01, int kk) {
+  const long long xk = x + kk;
+  const long long o2m = kk == 1 ? (long long)(G.n[2] - 1) : -1;
+  const int km = kk == 1 ? G.n[2] : kk - 1;
+  T acc = T(0);
+  acc += __ldg(v0 + xk + o0m) * q0m - __ldg(v0 + xk) * q0;
+  acc += __ldg(v1 + xk + o1m) * q1m - __ldg(v1 + xk) * q1;
+  acc += __ldg(v2 + xk + o2m) * tab(G, 2, T_RDU, km) - __ldg(v2 + xk) * tab(G, 2, T_RDU, kk);
+  acc = T(-1) * acc;
+  return acc * (rw01 * tab(G, 2, T_RDX, kk));
+}
+
+template <typename T, int A, int B, bool WALL1 = false, bool GT = false>
 __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW_MINB_T(T, SFB_R2CDIV_MINB))
     k_rfft_r2c_div(Geo<T> G, CV<T> U, typename CX<T>::t* __restrict__ out, long long rows, long long out_row,
                    const typename CX<T>::t* __restrict__ twM, const typename CX<T>::t* __restrict__ twN, int tlog,
@@ -515,11 +533,24 @@ __global__ void __launch_bounds__(RegGeo<typename CX<T>::t, A, B>::NT_R, SFB_ROW
       const bool w1lo = WALL1 && j == 1, w1hi = WALL1 && j == G.n[1];
       const T v1lo = (WALL1 && G.bc_lo[1] == SFB_BC_DIRICHLET) ? G.vlo[1][1] : T(0);
       const T v1hi = (WALL1 && G.bc_hi[1] == SFB_BC_DIRICHLET) ? G.vhi[1][1] : T(0);
+      if constexpr (GT) {
+        const int im = i == 1 ? G.n[0] : i - 1, jm = j == 1 ? G.n[1] : j - 1;
+        const T q0m = tab(G, 0, T_RDU, im), q0 = tab(G, 0, T_RDU, i);
+        const T q1m = tab(G, 1, T_RDU, jm), q1 = tab(G, 1, T_RDU, j);
+        const T rw01 = (T(1) * r0) * r1;
 #pragma unroll
-      for (int n1 = 0; n1 < A; ++n1) {
-        const int m = B * n1 + n2;
-        v[n1].x = div_at<T, WALL1>(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 1, w1lo, w1hi, v1lo, v1hi);
-        v[n1].y = div_at<T, WALL1>(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 2, w1lo, w1hi, v1lo, v1hi);
+        for (int n1 = 0; n1 < A; ++n1) {
+          const int m = B * n1 + n2;
+          v[n1].x = gradT_at(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, q0m, q0, q1m, q1, rw01, 2 * m + 1);
+          v[n1].y = gradT_at(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, q0m, q0, q1m, q1, rw01, 2 * m + 2);
+        }
+      } else {
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) {
+          const int m = B * n1 + n2;
+          v[n1].x = div_at<T, WALL1>(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 1, w1lo, w1hi, v1lo, v1hi);
+          v[n1].y = div_at<T, WALL1>(G, U.c[0], U.c[1], U.c[2], x, o0m, o1m, r0, r1, 2 * m + 2, w1lo, w1hi, v1lo, v1hi);
+        }
       }
     } else {
 #pragma unroll
@@ -669,6 +700,7 @@ struct RegCall {
   const void* u[3];    // kind 5: extended velocity components
   int tlog;            // kinds 3-5: tiled spectrum (r2c_epilogue), 0 = natural
   int wall1;           // kind 5: walls on axis 1 (channel), resolved inline
+  int gradt;           // kind 5: -G^T(v)/W (projection pullback) instead of div(v)
   long long ks;        //   its block stride
 };
 
@@ -703,6 +735,7 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     SFB_ATTR((k_rfft_c2r<T, A, B>), RG::SMEM_R);
     SFB_ATTR((k_rfft_r2c_div<T, A, B>), RG::SMEM_R);
     SFB_ATTR((k_rfft_r2c_div<T, A, B, true>), RG::SMEM_R);
+    SFB_ATTR((k_rfft_r2c_div<T, A, B, false, true>), RG::SMEM_R);
 #undef SFB_ATTR
     if (e != cudaSuccess) return -2;
   }
@@ -738,7 +771,10 @@ static int reg_launch(const RegCall& c, cudaStream_t st) {
     else {
       CV<T> U;
       for (int a = 0; a < 3; ++a) U.c[a] = (const T*)c.u[a];
-      if (c.wall1)
+      if (c.gradt)
+        k_rfft_r2c_div<T, A, B, false, true><<<nb, RG::NT_R, RG::SMEM_R, st>>>(
+            *(const Geo<T>*)c.geo, U, (C*)c.out, c.rows, c.out_row, (const C*)c.twL, (const C*)c.twN, c.tlog, c.ks);
+      else if (c.wall1)
         k_rfft_r2c_div<T, A, B, true><<<nb, RG::NT_R, RG::SMEM_R, st>>>(*(const Geo<T>*)c.geo, U, (C*)c.out, c.rows,
                                                                       c.out_row, (const C*)c.twL, (const C*)c.twN,
                                                                       c.tlog, c.ks);
