@@ -106,6 +106,10 @@ const char* sfb_last_error(void);
 /* Grid / BC plan: grid.py:115-223, bcs.py:47-83, operators.py:38-90. */
 int sfb_plan_create(const sfb_grid_desc* desc, sfb_plan** out);
 int sfb_plan_destroy(sfb_plan* plan);
+/* New Dirichlet wall values ([axis][component], row-major 3x3 each side) for
+ * a time-dependent, spatially uniform callable Dirichlet (fields.py:72-76,
+ * evaluated by the caller at the fill time). */
+int sfb_plan_set_walls(sfb_plan* plan, const double* val_lo, const double* val_hi);
 
 /* Ghost fills: fields.py:96-140 (velocity), fields.py:81-93 (scalar). */
 int sfb_fill_ghosts_velocity(sfb_plan* plan, void* const* u, void* stream);

@@ -61,6 +61,7 @@ class StageArgs(ctypes.Structure):
 _SIGS = {
     "sfb_plan_create": [ctypes.POINTER(GridDesc), ctypes.POINTER(vp)],
     "sfb_plan_destroy": [vp],
+    "sfb_plan_set_walls": [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
     "sfb_fill_ghosts_velocity": [vp, VP3, vp],
     "sfb_fill_ghosts_scalar": [vp, vp, vp],
     "sfb_divergence": [vp, VP3, vp, vp],

@@ -2,6 +2,7 @@
 // (replaces grid.py:115-223 + operators.py:38-90 as seen by the kernels).
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -165,6 +166,31 @@ int sfb_plan_create(const sfb_grid_desc* d, sfb_plan** out) {
 bad:
   sfb_plan_destroy(p);
   return rc;
+}
+
+// Dirichlet wall values of a plan whose walls move (a callable Dirichlet
+// evaluated at a new time, fields.py:72-76); kernels take the plan's Geo by
+// value at launch, so every launch after this call sees the new values
+int sfb_plan_set_walls(sfb_plan* p, const double* val_lo, const double* val_hi) {
+  if (!p || !val_lo || !val_hi) return fail(SFB_EINVAL, "null argument");
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < 3; ++c) {
+      p->val_lo[a][c] = val_lo[3 * a + c];
+      p->val_hi[a][c] = val_hi[3 * a + c];
+    }
+  auto put = [&](auto& G) {
+    typedef typename std::remove_reference<decltype(G.vlo[0][0])>::type T;
+    for (int a = 0; a < 3; ++a)
+      for (int c = 0; c < 3; ++c) {
+        G.c2lo[a][c] = (T)(2.0 * p->val_lo[a][c]);
+        G.c2hi[a][c] = (T)(2.0 * p->val_hi[a][c]);
+        G.vlo[a][c] = (T)p->val_lo[a][c];
+        G.vhi[a][c] = (T)p->val_hi[a][c];
+      }
+  };
+  put(p->g64);
+  put(p->g32);
+  return SFB_OK;
 }
 
 int sfb_plan_destroy(sfb_plan* p) {

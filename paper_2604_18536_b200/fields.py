@@ -90,9 +90,12 @@ def fill_ghosts_scalar(f, bcs):
 
 
 def fill_ghosts_velocity(v, bcs, t=0.0):
-    """fields.py:96-140 (constant Dirichlet values; ``t`` is accepted for
-    signature compatibility)."""
-    N.call("sfb_fill_ghosts_velocity", get_plan(v.grid, bcs).handle, N.ptr3(v.u), stream_ptr())
+    """fields.py:96-140; callable Dirichlet walls are evaluated at ``t``
+    (spatially uniform ones on the device path)."""
+    plan = get_plan(v.grid, bcs)
+    if plan.moving:
+        plan.set_time(float(t))
+    N.call("sfb_fill_ghosts_velocity", plan.handle, N.ptr3(v.u), stream_ptr())
     return v
 
 

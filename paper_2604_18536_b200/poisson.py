@@ -27,7 +27,7 @@ from .bcs import BoundarySpec, Dirichlet
 from .errors import ConfigurationError, ConvergenceError
 from .fields import ScalarField
 from .operators import pressure_weights
-from .plan import get_plan, stream_ptr
+from .plan import get_plan, set_time, stream_ptr
 
 
 def homogeneous(bcs):
@@ -247,6 +247,7 @@ def _native_solver(solver, bcs):
 def project_into(u, solver, bcs, t=0.0, scratch=None, p_div=None, p_out=None):
     """poisson.py:321-341: make ``u`` discretely divergence-free in place
     (one fused native call); returns the ghost-filled pressure."""
+    set_time(u.grid, bcs, t)  # callable (moving) Dirichlet walls at the fill time
     s = _native_solver(solver, bcs)
     if p_out is None:
         p_out = ScalarField(u.grid)

@@ -17,6 +17,10 @@ Cases (each a small .npz next to this script):
 * ``solve_transpose``: ``poisson_solve_transpose`` (adjoint.py:236-250) with
   the spectral solver on a uniform box and the direct solver on a stretched
   periodic box.
+* ``moving_wall``: time-dependent callable Dirichlet walls (fields.py:72-77,
+  evaluated at every stage's fill time, timestep.py:189-209/232-245) -- a 3D
+  channel whose top wall oscillates in x and a 2D cavity whose lid
+  accelerates -- three RK4, SSP33 and Wray3 steps each.
 """
 
 import os
@@ -35,6 +39,19 @@ def force_fn(c, *x):
     if c == 1:
         return 0.2 * np.cos(2.0 * np.pi * x[0]) * (1.0 + 0.0 * x[1])
     return -0.15 * np.sin(x[0] + x[1]) * np.cos(x[2])
+
+
+def lid_channel(c, *x):
+    """Top wall of the channel: oscillating streamwise velocity, uniform
+    over the wall (last positional argument is the time)."""
+    t = x[-1]
+    return 0.7 * np.cos(3.0 * t) if c == 0 else 0.0 * x[0]
+
+
+def lid_cavity(c, *x):
+    """Lid of the cavity: a smoothly accelerating tangential velocity."""
+    t = x[-1]
+    return np.tanh(5.0 * t) + 0.0 * x[0] if c == 0 else 0.0
 
 
 def main():
@@ -157,6 +174,37 @@ def main():
         out[f"{tag}_pbar"] = pb.data.copy()
         out[f"{tag}_out"] = res.data.copy()
     save("solve_transpose", **out)
+
+    # ---- moving (time-dependent, spatially uniform) Dirichlet walls
+    rng = np.random.default_rng(15)
+    out = {"dt": 0.02, "nsteps": 3}
+    cases = (
+        ("chan", Grid((uniform_grid(0.0, 2.0, 8), tanh_grid(0.0, 1.0, 6, 1.4), uniform_grid(0.0, 1.0, 4)),
+                      (True, False, True)),
+         BoundarySpec([(Periodic(), Periodic()), (Dirichlet(0.0), Dirichlet(lid_channel)), (Periodic(), Periodic())])),
+        ("cav", Grid((tanh_grid(0.0, 1.0, 7, 1.5), uniform_grid(0.0, 1.2, 6)), (False, False)),
+         BoundarySpec([(Dirichlet(0.0), Dirichlet(0.0)), (Dirichlet(0.0), Dirichlet(lid_cavity))])),
+    )
+    for tag, g, bcs in cases:
+        u = rvel(g, rng)
+        solver = poisson.make_solver("direct", g, bcs)
+        u0, _ = poisson.project(u, solver, bcs, t=0.0)
+        out.update({f"{tag}_{k}": val for k, val in grid_meta(g).items()})
+        out.update(vel(f"{tag}_u0", u0))
+        for meth, tab in (("rk4", rk4), ("ssp33", ts.SSP33), ("wray3", None)):
+            setup = ts.Setup(g, bcs, nu=0.05, solver="direct", method="ssp33")
+            if tab is not None:
+                setup.tableau = tab
+            st = setup.new_state(u0=u0)
+            for _ in range(out["nsteps"]):
+                if tab is None:
+                    ts.wray3_step(st, out["dt"], setup.solver, setup)
+                else:
+                    ts.rk_step(st, out["dt"], tab, setup.solver, setup)
+            out.update(vel(f"{tag}_{meth}_u", st.u))
+            out[f"{tag}_{meth}_p"] = st.pressure.data.copy()
+            out[f"{tag}_{meth}_t"] = st.t
+    save("moving_wall", **out)
 
 
 if __name__ == "__main__":

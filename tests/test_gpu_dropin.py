@@ -194,3 +194,74 @@ def test_config_build_setup_channel_rk4(P):
     st = setup.new_state(u0=cases.channel_ic(setup.grid, 0.0055, seed=1))
     P.rk_step(st, 1e-3, P.RK4, setup.solver, setup)
     assert float(P.divergence(st.u).data.abs().max()) < 1e-10
+
+
+def _lid_channel(c, *x):
+    t = x[-1]
+    return 0.7 * np.cos(3.0 * t) if c == 0 else 0.0 * x[0]
+
+
+def _lid_cavity(c, *x):
+    t = x[-1]
+    return np.tanh(5.0 * t) + 0.0 * x[0] if c == 0 else 0.0
+
+
+@pytest.mark.parametrize("meth", ["rk4", "ssp33", "wray3"])
+def test_moving_wall_golden(P, meth):
+    """Time-dependent, spatially uniform callable Dirichlet walls
+    (fields.py:72-77), re-evaluated at every stage's fill time: an
+    oscillating channel wall (direct solver = FFT x tridiagonal) and an
+    accelerating cavity lid (direct solver = CG to 1e-12), three steps."""
+    c = load("moving_wall")
+    dt, nsteps = float(c["dt"]), int(c["nsteps"])
+    for tag, lid, t in (("chan", _lid_channel, 1e-11), ("cav", _lid_cavity, 1e-8)):
+        cc = {k[len(tag) + 1:]: v for k, v in c.items() if k.startswith(tag + "_")}
+        pg, og = _grid(P, cc)
+        if tag == "chan":
+            bcs = P.BoundarySpec([(P.Periodic(), P.Periodic()), (P.Dirichlet(0.0), P.Dirichlet(lid)),
+                                  (P.Periodic(), P.Periodic())])
+        else:
+            bcs = P.BoundarySpec([(P.Dirichlet(0.0), P.Dirichlet(0.0)), (P.Dirichlet(0.0), P.Dirichlet(lid))])
+        d = pg.dim
+        setup = P.Setup(pg, bcs, nu=0.05, solver="direct", method=meth)
+        st = setup.new_state(u0=vel(P, pg, [cc[f"u0{a}"] for a in range(d)]))
+        for _ in range(nsteps):
+            if meth == "wray3":
+                P.wray3_step(st, dt, setup.solver, setup)
+            else:
+                P.rk_step(st, dt, setup.tableau, setup.solver, setup)
+        assert abs(st.t - float(cc[f"{meth}_t"])) <= 1e-15
+        got = st.u.numpy()
+        for a in range(d):
+            assert rel(got[a], cc[f"{meth}_u{a}"]) <= t, (tag, meth, a)
+        assert rel(st.pressure.numpy(), cc[f"{meth}_p"]) <= t, (tag, meth)
+
+
+def test_moving_wall_simulate_matches_steps(P):
+    """simulate/run_steps carry the wall time through (t advances with the
+    state): run_steps(3) equals three rk_step calls bit for bit."""
+    c = load("moving_wall")
+    cc = {k[5:]: v for k, v in c.items() if k.startswith("chan_")}
+    pg, og = _grid(P, cc)
+    bcs = P.BoundarySpec([(P.Periodic(), P.Periodic()), (P.Dirichlet(0.0), P.Dirichlet(_lid_channel)),
+                          (P.Periodic(), P.Periodic())])
+    u0 = [cc[f"u0{a}"] for a in range(3)]
+    setup = P.Setup(pg, bcs, nu=0.05, solver="direct", method="rk4")
+    st = setup.new_state(u0=vel(P, pg, u0))
+    for _ in range(3):
+        P.rk_step(st, 0.02, setup.tableau, setup.solver, setup)
+    st2 = P.run_steps(setup, 3, dt=0.02, u0=vel(P, pg, u0), project_initial=False)
+    for x, y in zip(st.u.numpy(), st2.u.numpy()):
+        assert np.array_equal(x, y)
+    assert rel(st2.u.numpy()[0], cc["rk4_u0"]) <= 1e-11
+    assert st2.t == st.t
+
+
+def test_moving_wall_must_be_uniform(P):
+    g = P.Grid([P.uniform_grid(0.0, 1.0, 8), P.tanh_grid(0.0, 1.0, 6, 1.4), P.uniform_grid(0.0, 1.0, 4)],
+               (True, False, True))
+    bcs = P.BoundarySpec([(P.Periodic(), P.Periodic()),
+                          (P.Dirichlet(0.0), P.Dirichlet(lambda c, x, y, z, t: np.sin(x) * (1.0 + t))),
+                          (P.Periodic(), P.Periodic())])
+    with pytest.raises(P.ConfigurationError, match="uniform"):
+        P.Setup(g, bcs, nu=0.05, solver="direct", method="rk4").new_state()
