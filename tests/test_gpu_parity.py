@@ -492,3 +492,33 @@ def test_errors_map_to_reference_exceptions(P):
     setup = P.Setup(gw, wall, nu=0.01, solver="direct", method="rk4")
     with pytest.raises(P.ConfigurationError):
         P.unrolled_gradient(P.KineticEnergyLoss(), P.VelocityField(gw), 1, 0.01, setup)
+
+
+@pytest.mark.parametrize("shape", [(20, 13, 37), (9, 40, 33), (64, 8, 96)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_rhs_pullback_ragged_tiles_garbage_ghosts(P, shape, dtype):
+    """The marching rhs pullback (TMA ring in fp64, wrapped cp.async in fp32)
+    on stretched periodic grids whose sizes are not multiples of the tile,
+    with random values in the ghost layers of vbar and u: equal to the
+    oracle's rhs_pullback (adjoint.py:253-261); vbar's ghosts come back zero
+    (adjoint.py:119-136), u keeps its interior."""
+    import torch
+
+    rng = np.random.default_rng(sum(shape))
+    bounds = [O.tanh_bounds(0.0, 1.0 + 0.2 * a, n, 1.3) for a, n in enumerate(shape)]
+    pg, og = grids(P, bounds, (True,) * 3, dtype)
+    bcs = P.BoundarySpec.all_periodic(3)
+    vb = [rng.standard_normal(og.ext_shape).astype(dtype) for _ in range(3)]
+    u = [rng.standard_normal(og.ext_shape).astype(dtype) for _ in range(3)]
+    ref = O.rhs_pullback(og, O.periodic_bcs(3), [x.copy() for x in vb], [x.copy() for x in u], 0.013)
+    vbd, ud = vel(P, pg, vb), vel(P, pg, u)
+    got = P.rhs_pullback(vbd, ud, 0.013, bcs).numpy()
+    torch.cuda.synchronize()
+    for a in range(3):
+        assert rel(got[a], ref[a]) <= tol(dtype)
+    vbo, uo = vbd.numpy(), ud.numpy()
+    for a in range(3):
+        ghost = np.ones(og.ext_shape, bool)
+        ghost[1:-1, 1:-1, 1:-1] = False
+        assert not np.any(vbo[a][ghost])
+        assert np.array_equal(uo[a][1:-1, 1:-1, 1:-1], u[a][1:-1, 1:-1, 1:-1])
