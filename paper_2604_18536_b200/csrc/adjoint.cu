@@ -12,6 +12,7 @@
 
 #include "sfb_solver.cuh"
 #include "sfb_stage.cuh"
+#include "sfb_tma.cuh"
 
 namespace sfb {
 
@@ -220,14 +221,31 @@ __global__ void __launch_bounds__(256) k_rhs_pb(Geo<T> G, CV<T> Vb, CV<T> U, MV<
 #define SFB_PB_MINB 3
 #endif
 constexpr int kPbTJ = SFB_PB_TJ, kPbTK = 32, kPbRing = 5;
-constexpr int kPbPW = kPbTK + 2, kPbPH = kPbTJ + 2, kPbPS = kPbPW * kPbPH, kPbNE = 6 * kPbPS;
+// a field's plane tile in a ring slot: PS values at a 128-byte-aligned stride
+// (kPbCS) so every TMA box lands aligned
+constexpr int kPbPW = kPbTK + 2, kPbPH = kPbTJ + 2, kPbPS = kPbPW * kPbPH, kPbCS = (kPbPS + 15) / 16 * 16,
+              kPbNE = 6 * kPbCS;
 constexpr int kPbNT = kPbTJ * kPbTK, kPbNQ = (kPbNE + kPbNT - 1) / kPbNT;
 
-template <typename T, int ACC>
-__global__ void __launch_bounds__(kPbNT, SFB_PB_MINB) k_rhs_pb_march(Geo<T> G, CV<T> Vb, CV<T> U, MV<T> O, T nu, int diff,
-                                                            int chunk) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw);  // [slot][6][PS]: vbar0..2, u0..2
+// TMA descriptors of vbar0..2, u0..2: (TK+2) x (TJ+2) x 1 boxes of the
+// extended arrays (fp64, ghosts holding the periodic images)
+struct alignas(64) PbMaps {
+  CUtensorMap m[6];
+};
+
+// TMA: every plane tile comes in as six boxes issued by one thread and
+// completed on the slot's mbarrier; the halo is read from the ghost layers,
+// which the caller fills with the periodic images first.  Otherwise the
+// per-element cp.async fill reads the wrapped source indices.
+#ifndef SFB_PB_MINB_TMA
+#define SFB_PB_MINB_TMA 4  // 128 registers without spills: rhs pullback 3.81 -> 3.41 ms at 512^3
+#endif
+template <typename T, int ACC, bool TMA = false>
+__global__ void __launch_bounds__(kPbNT, TMA ? SFB_PB_MINB_TMA : SFB_PB_MINB) k_rhs_pb_march(Geo<T> G, CV<T> Vb, CV<T> U, MV<T> O, T nu, int diff,
+                                                            int chunk, const __grid_constant__ PbMaps M) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);  // [slot][6][CS]: vbar0..2, u0..2
+  __shared__ __align__(8) unsigned long long pbar[kPbRing];
   // stencil tables staged in shared memory (wrapped indices, see below):
   // axis 1 per tile row, axis 2 per tile column, axis 0 per plane (two
   // alternating sets of planes i-1, i, i+1)
@@ -240,26 +258,55 @@ __global__ void __launch_bounds__(kPbNT, SFB_PB_MINB) k_rhs_pb_march(Geo<T> G, C
   const int ie = min(ib + chunk, G.n[0] + 1);
   const int n0 = G.n[0], n1 = G.n[1], n2 = G.n[2];
   const long long s0 = G.s[0], s1 = G.s[1];
-  const T* fsrc[kPbNQ];
-  bool fok[kPbNQ];
+  constexpr int NQ = TMA ? 1 : kPbNQ;
+  const T* fsrc[NQ];
+  bool fok[NQ];
+  if constexpr (!TMA) {
 #pragma unroll
-  for (int q = 0; q < kPbNQ; ++q) {
-    const int e = tid + q * kPbNT;
-    const int f = e / kPbPS;
-    const int r = e - f * kPbPS;
-    const int jj = r / kPbPW, kk = r - jj * kPbPW;
-    const int gj = wr(j0 - 1 + jj, n1), gk = wr(k0 - 1 + kk, n2);  // periodic wrap of the halo
-    fok[q] = e < kPbNE;
-    const T* base = f < 3 ? Vb.c[f] : U.c[f < 6 ? f - 3 : 0];
-    fsrc[q] = base + (fok[q] ? (long long)gj * s1 + gk : 0);
+    for (int q = 0; q < NQ; ++q) {
+      const int e = tid + q * kPbNT;
+      const int f = e / kPbCS;
+      const int r = e - f * kPbCS;
+      const int jj = r / kPbPW, kk = r - jj * kPbPW;
+      const int gj = wr(j0 - 1 + jj, n1), gk = wr(k0 - 1 + kk, n2);  // periodic wrap of the halo
+      fok[q] = e < kPbNE && r < kPbPS;
+      const T* base = f < 3 ? Vb.c[f] : U.c[f < 6 ? f - 3 : 0];
+      fsrc[q] = base + (fok[q] ? (long long)gj * s1 + gk : 0);
+    }
   }
+  unsigned yph = 0, ypend = 0;  // per-slot barrier parity / loads in flight (tracked by every thread)
+  if constexpr (TMA) {
+    if (tid == 0) {
+#pragma unroll
+      for (int b = 0; b < kPbRing; ++b) mbar_init(&pbar[b], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  auto ywait = [&](int slot) {
+    if (TMA && ((ypend >> slot) & 1)) {
+      mbar_wait(&pbar[slot], (yph >> slot) & 1);
+      yph ^= 1u << slot;
+      ypend &= ~(1u << slot);
+    }
+  };
   auto load_plane = [&](int ip, int slot) {
     if (ip < 0 || ip > n0 + 1) return;
-    const long long base = (long long)wr(ip, n0) * s0;
-    T* dst = ring + slot * kPbNE + tid;
+    if constexpr (TMA) {
+      ypend |= 1u << slot;
+      if (tid == 0) {
+        T* dst = ring + slot * kPbNE;
+        mbar_arm(&pbar[slot], 6u * kPbPS * (unsigned)sizeof(T));
 #pragma unroll
-    for (int q = 0; q < kPbNQ; ++q)
-      if (q < kPbNQ - 1 || tid + q * kPbNT < kPbNE) cp_async_val(dst + q * kPbNT, fsrc[q] + (fok[q] ? base : 0), fok[q]);
+        for (int f = 0; f < 6; ++f) tma_load(&M.m[f], 3, dst + f * kPbCS, &pbar[slot], k0 - 1, j0 - 1, ip);
+      }
+    } else {
+      const long long base = (long long)wr(ip, n0) * s0;
+      T* dst = ring + slot * kPbNE + tid;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < NQ - 1 || tid + q * kPbNT < kPbNE) cp_async_val(dst + q * kPbNT, fsrc[q] + (fok[q] ? base : 0), fok[q]);
+    }
   };
   const int j = j0 + tj, k = k0 + tk;
   const bool inside = j <= n1 && k <= n2;
@@ -292,19 +339,29 @@ __global__ void __launch_bounds__(kPbNT, SFB_PB_MINB) k_rhs_pb_march(Geo<T> G, C
 #pragma unroll
       for (int c = 0; c < 3; ++c) accin[c] = O.c[c][x];
     }
-    cp_wait<1>();
+    int s1i = sl_m + 1, s2i = sl_m + 2;
+    if (s1i >= kPbRing) s1i -= kPbRing;
+    if (s2i >= kPbRing) s2i -= kPbRing;
+    if (TMA) {
+      if (i == ib) {
+        ywait(sl_m);
+        ywait(s1i);
+      }
+      ywait(s2i);
+      // this thread's reads of the slot refilled below, before the TMA write
+      fence_proxy_async_smem();
+    } else {
+      cp_wait<1>();
+    }
     __syncthreads();
     int sl_l = sl_m + 4;
     if (sl_l >= kPbRing) sl_l -= kPbRing;
     load_plane(i + 3, sl_l);
     cp_commit();
-    int s1i = sl_m + 1, s2i = sl_m + 2;
-    if (s1i >= kPbRing) s1i -= kPbRing;
-    if (s2i >= kPbRing) s2i -= kPbRing;
     if (inside) {
       const T* P[3] = {ring + sl_m * kPbNE + c0, ring + s1i * kPbNE + c0, ring + s2i * kPbNE + c0};
       // field f at offset (d0, d1, d2), f in 0..2 vbar, 3..5 u
-      auto R = [&](int f, int d0, int d1, int d2) -> T { return P[1 + d0][f * kPbPS + d1 * kPbPW + d2]; };
+      auto R = [&](int f, int d0, int d1, int d2) -> T { return P[1 + d0][f * kPbCS + d1 * kPbPW + d2]; };
       // table value of axis ax, slot sl at the cell's index + off (wrapped)
       const T* ti = tbi + (i & 1) * SFB_NTAB * 3;
       auto TB = [&](int ax, int sl, int off) -> T {
@@ -378,13 +435,45 @@ __global__ void __launch_bounds__(kPbNT, SFB_PB_MINB) k_rhs_pb_march(Geo<T> G, C
     sl_m = s1i;
   }
   cp_wait<0>();
+  // no TMA write may still target this CTA's shared memory when it exits
+#pragma unroll
+  for (int b = 0; b < kPbRing; ++b) ywait(b);
 }
 
+// TMA maps of vbar and u for k_rhs_pb_march (fp64: a (TK+2)-wide fp32 box row
+// is not a multiple of 16 bytes); false -> the cp.async fill
 template <typename T>
-static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int diff, int accumulate, cudaStream_t st) {
+static bool pb_maps(const Geo<T>& G, CV<T> V, CV<T> Uf, PbMaps& M) {
+  static const bool off = env_int("SFB_PB_NOTMA") != 0;
+  if (sizeof(T) != 8 || off || G.dim != 3) return false;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encode_fn();
+  if (!enc) return false;
+  const size_t esz = sizeof(T);
+  if ((G.s[1] * esz) % 16 || (G.s[0] * esz) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)G.E[2], (cuuint64_t)G.E[1], (cuuint64_t)G.E[0]};
+  cuuint64_t strides[2] = {(cuuint64_t)(G.s[1] * esz), (cuuint64_t)(G.s[0] * esz)};
+  cuuint32_t box[3] = {(cuuint32_t)kPbPW, (cuuint32_t)kPbPH, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  for (int f = 0; f < 6; ++f) {
+    const T* ptr = f < 3 ? V.c[f] : Uf.c[f - 3];
+    if (!ptr || ((uintptr_t)ptr % 16)) return false;
+    if (enc(&M.m[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)ptr, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
+}
+
+// tma: the caller has filled the ghosts of V and Uf with their periodic images
+template <typename T>
+static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int diff, int accumulate, cudaStream_t st,
+                        const PbMaps* maps = nullptr) {
   const size_t smem = ((size_t)kPbRing * kPbNE + SFB_NTAB * (kPbPH + kPbPW + 6)) * sizeof(T);
   cudaError_t e = ensure_smem((const void*)k_rhs_pb_march<T, 0>, smem);
   if (e == cudaSuccess) e = ensure_smem((const void*)k_rhs_pb_march<T, 1>, smem);
+  if (e == cudaSuccess) e = ensure_smem((const void*)k_rhs_pb_march<T, 0, true>, smem);
+  if (e == cudaSuccess) e = ensure_smem((const void*)k_rhs_pb_march<T, 1, true>, smem);
   if (e != cudaSuccess) return cuda_check(e, "rhs pullback: shared-memory attribute");
   const int bx = (G.n[2] + kPbTK - 1) / kPbTK, by = (G.n[1] + kPbTJ - 1) / kPbTJ;
   const long long bps = (long long)bx * by;
@@ -397,8 +486,12 @@ static int rhs_pb_march(const Geo<T>& G, CV<T> V, CV<T> Uf, MV<T> O, T nu, int d
   if (chunk < 16) chunk = 16;
   const int bz = (G.n[0] + chunk - 1) / chunk;
   dim3 grid(bx, by, bz), blk(kPbTK, kPbTJ);
-  if (accumulate) k_rhs_pb_march<T, 1><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk);
-  else k_rhs_pb_march<T, 0><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk);
+  static const PbMaps none{};
+  const PbMaps& M = maps ? *maps : none;
+  if (maps && accumulate) k_rhs_pb_march<T, 1, true><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk, M);
+  else if (maps) k_rhs_pb_march<T, 0, true><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk, M);
+  else if (accumulate) k_rhs_pb_march<T, 1><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk, M);
+  else k_rhs_pb_march<T, 0><<<grid, blk, smem, st>>>(G, V, Uf, O, nu, diff, chunk, M);
   SFB_LAUNCH_CHECK("rhs pullback (march)");
   if (!accumulate) return launch_planes<T>(G, O, 3, 2, st);  // non-DOF entries of the output are zero
   return SFB_OK;
@@ -614,9 +707,23 @@ int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, doubl
   cudaStream_t st = (cudaStream_t)stream;
   return SFB_TYPED(p, ([&]() {
     const Geo<T>& G = geo<T>(p);
+    static const bool pb_generic = env_int("SFB_PB_GENERIC") != 0;
+    PbMaps maps;
+    if (G.dim == 3 && !pb_generic &&
+        pb_maps<T>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), maps)) {
+      // TMA tiles read the halo from the ghost layers: periodic images of
+      // vbar and u first (the primal's refill is the reference's own,
+      // adjoint.py:189); vbar's ghosts are zeroed afterwards, as the
+      // reference leaves them (adjoint.py:119-136 zero_non_dofs)
+      int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 0, st);
+      if (!rc) rc = launch_planes<T>(G, mvp<T>(p, (void* const*)u), p->dim, 0, st);
+      if (!rc) rc = rhs_pb_march<T>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), mvp<T>(p, out), (T)nu,
+                                    nu != 0.0, accumulate, st, &maps);
+      if (!rc) rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);
+      return rc;
+    }
     int rc = launch_planes<T>(G, mvp<T>(p, vbar), p->dim, 2, st);
     if (rc) return rc;
-    static const bool pb_generic = env_int("SFB_PB_GENERIC") != 0;
     if (G.dim == 3 && !pb_generic)
       return rhs_pb_march<T>(G, cvp<T>(p, (const void* const*)vbar), cvp<T>(p, u), mvp<T>(p, out), (T)nu, nu != 0.0,
                              accumulate, st);
