@@ -29,7 +29,7 @@ import torch
 
 from .errors import ConfigurationError
 from .fields import VelocityField, fill_ghosts_velocity
-from .timestep import SimState, _step
+from .timestep import SimState, _finish_pending, _step
 
 
 class HostEnsemble:
@@ -58,6 +58,7 @@ class HostEnsemble:
         self.host = host
         # member 0 may reuse an existing state (its workspace and velocity)
         base = state if state is not None else setup.new_state(t0=t0)
+        _finish_pending(base, setup)  # a deferred projection must not meet an upload
         ws = base.workspace
         self.states = [base] + [SimState(u=VelocityField(g, empty=True), t=base.t, workspace=ws)
                                 for _ in range(len(host) - 1)]
