@@ -639,6 +639,7 @@ static bool okp(const sfb_plan* p, const void* const* u) {
 extern "C" {
 
 int sfb_divergence_pullback(sfb_plan* p, void* pbar, void* const* out, void* stream) {
+  SFB_RANGE();
   if (!p || !pbar || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
   if (int rc = need_periodic(p)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -654,6 +655,7 @@ int sfb_divergence_pullback(sfb_plan* p, void* pbar, void* const* out, void* str
 }
 
 int sfb_pressure_gradient_pullback(sfb_plan* p, void* const* vbar, void* out, void* stream) {
+  SFB_RANGE();
   if (!p || !okp(p, vbar) || !out) return fail(SFB_EINVAL, "null argument");
   if (int rc = need_periodic(p)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -669,6 +671,7 @@ int sfb_pressure_gradient_pullback(sfb_plan* p, void* const* vbar, void* out, vo
 }
 
 int sfb_diffusion_pullback(sfb_plan* p, void* const* vbar, double nu, void* const* out, void* stream) {
+  SFB_RANGE();
   if (!p || !okp(p, vbar) || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
   if (int rc = need_periodic(p)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -685,6 +688,7 @@ int sfb_diffusion_pullback(sfb_plan* p, void* const* vbar, double nu, void* cons
 }
 
 int sfb_convection_pullback(sfb_plan* p, void* const* vbar, const void* const* u, void* const* out, void* stream) {
+  SFB_RANGE();
   if (!p || !okp(p, vbar) || !okp(p, u) || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
   if (int rc = need_periodic(p)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -701,6 +705,7 @@ int sfb_convection_pullback(sfb_plan* p, void* const* vbar, const void* const* u
 
 int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, double nu, void* const* out, double scale,
                      int accumulate, void* stream) {
+  SFB_RANGE();
   if (!p || !okp(p, vbar) || !okp(p, u) || !okp(p, out)) return fail(SFB_EINVAL, "null argument");
   if (int rc = need_periodic(p)) return rc;
   if (scale != 1.0) return fail(SFB_EINVAL, "scale must be 1 (reserved)");
@@ -735,6 +740,7 @@ int sfb_rhs_pullback(sfb_plan* p, void* const* vbar, const void* const* u, doubl
 }
 
 int sfb_solve_transpose(sfb_solver* s, const void* pbar, void* out, void* stream) {
+  SFB_RANGE();
   if (!s || !pbar || !out) return fail(SFB_EINVAL, "null argument");
   if (s->slab) return fail(SFB_ECONFIG, "solve transpose: not available on a slab solver");
   return s->plan->dtype == SFB_F64 ? solve_transpose<double>(s, (const double*)pbar, (double*)out, (cudaStream_t)stream)
@@ -742,10 +748,12 @@ int sfb_solve_transpose(sfb_solver* s, const void* pbar, void* out, void* stream
 }
 
 int sfb_project_pullback(sfb_solver* s, void* const* vbar, void* const* out, void* stream) {
+  SFB_RANGE();
   return sfb_project_pullback_ex(s, vbar, out, nullptr, stream);
 }
 
 int sfb_project_pullback_ex(sfb_solver* s, void* const* vbar, void* const* out, void* const* acc, void* stream) {
+  SFB_RANGE();
   if (!s || !okp(s->plan, vbar)) return fail(SFB_EINVAL, "null argument");
   if (out && !okp(s->plan, out)) return fail(SFB_EINVAL, "bad out");
   if (acc && !okp(s->plan, acc)) return fail(SFB_EINVAL, "bad acc");
@@ -757,6 +765,7 @@ int sfb_project_pullback_ex(sfb_solver* s, void* const* vbar, void* const* out, 
 
 int sfb_project_pullback_kb(sfb_solver* s, void* const* vbar, void* const* acc, const void* const* ybar, double c1,
                             double c2, void* const* kb, void* stream) {
+  SFB_RANGE();
   if (!s || !okp(s->plan, vbar) || !okp(s->plan, acc) || !okp(s->plan, ybar) || !okp(s->plan, kb))
     return fail(SFB_EINVAL, "null argument");
   if (int rc = need_periodic(s->plan)) return rc;

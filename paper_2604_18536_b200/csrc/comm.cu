@@ -111,6 +111,7 @@ int sfb_comm_rank(const sfb_comm* c) { return c ? c->rank : -1; }
 // peer_recv, one NCCL group (either side may be skipped with a null pointer)
 int sfb_comm_sendrecv(sfb_comm* c, const void* send, int peer_send, void* recv, int peer_recv, size_t bytes,
                       void* stream) {
+  SFB_RANGE();
   if (!c) return fail(SFB_EINVAL, "null communicator");
   cudaStream_t st = (cudaStream_t)stream;
   if (c->nranks == 1) {  // periodic self-exchange
@@ -129,6 +130,7 @@ int sfb_comm_sendrecv(sfb_comm* c, const void* send, int peer_send, void* recv, 
 // (plane_bytes each): plane 0 <- prev rank's plane m, plane m+1 <- next
 // rank's plane 1; one group for all fields
 int sfb_comm_halo(sfb_comm* c, void* const* fields, int nf, size_t plane_bytes, int m, void* stream) {
+  SFB_RANGE();
   if (!c || !fields || nf < 1 || m < 1) return fail(SFB_EINVAL, "bad halo arguments");
   cudaStream_t st = (cudaStream_t)stream;
   if (c->nranks == 1) {
@@ -160,6 +162,7 @@ int sfb_comm_halo(sfb_comm* c, void* const* fields, int nf, size_t plane_bytes, 
 // equal-split all-to-all: block q (bytes_per_peer) of send goes to rank q,
 // block q of recv comes from rank q
 int sfb_comm_alltoall(sfb_comm* c, const void* send, void* recv, size_t bytes_per_peer, void* stream) {
+  SFB_RANGE();
   if (!c || !send || !recv) return fail(SFB_EINVAL, "bad all-to-all arguments");
   cudaStream_t st = (cudaStream_t)stream;
   if (c->nranks == 1)
@@ -178,6 +181,7 @@ int sfb_comm_alltoall(sfb_comm* c, const void* send, void* recv, size_t bytes_pe
 // in-place all-reduce of count fp64 values in device memory: op 0 sum,
 // 1 min, 2 max
 int sfb_comm_allreduce_f64(sfb_comm* c, double* buf, size_t count, int op, void* stream) {
+  SFB_RANGE();
   if (!c || !buf || op < 0 || op > 2) return fail(SFB_EINVAL, "bad all-reduce arguments");
   if (c->nranks == 1) return SFB_OK;
   const ncclRedOp_t o = op == 0 ? ncclSum : (op == 1 ? ncclMin : ncclMax);

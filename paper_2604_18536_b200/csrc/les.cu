@@ -549,6 +549,7 @@ using namespace sfb;
 extern "C" {
 
 int sfb_closure_nut(sfb_plan* p, int kind, double c, double pexp, const void* const* u, void* nut, void* stream) {
+  SFB_RANGE();
   if (!p || !u || !nut) return fail(SFB_EINVAL, "null argument");
   for (int a = 0; a < p->dim; ++a)
     if (!u[a]) return fail(SFB_EINVAL, "null velocity component");
@@ -559,6 +560,7 @@ int sfb_closure_nut(sfb_plan* p, int kind, double c, double pexp, const void* co
 
 int sfb_eddy_stress_divergence(sfb_plan* p, const void* const* u, const void* nut, void* const* out, int accumulate,
                                void* stream) {
+  SFB_RANGE();
   if (!p || !u || !nut || !out) return fail(SFB_EINVAL, "null argument");
   for (int a = 0; a < p->dim; ++a)
     if (!u[a] || !out[a]) return fail(SFB_EINVAL, "null velocity component");
@@ -584,6 +586,7 @@ int sfb_eddy_stress_divergence(sfb_plan* p, const void* const* u, const void* nu
 
 int sfb_closure_pullback(sfb_plan* p, int kind, double c, const void* const* u, const void* nut,
                          const void* const* vbar, void* const* out, void* scratch, void* stream) {
+  SFB_RANGE();
   if (!p || !u || !nut || !vbar || !out || !scratch) return fail(SFB_EINVAL, "null argument");
   if (kind != LES_SMAG) return fail(SFB_ECONFIG, "closure pullback: Smagorinsky only");
   if (p->dim != 3 || !p->all_periodic) return fail(SFB_ECONFIG, "closure pullback: periodic 3D grids only");
@@ -593,6 +596,7 @@ int sfb_closure_pullback(sfb_plan* p, int kind, double c, const void* const* u, 
 }
 
 int sfb_scalar_minmax(sfb_plan* p, const void* f, double* mn, double* mx, void* stream) {
+  SFB_RANGE();
   if (!p || !f || !mn || !mx) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   int nb = p->red_blocks / 2;

@@ -781,6 +781,7 @@ int sfb_solver_destroy(sfb_solver* s) {
 }
 
 int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream) {
+  SFB_RANGE();
   if (!s || !rhs || !out) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   sfb_plan* p = s->plan;
@@ -793,6 +794,7 @@ int sfb_solver_solve(sfb_solver* s, const void* rhs, void* out, void* stream) {
 }
 
 int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, void* stream) {
+  SFB_RANGE();
   if (!s || !u || !p_int) return fail(SFB_EINVAL, "null argument");
   if (s->slab) return fail(SFB_ECONFIG, "sfb_project_solve: slab solvers use the sfb_slab_* sequence");
   for (int a = 0; a < s->plan->dim; ++a)
@@ -804,6 +806,7 @@ int sfb_project_solve(sfb_solver* s, const void* const* u, const void** p_int, v
 }
 
 int sfb_project_finish(sfb_solver* s, void* const* u, void* p_ext, void* stream) {
+  SFB_RANGE();
   if (!s || !u) return fail(SFB_EINVAL, "null argument");
   if (s->slab) return fail(SFB_ECONFIG, "sfb_project_finish: slab solvers use sfb_slab_correct");
   for (int a = 0; a < s->plan->dim; ++a)
@@ -835,6 +838,7 @@ int sfb_project_launches(const sfb_solver* s, int mode) {
 }
 
 int sfb_project(sfb_solver* s, void* const* u, void* p_ext, void* stream) {
+  SFB_RANGE();
   if (!s || !u) return fail(SFB_EINVAL, "null argument");
   for (int a = 0; a < s->plan->dim; ++a)
     if (!u[a]) return fail(SFB_EINVAL, "null velocity component");
@@ -982,6 +986,7 @@ static int slab_correct(sfb_solver* s, void* const* u, void* p_ext, cudaStream_t
 extern "C" {
 
 int sfb_slab_r2c(sfb_solver* s, void* const* u, void* stream) {
+  SFB_RANGE();
   if (!s || !s->slab || !u || !u[0] || !u[1] || !u[2]) return fail(SFB_EINVAL, "bad slab call");
   return s->plan->dtype == SFB_F64 ? slab_r2c<double>(s, u, (cudaStream_t)stream)
                                    : slab_r2c<float>(s, u, (cudaStream_t)stream);
@@ -993,6 +998,7 @@ int sfb_slab_max_chunks(const sfb_solver* s) {
 }
 
 int sfb_slab_axis1(sfb_solver* s, int chunk, int nchunks, int inverse, void* stream) {
+  SFB_RANGE();
   if (!s || !s->slab || nchunks < 1 || chunk < 0 || chunk >= nchunks) return fail(SFB_EINVAL, "bad slab call");
   return s->plan->dtype == SFB_F64
              ? fft_slab_axis1<double>(s->fft, s->cbuf, s->xbuf, s->nranks, chunk, nchunks, inverse != 0,
@@ -1002,6 +1008,7 @@ int sfb_slab_axis1(sfb_solver* s, int chunk, int nchunks, int inverse, void* str
 }
 
 int sfb_slab_axis0(sfb_solver* s, int chunk, int nchunks, void* stream) {
+  SFB_RANGE();
   if (!s || !s->slab || nchunks < 1 || chunk < 0 || chunk >= nchunks) return fail(SFB_EINVAL, "bad slab call");
   const int c = s->plan->n[1] / s->nranks;
   return s->plan->dtype == SFB_F64
@@ -1010,12 +1017,14 @@ int sfb_slab_axis0(sfb_solver* s, int chunk, int nchunks, void* stream) {
 }
 
 int sfb_slab_c2r(sfb_solver* s, void* stream) {
+  SFB_RANGE();
   if (!s || !s->slab) return fail(SFB_EINVAL, "bad slab call");
   return s->plan->dtype == SFB_F64 ? fft_slab_c2r<double>(s->fft, s->cbuf, slab_local<double>(s), (cudaStream_t)stream)
                                    : fft_slab_c2r<float>(s->fft, s->cbuf, slab_local<float>(s), (cudaStream_t)stream);
 }
 
 int sfb_slab_correct(sfb_solver* s, void* const* u, void* p_ext, void* stream) {
+  SFB_RANGE();
   if (!s || !s->slab || !u || !u[0] || !u[1] || !u[2]) return fail(SFB_EINVAL, "bad slab call");
   return s->plan->dtype == SFB_F64 ? slab_correct<double>(s, u, p_ext, (cudaStream_t)stream)
                                    : slab_correct<float>(s, u, p_ext, (cudaStream_t)stream);

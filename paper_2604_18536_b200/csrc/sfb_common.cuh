@@ -1,6 +1,8 @@
 // Shared definitions for the stagflow_b200 kernels (sm_100a).
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -186,6 +188,17 @@ Box int_box(const Geo<T>& G) {
   }
   return b;
 }
+
+// NVTX range over one C-ABI call (tracing): the host span in which
+// the call enqueues its kernels, named after the entry point; free when no
+// tool is attached (NVTX3 is header-only)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
+#define SFB_RANGE() ::sfb::NvtxScope sfb_nvtx_scope_(__func__)
 
 }  // namespace sfb
 

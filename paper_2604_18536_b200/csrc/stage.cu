@@ -572,6 +572,7 @@ static int run_stage(sfb_plan* p, const sfb_stage_args* a, cudaStream_t st) {
 using namespace sfb;
 
 extern "C" int sfb_rk_stage(sfb_plan* p, const sfb_stage_args* a, void* stream) {
+  SFB_RANGE();
   if (!p || !a || !a->y[0]) return fail(SFB_EINVAL, "null argument");
   if (a->nu < 0) return fail(SFB_EINVAL, "viscosity must be nonnegative");
   return SFB_TYPED(p, run_stage<T>(p, a, (cudaStream_t)stream));

@@ -149,6 +149,7 @@ using namespace sfb;
 extern "C" {
 
 int sfb_plane_sums(sfb_plan* p, int wall_axis, const void* const* u, int mode, double* out, void* stream) {
+  SFB_RANGE();
   if (!p || !u || !out) return fail(SFB_EINVAL, "null argument");
   if (wall_axis < 0 || wall_axis >= p->dim) return fail(SFB_EINVAL, "wall axis out of range");
   if (mode != 0 && mode != 1) return fail(SFB_EINVAL, "unknown plane-sum mode");
@@ -158,6 +159,7 @@ int sfb_plane_sums(sfb_plan* p, int wall_axis, const void* const* u, int mode, d
 }
 
 int sfb_sub_plane_mean(sfb_plan* p, int wall_axis, void* const* u, const double* mean, void* stream) {
+  SFB_RANGE();
   if (!p || !u || !mean) return fail(SFB_EINVAL, "null argument");
   if (wall_axis < 0 || wall_axis >= p->dim) return fail(SFB_EINVAL, "wall axis out of range");
   cudaStream_t st = (cudaStream_t)stream;

@@ -501,21 +501,25 @@ using namespace sfb;
 extern "C" {
 
 int sfb_fill_ghosts_velocity(sfb_plan* p, void* const* u, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u)) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, launch_planes<T>(geo<T>(p), mv<T>(p, u), p->dim, 0, (cudaStream_t)stream));
 }
 
 int sfb_fill_ghosts_scalar(sfb_plan* p, void* f, void* stream) {
+  SFB_RANGE();
   if (!p || !f) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, launch_planes<T>(geo<T>(p), MV<T>{{(T*)f, nullptr, nullptr}}, 1, 1, (cudaStream_t)stream));
 }
 
 int sfb_fold_ghosts_velocity(sfb_plan* p, void* const* u, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u)) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, launch_fold<T>(geo<T>(p), mv<T>(p, u), p->dim, false, (cudaStream_t)stream));
 }
 
 int sfb_fold_ghosts_scalar(sfb_plan* p, void* f, void* stream) {
+  SFB_RANGE();
   if (!p || !f) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, launch_fold<T>(geo<T>(p), MV<T>{{(T*)f, nullptr, nullptr}}, 1, true, (cudaStream_t)stream));
 }
@@ -531,6 +535,7 @@ int sfb_zero_ghosts_scalar(sfb_plan* p, void* f, void* stream) {
 }
 
 int sfb_divergence(sfb_plan* p, const void* const* u, void* out, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !out) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   return SFB_TYPED(p, ([&]() {
@@ -543,6 +548,7 @@ int sfb_divergence(sfb_plan* p, const void* const* u, void* out, void* stream) {
 }
 
 int sfb_pressure_gradient(sfb_plan* p, const void* pf, void* const* out, void* stream) {
+  SFB_RANGE();
   if (!p || !pf || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   return SFB_TYPED(p, ([&]() {
@@ -555,11 +561,13 @@ int sfb_pressure_gradient(sfb_plan* p, const void* pf, void* const* out, void* s
 }
 
 int sfb_convection(sfb_plan* p, const void* const* u, void* const* out, int accumulate, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, do_rhs<T>(p, u, out, 0.0, nullptr, nullptr, 1 | (accumulate ? 4 : 0), (cudaStream_t)stream));
 }
 
 int sfb_diffusion(sfb_plan* p, const void* const* u, double nu, void* const* out, int accumulate, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
   if (nu < 0) return fail(SFB_EINVAL, "viscosity must be nonnegative");
   return SFB_TYPED(p, do_rhs<T>(p, u, out, nu, nullptr, nullptr, 2 | (accumulate ? 4 : 0), (cudaStream_t)stream));
@@ -567,6 +575,7 @@ int sfb_diffusion(sfb_plan* p, const void* const* u, double nu, void* const* out
 
 int sfb_momentum_rhs(sfb_plan* p, const void* const* u, double nu, const double* force, const void* const* force_field,
                      void* const* out, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
   if (nu < 0) return fail(SFB_EINVAL, "viscosity must be nonnegative");
   int flags = 1 | (nu != 0.0 ? 2 : 0);
@@ -575,6 +584,7 @@ int sfb_momentum_rhs(sfb_plan* p, const void* const* u, double nu, const double*
 
 int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, const void* const* k,
                 const double* coef, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, dst) || nk < 0 || nk > SFB_MAX_K) return fail(SFB_EINVAL, "bad combine args");
   if (base && !base[0]) base = nullptr;  // all-NULL base: zero
   if (base && !ptrs_ok(p, base)) return fail(SFB_EINVAL, "bad combine base");
@@ -595,6 +605,7 @@ int sfb_combine(sfb_plan* p, void* const* dst, const void* const* base, int nk, 
 }
 
 int sfb_wray_update(sfb_plan* p, void* const* u, void* const* fnew, void* const* fold, double g, double z, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, fnew)) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   int has_fold = fold && fold[0];
@@ -609,6 +620,7 @@ int sfb_wray_update(sfb_plan* p, void* const* u, void* const* fnew, void* const*
 }
 
 int sfb_weighted_scale(sfb_plan* p, const void* const* u, void* const* out, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, out)) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   return SFB_TYPED(p, ([&]() {
@@ -621,6 +633,7 @@ int sfb_weighted_scale(sfb_plan* p, const void* const* u, void* const* out, void
 }
 
 int sfb_kinetic_energy(sfb_plan* p, const void* const* u, double* out, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !out) return fail(SFB_EINVAL, "null argument");
   double s = 0;
   int rc = SFB_TYPED(p, reduce<T>(p, cv<T>(p, u), cv<T>(p, u), 0, &s, (cudaStream_t)stream));
@@ -630,11 +643,13 @@ int sfb_kinetic_energy(sfb_plan* p, const void* const* u, double* out, void* str
 }
 
 int sfb_weighted_inner(sfb_plan* p, const void* const* u, const void* const* v, double* out, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !ptrs_ok(p, v) || !out) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, reduce<T>(p, cv<T>(p, u), cv<T>(p, v), 0, out, (cudaStream_t)stream));
 }
 
 int sfb_cfl_conv(sfb_plan* p, const void* const* u, double* out, void* stream) {
+  SFB_RANGE();
   if (!p || !ptrs_ok(p, u) || !out) return fail(SFB_EINVAL, "null argument");
   return SFB_TYPED(p, reduce<T>(p, cv<T>(p, u), cv<T>(p, u), 1, out, (cudaStream_t)stream));
 }

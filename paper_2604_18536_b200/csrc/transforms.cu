@@ -160,12 +160,14 @@ int sfb_fft_destroy(sfb_fft* f) {
 int sfb_fft_uses_own(const sfb_fft* f) { return f && f->F.enabled ? 1 : 0; }
 
 int sfb_rfftn(sfb_fft* f, const void* in, void* out, void* stream) {
+  SFB_RANGE();
   if (!f || !in || !out) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   return f->f64 ? run_forward<double>(f, in, out, st) : run_forward<float>(f, in, out, st);
 }
 
 int sfb_irfftn(sfb_fft* f, const void* in, void* out, void* stream) {
+  SFB_RANGE();
   if (!f || !in || !out) return fail(SFB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   return f->f64 ? run_inverse<double>(f, in, out, st) : run_inverse<float>(f, in, out, st);
