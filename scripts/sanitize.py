@@ -2,7 +2,8 @@
 every native path -- RK4 steps through rk_step and run_steps (fused stage
 kernels, on-the-fly and deferred projections, register FFT with the tiled
 spectrum), the VJP (tape + backward), the channel (FFT x tridiagonal) and CG
-solvers, an LES closure, and the slab code path at P = 1.
+solvers, an LES closure, HostEnsemble's copy streams and the rhs pullback's
+TMA ring on a ragged grid.
     compute-sanitizer --tool memcheck python scripts/sanitize.py"""
 import os
 import sys
@@ -34,5 +35,22 @@ setup = P.Setup(g, P.BoundarySpec.channel(dim=3, wall_axis=1), nu=1 / 180, force
                 method="ssp33", solver_max_iter=5000)
 st = setup.new_state(u0=cases.channel_ic(g, 1 / 180))
 P.rk_step(st, 1e-3, P.SSP33, setup.solver, setup)
+torch.cuda.synchronize()
+# HostEnsemble: two pinned-host members, copies on their own streams
+g = cases.periodic_box(16)
+setup = P.Setup(g, P.BoundarySpec.all_periodic(3), nu=1 / 1600, solver="spectral", method="rk4")
+host = []
+for seed in (1, 2):
+    u = cases.isotropic(g, setup.solver, seed=seed)
+    host.append([c.cpu().pin_memory() for c in u.u])
+ens = P.HostEnsemble(setup, host, chunks=4)
+ens.run(2, 1e-3)
+ens.synchronize()
+# rhs pullback on a ragged stretched grid (TMA ring with out-of-bounds boxes)
+g = P.Grid(tuple(P.tanh_grid(0.0, 1.0 + 0.2 * a, n, 1.3) for a, n in enumerate((9, 13, 37))), (True,) * 3)
+rng = np.random.default_rng(0)
+vb = P.VelocityField(g, [rng.standard_normal(g.ext_shape) for _ in range(3)])
+uu = P.VelocityField(g, [rng.standard_normal(g.ext_shape) for _ in range(3)])
+P.rhs_pullback(vb, uu, 0.01, P.BoundarySpec.all_periodic(3))
 torch.cuda.synchronize()
 print("sanitize target ok")
