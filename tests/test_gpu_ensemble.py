@@ -38,11 +38,13 @@ def _members(P, pg, og, n, seed):
     return out, host, solve
 
 
-@pytest.mark.parametrize("n_members,method", [(1, "rk4"), (2, "rk4"), (3, "rk4"), (2, "ssp33"), (2, "wray3")])
-def test_host_ensemble_matches_chained_steps(P, n_members, method):
+@pytest.mark.parametrize("n_members,method,dtype", [(1, "rk4", np.float64), (2, "rk4", np.float64),
+                                                    (3, "rk4", np.float64), (2, "ssp33", np.float64),
+                                                    (2, "wray3", np.float64), (2, "rk4", np.float32)])
+def test_host_ensemble_matches_chained_steps(P, n_members, method, dtype):
     import torch
 
-    pg, og = grids(P, cube_bounds(16), (True,) * 3)
+    pg, og = grids(P, cube_bounds(16), (True,) * 3, dtype)
     bcs = P.BoundarySpec.all_periodic(3)
     setup = P.Setup(pg, bcs, nu=0.05, force=(0.1, 0.0, 0.0), solver="spectral", method=method)
     us, host, _ = _members(P, pg, og, n_members, 7)
